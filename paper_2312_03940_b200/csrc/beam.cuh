@@ -1,0 +1,383 @@
+// Warp-level greedy beam search, candidate sorting and RobustPrune.
+//
+// One warp owns one query.  The semantics are those of the reference
+// (_kernels.py:125-212): seed with the start set, repeatedly expand the
+// closest unvisited beam entry, insert every neighbour not yet in the beam,
+// keep the best L by (dist, id), stop when every beam entry is visited.
+//
+// Two reorganisations keep the output bit-identical while doing less work
+// (SURVEY.md §0.4, §0.11):
+//  * the neighbours of one expansion are inserted as one batch (a merge of up
+//    to 32 sorted candidates into the sorted beam).  Top-L of a union is
+//    associative, so the batch merge equals sequential inserts;
+//  * a node whose distance was already evaluated is not evaluated again.  The
+//    reference re-evaluates evicted / rejected nodes, but their key is above
+//    the beam's L-th key, which never increases once the beam is full, so they
+//    can never re-enter.  The "seen" table is lossy (direct-mapped, ids may be
+//    overwritten), which only costs re-evaluations; a re-evaluated node that
+//    is still in the beam is recognised by its identical key and dropped.
+//    Start points never need re-evaluation after seeding, so a bitmap of the
+//    start set skips them exactly.
+//
+// Output rule (member queries): sorted(visited U unvisited beam) is the
+// final beam followed by the evicted visited entries, so the first kk
+// non-self entries are the beam minus the query itself plus, when the query
+// sits in a full beam and kk == L, the best evicted visited entry.
+#pragma once
+
+#include "common.cuh"
+
+namespace pk {
+
+struct BeamSmem {
+    double* bd;       // [Lcap] squared distances, (dist,id)-sorted
+    unsigned* bi;     // [Lcap] ids | PK_VIS
+    unsigned* hash;   // [hmask+1] lossy seen table, 0xffffffff = empty
+    unsigned hmask;
+    int* spos;        // [32] scratch: sorted insert positions
+    unsigned* cbuf;   // [32] scratch: compacted candidate ids
+};
+
+struct SearchParams {
+    const float* X;          // (n, dp)
+    int dp;
+    const int* adj;          // (n, R)
+    int R;
+    const int* deg;          // (n,)
+    const int* starts;       // (s,)
+    int s;
+    const unsigned* start_bm;  // bitmap of the start set (may be null)
+};
+
+template <class Dist>
+struct WarpBeam {
+    BeamSmem sm;
+    int L;
+    int bl;        // beam length (warp-uniform)
+    int cursor;    // every entry below cursor is visited
+    double ev_d;   // best evicted visited entry (per-lane running min)
+    unsigned ev_i;
+    // optional visit log (build)
+    unsigned* vlog_i;
+    double* vlog_d;
+    int vcap;
+    int vl;
+    unsigned* err;
+    long long evals;  // distance evaluations (lane 0 count)
+
+    __device__ void init(const BeamSmem& s_, int L_, unsigned* vi, double* vd, int vcap_, unsigned* err_) {
+        sm = s_;
+        L = L_;
+        bl = 0;
+        cursor = 0;
+        ev_d = __longlong_as_double(0x7ff0000000000000LL);
+        ev_i = 0xffffffffu;
+        vlog_i = vi;
+        vlog_d = vd;
+        vcap = vcap_;
+        vl = 0;
+        err = err_;
+        evals = 0;
+        for (unsigned h = lane_id(); h <= sm.hmask; h += 32) sm.hash[h] = 0xffffffffu;
+        __syncwarp();
+    }
+
+    // Merge the candidates held by lanes with `valid` into the beam.
+    __device__ void merge(double cd, unsigned cid, bool valid) {
+        const int lane = lane_id();
+        double* bd = sm.bd;
+        unsigned* bi = sm.bi;
+        int pos = 0;
+        bool keep = valid;
+        if (valid) {
+            int lo = 0, hi = bl;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (key_lt(bd[mid], bi[mid] & PK_IDMASK, cd, cid)) lo = mid + 1;
+                else hi = mid;
+            }
+            pos = lo;
+            if (pos < bl && bd[pos] == cd && (bi[pos] & PK_IDMASK) == cid) keep = false;
+        }
+        unsigned vb = __ballot_sync(PK_FULL, keep);
+        if (!vb) return;
+        // equal keys inside the batch (duplicate start ids): keep the lowest lane;
+        // then rank every survivor among the survivors
+        int rank = 0;
+        bool dupl = false;
+        for (unsigned b = vb; b; b &= b - 1) {
+            int j = __ffs(b) - 1;
+            double dj = __shfl_sync(PK_FULL, cd, j);
+            unsigned ij = __shfl_sync(PK_FULL, cid, j);
+            if (j < lane && key_eq(dj, ij, cd, cid)) dupl = true;
+        }
+        unsigned fb = __ballot_sync(PK_FULL, keep && !dupl);
+        keep = keep && !dupl;
+        for (unsigned b = fb; b; b &= b - 1) {
+            int j = __ffs(b) - 1;
+            double dj = __shfl_sync(PK_FULL, cd, j);
+            unsigned ij = __shfl_sync(PK_FULL, cid, j);
+            if (key_lt(dj, ij, cd, cid)) ++rank;
+        }
+        const int c = __popc(fb);
+        if (keep) sm.spos[rank] = pos;
+        __syncwarp();
+        const int minpos = sm.spos[0];
+        const int nbl = min(L, bl + c);
+        // shift the tail [minpos, bl) right, top-down in chunks of 32
+        for (int top = bl - 1; top >= minpos; top -= 32) {
+            const int e = top - lane;
+            const bool act = e >= minpos;
+            double de = 0.0;
+            unsigned ie = 0;
+            int ne = 0;
+            if (act) {
+                de = bd[e];
+                ie = bi[e];
+                int lo = 0, hi = c;
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (sm.spos[mid] <= e) lo = mid + 1;
+                    else hi = mid;
+                }
+                ne = e + lo;
+            }
+            __syncwarp();
+            if (act) {
+                if (ne < L) {
+                    bd[ne] = de;
+                    bi[ne] = ie;
+                } else if ((ie & PK_VIS) && key_lt(de, ie & PK_IDMASK, ev_d, ev_i)) {
+                    ev_d = de;
+                    ev_i = ie & PK_IDMASK;
+                }
+            }
+            __syncwarp();
+        }
+        const int np = pos + rank;
+        if (keep && np < L) {
+            bd[np] = cd;
+            bi[np] = cid;
+        }
+        int mn = (keep && np < L) ? np : 0x7fffffff;
+#pragma unroll
+        for (int s = 16; s; s >>= 1) mn = min(mn, __shfl_xor_sync(PK_FULL, mn, s));
+        if (mn < cursor) cursor = mn;
+        bl = nbl;
+        __syncwarp();
+    }
+
+    // Seed with the start set (batch insert of ceil(s/32) chunks).
+    template <class D>
+    __device__ void seed(const SearchParams& P, const D& dist) {
+        const int lane = lane_id();
+        for (int b = 0; b < P.s; b += 32) {
+            const int cnt = min(32, P.s - b);
+            unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
+            if (!P.start_bm && lane < cnt) sm.hash[seen_slot(id, sm.hmask)] = id;
+            double dd = dist.eval(P.X, (int)id, cnt);
+            if (lane == 0) evals += cnt;
+            merge(dd, id, lane < cnt);
+        }
+    }
+
+    // First unvisited beam position at or after the cursor, -1 if none.
+    __device__ int next_unvisited() {
+        const int lane = lane_id();
+        for (int base = cursor; base < bl; base += 32) {
+            int e = base + lane;
+            bool unv = e < bl && !(sm.bi[e] & PK_VIS);
+            unsigned b = __ballot_sync(PK_FULL, unv);
+            if (b) return base + __ffs(b) - 1;
+        }
+        return -1;
+    }
+
+    // Run the walk to completion.
+    template <class D>
+    __device__ void walk(const SearchParams& P, const D& dist) {
+        const int lane = lane_id();
+        for (;;) {
+            const int pos = next_unvisited();
+            if (pos < 0) break;
+            const unsigned p = sm.bi[pos] & PK_IDMASK;
+            const double pd = sm.bd[pos];
+            __syncwarp();
+            if (lane == 0) {
+                sm.bi[pos] = p | PK_VIS;
+                if (vlog_i) {
+                    if (vl < vcap) {
+                        vlog_i[vl] = p;
+                        vlog_d[vl] = pd;
+                    } else {
+                        atomicOr(err, ERR_VISIT_OVERFLOW);
+                    }
+                }
+            }
+            ++vl;
+            cursor = pos + 1;
+            __syncwarp();
+            const int nd = __ldg(P.deg + p);
+            const int* row = P.adj + (size_t)p * P.R;
+            for (int e0 = 0; e0 < nd; e0 += 32) {
+                int w = e0 + lane < nd ? __ldg(row + e0 + lane) : -1;
+                bool cand = w >= 0;
+                if (cand && P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u)) cand = false;
+                if (cand) {
+                    unsigned sl = seen_slot((unsigned)w, sm.hmask);
+                    if (sm.hash[sl] == (unsigned)w) cand = false;
+                    else sm.hash[sl] = (unsigned)w;
+                }
+                unsigned b = __ballot_sync(PK_FULL, cand);
+                const int c = __popc(b);
+                if (!c) continue;
+                if (cand) sm.cbuf[warp_excl_prefix(b)] = (unsigned)w;
+                __syncwarp();
+                unsigned cid = lane < c ? sm.cbuf[lane] : 0u;
+                __syncwarp();
+                double dd = dist.eval(P.X, (int)cid, c);
+                if (lane == 0) evals += c;
+                merge(dd, cid, lane < c);
+            }
+        }
+    }
+
+    // Member-query output: first kk entries of the beam without `self`, then
+    // the best evicted visited entry if still short.  Returns the count.
+    __device__ int emit(unsigned self, int kk, long long* out_ids, double* out_d) {
+        const int lane = lane_id();
+        int got = 0;
+        for (int base = 0; base < bl && got < kk; base += 32) {
+            int e = base + lane;
+            unsigned id = e < bl ? (sm.bi[e] & PK_IDMASK) : self;
+            bool ok = e < bl && id != self;
+            unsigned b = __ballot_sync(PK_FULL, ok);
+            int o = got + warp_excl_prefix(b);
+            if (ok && o < kk) {
+                out_ids[o] = id;
+                out_d[o] = sm.bd[e];
+            }
+            got += __popc(b);
+        }
+        got = min(got, kk);
+        // warp-wide best evicted visited
+        double bd_ = ev_d;
+        unsigned bi_ = ev_i;
+#pragma unroll
+        for (int s = 16; s; s >>= 1) {
+            double od = __shfl_xor_sync(PK_FULL, bd_, s);
+            unsigned oi = __shfl_xor_sync(PK_FULL, bi_, s);
+            if (key_lt(od, oi, bd_, bi_)) { bd_ = od; bi_ = oi; }
+        }
+        if (got < kk && bi_ != 0xffffffffu && bi_ != self) {
+            if (lane == 0) {
+                out_ids[got] = bi_;
+                out_d[got] = bd_;
+            }
+            ++got;
+        }
+        return got;
+    }
+};
+
+// ---- warp bitonic sort of (dist, id) keys in shared memory ----------------------
+// P must be a power of two; entries beyond the live count must hold (+inf, ~0).
+__device__ __forceinline__ void warp_sort(double* kd, unsigned* ki, int P) {
+    const int lane = lane_id();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                int x = i ^ j;
+                if (x > i) {
+                    double a = kd[i], b = kd[x];
+                    unsigned ia = ki[i], ib = ki[x];
+                    bool asc = (i & k) == 0;
+                    bool gt = key_lt(b, ib, a, ia);
+                    if (gt == asc) {
+                        kd[i] = b; kd[x] = a;
+                        ki[i] = ib; ki[x] = ia;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Drop duplicate keys (same id => same dist) and `self`, in place; returns count.
+__device__ __forceinline__ int warp_unique(double* kd, unsigned* ki, int c, unsigned self) {
+    const int lane = lane_id();
+    int out = 0;
+    for (int base = 0; base < c; base += 32) {
+        int i = base + lane;
+        double d = 0.0;
+        unsigned id = self;
+        bool keep = false;
+        if (i < c) {
+            d = kd[i];
+            id = ki[i];
+            keep = id != self && !(i > 0 && ki[i - 1] == id && kd[i - 1] == d);
+        }
+        unsigned b = __ballot_sync(PK_FULL, keep);
+        __syncwarp();
+        if (keep) {
+            int o = out + warp_excl_prefix(b);
+            kd[o] = d;
+            ki[o] = id;
+        }
+        out += __popc(b);
+        __syncwarp();
+    }
+    return out;
+}
+
+// RobustPrune over (dist,id)-sorted candidates kd/ki[0..c) (_kernels.py:290-315):
+// take the closest alive candidate p*, kill every later u with
+// alpha2 * d(p*, u) <= d(p, u); stop after R picks.  `alive` is c bytes of
+// scratch.  Writes the picks to out[0..sel) and returns sel.
+template <class MakeDist>
+__device__ int warp_prune(const float* __restrict__ X, const double* kd, const unsigned* ki, int c,
+                          double alpha2, int R, unsigned char* alive, unsigned* cbuf, int* out,
+                          const MakeDist& make, long long* evals) {
+    const int lane = lane_id();
+    for (int i = lane; i < c; i += 32) alive[i] = 1;
+    __syncwarp();
+    int sel = 0;
+    int t = 0;
+    while (sel < R) {
+        // next alive position >= t
+        int nt = -1;
+        for (int base = t; base < c; base += 32) {
+            int i = base + lane;
+            unsigned b = __ballot_sync(PK_FULL, i < c && alive[i]);
+            if (b) { nt = base + __ffs(b) - 1; break; }
+        }
+        if (nt < 0) break;
+        t = nt;
+        const unsigned ps = ki[t];
+        if (lane == 0) out[sel] = (int)ps;
+        ++sel;
+        if (sel >= R) break;
+        auto dist = make(ps);
+        for (int base = t + 1; base < c; base += 32) {
+            int u = base + lane;
+            bool a = u < c && alive[u];
+            unsigned b = __ballot_sync(PK_FULL, a);
+            const int cnt = __popc(b);
+            if (!cnt) continue;
+            if (a) cbuf[warp_excl_prefix(b)] = (unsigned)u;
+            __syncwarp();
+            unsigned uu = lane < cnt ? cbuf[lane] : 0u;
+            __syncwarp();
+            double duv = dist.eval(X, (int)(lane < cnt ? ki[uu] : ki[t]), cnt);
+            if (lane == 0) *evals += cnt;
+            if (lane < cnt && alpha2 * duv <= kd[uu]) alive[uu] = 0;
+            __syncwarp();
+        }
+        ++t;
+    }
+    __syncwarp();
+    return sel;
+}
+
+}  // namespace pk

@@ -1,0 +1,192 @@
+// Shared device helpers for the peakann-b200 kernels (sm_100a).
+//
+// Conventions (mirroring /root/reference/pkg/src/peakann/_kernels.py:1-11):
+//  * coordinates are float32, stored row-major with rows padded to `dp`
+//    floats (dp % 4 == 0, padding is zero, which adds exactly +0.0 to any
+//    squared distance);
+//  * squared distances are float64 and every ordering is the key
+//    (squared distance, id), compared lexicographically;
+//  * ids are int32 on device (n < 2^31), int64 at the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PK_FULL 0xffffffffu
+#define PK_VIS 0x80000000u   // visited flag, stored in bit 31 of a beam id
+#define PK_IDMASK 0x7fffffffu
+
+namespace pk {
+
+constexpr int kWarp = 32;
+
+// ---- error reporting -------------------------------------------------------
+// Device-side sticky error word (bit flags), read back by the host driver.
+enum DeviceError : unsigned {
+    ERR_VISIT_OVERFLOW = 1u,   // build visit log exceeded its capacity
+    ERR_CAND_OVERFLOW = 2u,    // candidate buffer exceeded its capacity
+    ERR_BEAM_CAPACITY = 4u,    // L larger than the kernel's beam capacity
+};
+
+// ---- keys --------------------------------------------------------------------
+// Squared distances are >= 0, so their IEEE bit patterns order like the values.
+__device__ __forceinline__ unsigned long long dbits(double d) {
+    return (unsigned long long)__double_as_longlong(d);
+}
+__device__ __forceinline__ bool key_lt(double da, unsigned ia, double db, unsigned ib) {
+    return da < db || (da == db && ia < ib);
+}
+__device__ __forceinline__ bool key_eq(double da, unsigned ia, double db, unsigned ib) {
+    return da == db && ia == ib;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ float4 ldg4(const float* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// hash for the per-query "seen" table (lossy, direct-mapped)
+__device__ __forceinline__ unsigned seen_slot(unsigned id, unsigned mask) {
+    return (id * 2654435761u >> 7) & mask;
+}
+
+// ---- distance policies ---------------------------------------------------------
+//
+// Both policies return, for lane i < c, the squared distance between the query
+// and candidate row `cid` (the id held by lane i), as a double that is
+// bit-identical to the reference's sequential float64 accumulation
+// (_kernels.py:21-28):
+//
+//  * Seq64: each lane walks its candidate's coordinates t = 0..d-1 in order
+//    with float64 fused multiply-adds.  (f64(a)-f64(b)) is exact and its square
+//    fits 50 bits, so fma(diff, diff, acc) == acc + diff*diff: the result is the
+//    reference's value for any float32 data.
+//  * Exact32: lanes split the dimensions and reduce float32 partial sums across
+//    the warp.  Only used when the point set is integer-valued with
+//    d * (2*max|x|)^2 < 2^24 (checked on upload): every partial sum is then an
+//    integer below 2^24, so each float32 operation is exact in any order and
+//    equals the float64 reference bit for bit.
+//
+// Query vectors: member queries read float32 rows (converted exactly to
+// float64, as `data[i].astype(np.float64)` does); free vector queries pass
+// float64 coordinates and always use Seq64.
+
+struct Seq64Member {
+    const float* q;  // query row (dp floats), global
+    int dp;
+    __device__ __forceinline__ double eval_one(const float* __restrict__ X, int id) const {
+        const float* r = X + (size_t)id * dp;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int t = 0; t < dp; t += 4) {
+            float4 x = ldg4(r + t);
+            float4 y = ldg4(q + t);
+            double a = (double)y.x - (double)x.x; acc = fma(a, a, acc);
+            double b = (double)y.y - (double)x.y; acc = fma(b, b, acc);
+            double c = (double)y.z - (double)x.z; acc = fma(c, c, acc);
+            double e = (double)y.w - (double)x.w; acc = fma(e, e, acc);
+        }
+        return acc;
+    }
+    // lane i < c: distance to its own cid
+    __device__ __forceinline__ double eval(const float* __restrict__ X, int cid, int c) const {
+        return lane_id() < c ? eval_one(X, cid) : 0.0;
+    }
+};
+
+struct Seq64Vector {
+    const double* q;  // float64 query (dp entries, zero padded), global
+    int dp;
+    __device__ __forceinline__ double eval_one(const float* __restrict__ X, int id) const {
+        const float* r = X + (size_t)id * dp;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int t = 0; t < dp; t += 4) {
+            float4 x = ldg4(r + t);
+            double a = __ldg(q + t) - (double)x.x; acc = fma(a, a, acc);
+            double b = __ldg(q + t + 1) - (double)x.y; acc = fma(b, b, acc);
+            double c = __ldg(q + t + 2) - (double)x.z; acc = fma(c, c, acc);
+            double e = __ldg(q + t + 3) - (double)x.w; acc = fma(e, e, acc);
+        }
+        return acc;
+    }
+    __device__ __forceinline__ double eval(const float* __restrict__ X, int cid, int c) const {
+        return lane_id() < c ? eval_one(X, cid) : 0.0;
+    }
+};
+
+// Exact32: QV float4 query slices per lane cover dims [4*lane + 128*v].
+template <int QV>
+struct Exact32 {
+    float4 q[QV];
+    int dp;
+
+    __device__ __forceinline__ void load(const float* qrow, int dp_) {
+        dp = dp_;
+        const int lane = lane_id();
+#pragma unroll
+        for (int v = 0; v < QV; ++v) {
+            int col = 4 * lane + 128 * v;
+            q[v] = col < dp ? ldg4(qrow + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+
+    __device__ __forceinline__ float partial(const float* __restrict__ X, int id) const {
+        const float* r = X + (size_t)id * dp;
+        const int lane = lane_id();
+        float acc = 0.f;
+#pragma unroll
+        for (int v = 0; v < QV; ++v) {
+            int col = 4 * lane + 128 * v;
+            if (col < dp) {
+                float4 x = ldg4(r + col);
+                float a = q[v].x - x.x, b = q[v].y - x.y, c = q[v].z - x.z, e = q[v].w - x.w;
+                acc = fmaf(a, a, acc);
+                acc = fmaf(b, b, acc);
+                acc = fmaf(c, c, acc);
+                acc = fmaf(e, e, acc);
+            }
+        }
+        return acc;
+    }
+
+    // Groups of 8 candidates: 8 independent row loads in flight, then a
+    // transposed butterfly (3 halving stages + 2 plain stages) leaves the sum of
+    // candidate j in lanes 4j..4j+3.
+    __device__ __forceinline__ double eval(const float* __restrict__ X, int cid, int c) const {
+        const int lane = lane_id();
+        double mine = 0.0;
+        for (int g = 0; g < c; g += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int id = __shfl_sync(PK_FULL, cid, (g + j) & 31);
+                v[j] = (g + j < c) ? partial(X, id) : 0.f;
+            }
+#pragma unroll
+            for (int s = 16, h = 4; s >= 4; s >>= 1, h >>= 1) {
+                const bool up = lane & s;
+#pragma unroll
+                for (int j = 0; j < h; ++j) {
+                    float send = up ? v[j] : v[j + h];
+                    float keep = up ? v[j + h] : v[j];
+                    v[j] = keep + __shfl_xor_sync(PK_FULL, send, s);
+                }
+            }
+            v[0] += __shfl_xor_sync(PK_FULL, v[0], 2);
+            v[0] += __shfl_xor_sync(PK_FULL, v[0], 1);
+            // candidate index held by this lane: bits (4,3,2) of lane
+            float got = __shfl_sync(PK_FULL, v[0], ((lane - g) & 7) << 2);
+            if (lane >= g && lane < g + 8 && lane < c) mine = (double)got;
+        }
+        return mine;
+    }
+};
+
+// ---- warp utilities --------------------------------------------------------------
+__device__ __forceinline__ int warp_excl_prefix(unsigned ballot) {
+    return __popc(ballot & ((1u << lane_id()) - 1u));
+}
+
+}  // namespace pk
