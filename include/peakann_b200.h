@@ -1,0 +1,184 @@
+/*
+ * peakann_b200 -- C ABI of the B200-native density-peaks hot path.
+ *
+ * The reference package's de-facto FFI for this path is its numba kernel
+ * module, /root/reference/pkg/src/peakann/_kernels.py: free functions over
+ * plain arrays (float32 points, int32 adjacency, int64 ids, float64 squared
+ * distances).  Each entry point below replaces one of those functions (or
+ * one numpy stage of the Python layer) and names the reference interface it
+ * stands in for.  All pointers are DEVICE pointers (caller-owned; nothing is
+ * retained after return) unless marked "host"; every call is enqueued on the
+ * given cudaStream_t (passed as void*) and returns 0 on success or a nonzero
+ * code, with a message from pk_last_error().
+ *
+ * Point layout: row-major float32 (n, dp) with dp = d rounded up to a
+ * multiple of 4 and zero padding (adds exactly +0.0 to squared distances).
+ * `mode` selects the distance policy: PK_MODE_SEQ64 (per-lane sequential
+ * float64 in index order -- bit-identical to _kernels.py:21-38 for any data)
+ * or PK_MODE_EXACT32 (warp-split float32, legal only when pk_check_exact32
+ * proved every partial sum is an exactly representable integer).
+ */
+#ifndef PEAKANN_B200_H
+#define PEAKANN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PK_MODE_SEQ64 0
+#define PK_MODE_EXACT32 1
+
+#define PK_DENSITY_KTH 0
+#define PK_DENSITY_KTH_NORMALIZED 1
+#define PK_DENSITY_EXP_SUM 2
+#define PK_DENSITY_SUM_EXP 3
+#define PK_DENSITY_SUM 4
+
+int pk_version(void);
+const char* pk_last_error(void);
+/* number of SMs / opt-in shared memory per block of the current device (host out) */
+int pk_device_info(int* sm_count, int* smem_optin);
+
+/* 1 in *out_flag (device int) when the data is integer-valued with
+ * d * (2 max|x|)^2 < 2^24, i.e. PK_MODE_EXACT32 is bit-exact.
+ * Replaces: nothing (reference always uses _kernels.py:21-38). */
+int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d, int* out_flag, void* stream);
+
+/* Beam-search kNN of member queries.  Replaces _kernels.beam_knn_batch
+ * (_kernels.py:230-262); with brute_fallback=1 also the short-row exact
+ * recompute of VamanaIndex.knn_batch (vamana.py:220-225).
+ * out_ids (m,kk) int64 (-1 pad), out_sqd (m,kk) float64 (+inf pad),
+ * out_counts (m,) int64 (counts BEFORE the fallback), kk = min(k, n-1).
+ * out_evals (device int64, may be null) accumulates distance evaluations.
+ * hash_bits: log2 of the per-query seen-table size (0 = automatic). */
+int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, const int32_t* adj, int64_t R,
+                const int32_t* deg, const int32_t* starts, int64_t s, const int64_t* qids, int64_t m,
+                int64_t L, int64_t k, int64_t* out_ids, double* out_sqd, int64_t* out_counts,
+                int brute_fallback, int64_t* out_evals, int hash_bits, void* stream);
+
+/* One search from an explicit start list for a member query (qid >= 0) or a
+ * float64 query vector (qid < 0, qvec = dp doubles, zero padded).  Replaces
+ * _kernels.beam_search_single (_kernels.py:215-227) as used by beam_search /
+ * find_knn_with_fallback (vamana.py:62-84, 175-197): writes the first k
+ * entries of sorted(visited U beam) without qid into top_ids/top_sqd (k
+ * slots), their count into *top_count, and the visit log (expansion order)
+ * into vis_ids/vis_sqd (capacity vcap; *vis_count may exceed vcap on overflow).
+ * Counts are device int64. */
+int pk_beam_search_single(const float* x, int64_t n, int64_t dp, const int32_t* adj, int64_t R,
+                          const int32_t* deg, const int32_t* starts, int64_t s, int64_t qid,
+                          const double* qvec, int64_t L, int64_t k, int64_t* top_ids, double* top_sqd,
+                          int64_t* top_count, int64_t* vis_ids, double* vis_sqd, int64_t vcap,
+                          int64_t* vis_count, void* stream);
+
+/* Exact kNN of member queries with (dist,id) order, self excluded.
+ * Replaces _kernels.brute_knn_batch (_kernels.py:86-104). kk = min(k, n-1). */
+int pk_brute_knn(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
+                 int64_t* out_ids, double* out_sqd, void* stream);
+
+/* Exact kNN of one float64 vector, no exclusion, kk = min(k, n).
+ * Replaces _kernels.brute_knn_vector (_kernels.py:107-118). */
+int pk_brute_knn_vector(const float* x, int64_t n, int64_t dp, const double* qvec, int64_t k,
+                        int64_t* out_ids, double* out_sqd, void* stream);
+
+/* Whole Vamana build: batches of 1, 2, 4, ... over `order`, each a fused
+ * beam-search + RobustPrune (_kernels.build_batch, _kernels.py:338-375), the
+ * out-list commit and the reverse-edge re-prune (_kernels.apply_reverse_edges,
+ * _kernels.py:378-415, grouped as in vamana.py:157-167).  Replaces the batch
+ * loop of build_vamana (vamana.py:141-169).  adj_out (n,R) int32 (-1 pad),
+ * deg_out (n,) int32.  starts/order are int32 device arrays (sampled on the
+ * host from the reference's PCG64 stream, vamana.py:132-143).
+ * stats (device int64[4], may be null): search evals, prune evals,
+ * reverse evals, expansions. */
+int pk_build_vamana(const float* x, int64_t n, int64_t dp, int mode, int64_t R, int64_t L, double alpha,
+                    const int32_t* starts, int64_t s, const int32_t* order, int32_t* adj_out,
+                    int32_t* deg_out, int64_t* stats, int hash_bits, void* stream);
+
+/* RobustPrune of vertex p over explicit candidates (ids, squared distances)
+ * merged with its current out-list cur_ids (distances recomputed).  Replaces
+ * _kernels.robust_prune_standalone (_kernels.py:318-335).  out (R,) int64,
+ * *out_count device int64. */
+int pk_robust_prune(const float* x, int64_t n, int64_t dp, int64_t p, const int64_t* cand_ids,
+                    const double* cand_sqd, int64_t m, const int64_t* cur_ids, int64_t dcount,
+                    double alpha, int64_t R, int64_t* out, int64_t* out_count, void* stream);
+
+/* Replaces _kernels.nearest_to_centroid (_kernels.py:418-435). *out device int64. */
+int pk_nearest_to_centroid(const float* x, int64_t n, int64_t dp, int64_t* out, void* stream);
+
+/* sqrt of squared distances, elementwise (index.py:131-139, vamana.py:226). */
+int pk_sqrt(const double* sqd, int64_t count, double* out, void* stream);
+
+/* Densities from (n,k) neighbour distances (true distances, not squared) and
+ * ids.  Replaces density.compute_densities (density.py:92-113) including
+ * numpy's pairwise row summation order. */
+int pk_densities(int kind, const int64_t* ids, const double* dists, int64_t n, int64_t k, double* rho,
+                 void* stream);
+
+/* kth_normalized from a given base density vector: rho*k / sum(base[ids])
+ * (density.density_kth_normalized, density.py:48-55, 69-73). */
+int pk_normalize_rho(const double* base, const int64_t* ids, int64_t n, int64_t k, double* out, void* stream);
+
+/* rank[i] in 1..n, higher = denser, ties by smaller id; *nan_flag (device
+ * int) set when rho has a NaN.  Replaces density.rank_order (density.py:116-129). */
+int pk_rank_order(const double* rho, int64_t n, int64_t* rank, int* nan_flag, void* stream);
+
+/* First strictly denser entry of each (dist,id)-sorted row.  Replaces
+ * dependent._resolve_from_lists (dependent.py:80-93): fills lam/delta for
+ * resolved rows, appends unresolved qids (ascending order preserved) to
+ * unresolved, count in *n_unresolved (device int64).  `skip` (>= 0) is a
+ * qid dropped from the unresolved list (the global density peak,
+ * dependent.py:112). */
+int pk_resolve_lists(const int64_t* rank, const int64_t* qids, int64_t m, const int64_t* ids,
+                     const double* dists, int64_t k, int64_t* lam, double* delta, int64_t* unresolved,
+                     int64_t* n_unresolved, int64_t skip, void* stream);
+
+/* Closest strictly denser point over all n for each query.  Replaces
+ * _kernels.dp_scan_all (_kernels.py:442-462).  out_id (m,) int64,
+ * out_sqd (m,) float64. */
+int pk_dp_scan(const float* x, int64_t n, int64_t dp, const int64_t* rank, const int64_t* qids, int64_t m,
+               int64_t* out_id, double* out_sqd, void* stream);
+
+/* Scatter: lam[qids[i]] = src_id[i], delta[qids[i]] = sqrt(src_sqd[i])
+ * (dependent.py:125-127). */
+int pk_scatter_dependents(const int64_t* qids, int64_t m, const int64_t* src_id, const double* src_sqd,
+                          int64_t* lam, double* delta, void* stream);
+
+/* index of the maximum rank (dependent.py:108: argmax(rank)); *out device int64 */
+int pk_argmax_rank(const int64_t* rank, int64_t n, int64_t* out, void* stream);
+
+/* Policies (cluster.py:134-180).  flags are device uint8 (n,).
+ *   noise:      flag[i] = rho[i] < rho_min
+ *   threshold:  flag[i] = !noise[i] && delta[i] >= delta_min
+ *   product:    the n_c non-noise ids with the largest delta*rho, ties by
+ *               larger delta then smaller id (lexsort, cluster.py:145-172);
+ *               requires n_c < number of non-noise points
+ *   local:      flag[i] = !noise[i] && rank[i] > max rank over its kNN row
+ *   orphans:    flag[i] |= lam[i] < 0 && !noise[i]   (cluster.py:248-253) */
+int pk_flag_noise(const double* rho, int64_t n, double rho_min, uint8_t* noise, int64_t* n_noise, void* stream);
+int pk_centers_threshold(const double* delta, const uint8_t* noise, int64_t n, double delta_min,
+                         uint8_t* center, void* stream);
+int pk_centers_product(const double* rho, const double* delta, const uint8_t* noise, int64_t n, int64_t n_c,
+                       uint8_t* center, void* stream);
+int pk_centers_local(const int64_t* rank, const int64_t* nbr_ids, int64_t k, const uint8_t* noise, int64_t n,
+                     uint8_t* center, void* stream);
+int pk_promote_orphans(const int64_t* lam, const uint8_t* noise, int64_t n, uint8_t* center, void* stream);
+
+/* Union-find assignment by pointer jumping on parent[i] = skip[i] ? i : lam[i]
+ * (dependency edges point strictly up in density rank, so each component is a
+ * tree rooted at its center / noise point).  Replaces assign_clusters +
+ * UnionFind (cluster.py:183-220, unionfind.py:16-41).  center/noise are
+ * device uint8 flags; labels (n,) int64.  status (device int64[2]):
+ * status[0] = 0 ok, 1 = a non-skip point with lam < 0 (status[1] = smallest
+ * such id), 3 = a component without center/noise (status[1] = smallest id). */
+int pk_assign_clusters(const int64_t* lam, const uint8_t* center, const uint8_t* noise, int64_t n,
+                       int64_t* labels, int64_t* status, void* stream);
+
+/* ids of set flags in ascending order: out (capacity n), *count device int64 */
+int pk_flags_to_ids(const uint8_t* flags, int64_t n, int64_t* out, int64_t* count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PEAKANN_B200_H */

@@ -1,0 +1,123 @@
+"""ctypes binding of the C ABI in include/peakann_b200.h.
+
+The product path has no CPU fallback: importing the kernels without a built
+`libpeakann_b200.so` or without a CUDA device raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpeakann_b200.so")
+
+MODE_SEQ64 = 0
+MODE_EXACT32 = 1
+
+DENSITY_CODES = {"kth": 0, "kth_normalized": 1, "exp_sum": 2, "sum_exp": 3, "sum": 4}
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int64
+_i = ctypes.c_int
+_D = ctypes.c_double
+
+# name -> argtypes (every entry returns int status)
+SIGNATURES = {
+    "pk_check_exact32": [_P, _I, _I, _I, _P, _P],
+    "pk_beam_knn": [_P, _I, _I, _i, _P, _I, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _i, _P, _i, _P],
+    "pk_beam_search_single": [_P, _I, _I, _P, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P],
+    "pk_brute_knn": [_P, _I, _I, _P, _I, _I, _P, _P, _P],
+    "pk_brute_knn_vector": [_P, _I, _I, _P, _I, _P, _P, _P],
+    "pk_build_vamana": [_P, _I, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P],
+    "pk_robust_prune": [_P, _I, _I, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P],
+    "pk_nearest_to_centroid": [_P, _I, _I, _P, _P],
+    "pk_sqrt": [_P, _I, _P, _P],
+    "pk_densities": [_i, _P, _P, _I, _I, _P, _P],
+    "pk_normalize_rho": [_P, _P, _I, _I, _P, _P],
+    "pk_rank_order": [_P, _I, _P, _P, _P],
+    "pk_resolve_lists": [_P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _P],
+    "pk_dp_scan": [_P, _I, _I, _P, _P, _I, _P, _P, _P],
+    "pk_scatter_dependents": [_P, _I, _P, _P, _P, _P, _P],
+    "pk_argmax_rank": [_P, _I, _P, _P],
+    "pk_flag_noise": [_P, _I, _D, _P, _P, _P],
+    "pk_centers_threshold": [_P, _P, _I, _D, _P, _P],
+    "pk_centers_product": [_P, _P, _P, _I, _I, _P, _P],
+    "pk_centers_local": [_P, _P, _I, _P, _I, _P, _P],
+    "pk_promote_orphans": [_P, _P, _I, _P, _P],
+    "pk_assign_clusters": [_P, _P, _P, _I, _P, _P, _P],
+    "pk_flags_to_ids": [_P, _I, _P, _P, _P],
+}
+
+_lib = None
+
+
+def build_library(force: bool = False) -> str:
+    """Compile csrc/ for sm_100a (nvcc cross-compiles without a GPU)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", os.path.join(_HERE, "csrc")], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"peakann-b200 CUDA library not built ({LIB_PATH} missing); run __graft_entry__.build()"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        for name, args in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.pk_last_error.restype = ctypes.c_char_p
+        L.pk_version.restype = ctypes.c_int
+        L.pk_device_info.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        _lib = L
+    return _lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("peakann-b200 needs a CUDA device (B200 / sm_100a); no CPU fallback exists")
+
+
+def call(name: str, *args) -> None:
+    """Invoke a C-ABI entry point; raise RuntimeError on a nonzero status."""
+    require_cuda()
+    fn = getattr(lib(), name)
+    conv = []
+    for a in args:
+        if isinstance(a, torch.Tensor):
+            conv.append(ctypes.c_void_p(a.data_ptr()))
+        elif a is None:
+            conv.append(ctypes.c_void_p(0))
+        else:
+            conv.append(a)
+    rc = fn(*conv)
+    if rc != 0:
+        msg = lib().pk_last_error().decode(errors="replace")
+        raise RuntimeError(f"{name} failed ({rc}): {msg}")
+
+
+def stream() -> int:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def device() -> torch.device:
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_dev(a: np.ndarray, dtype=None) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype)))
+    return t.to(device(), non_blocking=False)
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()

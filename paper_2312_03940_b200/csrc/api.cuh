@@ -1,0 +1,57 @@
+// Host-side helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace pk {
+
+void set_error(const std::string& msg);
+int fail(const char* where, cudaError_t e);
+
+#define PK_CHECK(call)                                   \
+    do {                                                 \
+        cudaError_t _e = (call);                         \
+        if (_e != cudaSuccess) return ::pk::fail(#call, _e); \
+    } while (0)
+
+#define PK_CHECK_LAUNCH(where)                                   \
+    do {                                                         \
+        cudaError_t _e = cudaGetLastError();                     \
+        if (_e != cudaSuccess) return ::pk::fail(where, _e);     \
+    } while (0)
+
+int sm_count();
+int max_smem_optin();
+
+inline int next_pow2(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// stream-ordered scratch allocation (cudaMallocAsync pool)
+template <class T>
+cudaError_t scratch(T** p, size_t count, cudaStream_t st) {
+    return cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T) + 16, st);
+}
+inline void release(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+// per-warp shared memory sizes
+inline size_t beam_smem_bytes(int L, int H) {
+    return (size_t)L * 12 + (size_t)H * 4 + 256;
+}
+inline size_t sort_smem_bytes(int cap) {
+    return (size_t)cap * 13 + 128;
+}
+inline size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
+
+int choose_hash(int L, int hash_bits);
+
+}  // namespace pk

@@ -40,6 +40,12 @@ __device__ __forceinline__ bool key_eq(double da, unsigned ia, double db, unsign
     return da == db && ia == ib;
 }
 
+__device__ __forceinline__ int next_pow2_dev(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 __device__ __forceinline__ float4 ldg4(const float* p) {

@@ -1,0 +1,629 @@
+// Beam-search kNN, single searches, exact kNN and the dependent-point scan.
+#include <cub/cub.cuh>
+
+#include "../../include/peakann_b200.h"
+#include "api.cuh"
+#include "beam.cuh"
+
+namespace pk {
+
+// ---- distance factories ------------------------------------------------------------
+template <int MODE, int QV>
+struct DistOf;
+
+template <int QV>
+struct DistOf<PK_MODE_SEQ64, QV> {
+    using T = Seq64Member;
+    __device__ static T make(const float* X, int dp, unsigned id) { return T{X + (size_t)id * dp, dp}; }
+};
+
+template <int QV>
+struct DistOf<PK_MODE_EXACT32, QV> {
+    using T = Exact32<QV>;
+    __device__ static T make(const float* X, int dp, unsigned id) {
+        T t;
+        t.load(X + (size_t)id * dp, dp);
+        return t;
+    }
+};
+
+__device__ __forceinline__ BeamSmem carve_beam(unsigned char* base, int L, int H) {
+    BeamSmem s;
+    s.bd = reinterpret_cast<double*>(base);
+    s.bi = reinterpret_cast<unsigned*>(base + (size_t)L * 8);
+    s.hash = reinterpret_cast<unsigned*>(base + (size_t)L * 12);
+    s.hmask = (unsigned)H - 1u;
+    s.spos = reinterpret_cast<int*>(base + (size_t)L * 12 + (size_t)H * 4);
+    s.cbuf = reinterpret_cast<unsigned*>(base + (size_t)L * 12 + (size_t)H * 4 + 128);
+    return s;
+}
+
+// ---- beam kNN of member queries (_kernels.py:230-262) --------------------------------
+template <int MODE, int QV>
+__global__ void __launch_bounds__(128) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
+                                                       int L, int kk, int H, size_t warp_bytes,
+                                                       long long* __restrict__ out_ids, double* __restrict__ out_d,
+                                                       long long* __restrict__ counts, long long* evals_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const int lane = lane_id();
+    unsigned char* mine = smem + (size_t)wib * warp_bytes;
+    BeamSmem sm = carve_beam(mine, L, H);
+    long long ev = 0;
+    for (long long t = (long long)blockIdx.x * wpb + wib; t < m; t += (long long)gridDim.x * wpb) {
+        const unsigned qi = (unsigned)qids[t];
+        auto dist = DistOf<MODE, QV>::make(P.X, P.dp, qi);
+        WarpBeam<decltype(dist)> wb;
+        wb.init(sm, L, nullptr, nullptr, 0, nullptr);
+        wb.seed(P, dist);
+        wb.walk(P, dist);
+        long long* oi = out_ids + t * kk;
+        double* od = out_d + t * kk;
+        int got = wb.emit(qi, kk, oi, od);
+        for (int x = got + lane; x < kk; x += 32) {
+            oi[x] = -1;
+            od[x] = __longlong_as_double(0x7ff0000000000000LL);
+        }
+        if (lane == 0) counts[t] = got;
+        ev += wb.evals;
+        __syncwarp();
+    }
+    if (evals_out && lane == 0 && ev) atomicAdd(reinterpret_cast<unsigned long long*>(evals_out), (unsigned long long)ev);
+}
+
+// rows with counts < kk -> list for the exact fallback
+__global__ void short_rows_kernel(const long long* counts, int m, int kk, int* list, int* nlist) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x)
+        if (counts[t] < kk) list[atomicAdd(nlist, 1)] = t;
+}
+
+// ---- single search (beam_search_single, _kernels.py:215-227) ---------------------------
+template <class Dist>
+__global__ void single_search_kernel(SearchParams P, Dist dist, unsigned self, int L, int k, int H,
+                                     long long* top_ids, double* top_d, long long* top_count,
+                                     long long* vis_ids, double* vis_d, int vcap, long long* vis_count,
+                                     unsigned* vtmp_i, double* vtmp_d) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    BeamSmem sm = carve_beam(smem, L, H);
+    __shared__ unsigned s_err;
+    if (threadIdx.x == 0) s_err = 0;
+    __syncwarp();
+    WarpBeam<Dist> wb;
+    wb.init(sm, L, vtmp_i, vtmp_d, vcap, &s_err);
+    wb.seed(P, dist);
+    wb.walk(P, dist);
+    int got = wb.emit(self, k, top_ids, top_d);
+    const int lane = lane_id();
+    for (int x = lane; x < min(wb.vl, vcap); x += 32) {
+        vis_ids[x] = vtmp_i[x];
+        vis_d[x] = vtmp_d[x];
+    }
+    if (lane == 0) {
+        *top_count = got;
+        *vis_count = wb.vl;
+    }
+}
+
+// ---- exact kNN: one block per row --------------------------------------------------------
+constexpr int BT = 256;
+
+struct RowQuery {
+    const float* qf;   // member row (float), or null
+    const double* qd;  // free vector (double), or null
+    int self;          // excluded id or -1
+};
+
+__device__ __forceinline__ double row_dist(const float* __restrict__ X, int dp, const RowQuery& q, int j) {
+    const float* r = X + (size_t)j * dp;
+    double acc = 0.0;
+    if (q.qf) {
+        for (int t = 0; t < dp; t += 4) {
+            float4 x = ldg4(r + t), y = ldg4(q.qf + t);
+            double a = (double)y.x - (double)x.x; acc = fma(a, a, acc);
+            double b = (double)y.y - (double)x.y; acc = fma(b, b, acc);
+            double c = (double)y.z - (double)x.z; acc = fma(c, c, acc);
+            double e = (double)y.w - (double)x.w; acc = fma(e, e, acc);
+        }
+    } else {
+        for (int t = 0; t < dp; t += 4) {
+            float4 x = ldg4(r + t);
+            double a = __ldg(q.qd + t) - (double)x.x; acc = fma(a, a, acc);
+            double b = __ldg(q.qd + t + 1) - (double)x.y; acc = fma(b, b, acc);
+            double c = __ldg(q.qd + t + 2) - (double)x.z; acc = fma(c, c, acc);
+            double e = __ldg(q.qd + t + 3) - (double)x.w; acc = fma(e, e, acc);
+        }
+    }
+    return acc;
+}
+
+// Block-wide exact top-kk of one distance row (the selection of
+// _kernels.py:55-83): radix-select the kk-th key, gather keys below it plus
+// the smallest ids among equal keys, bitonic-sort the survivors by (dist, id).
+__device__ void block_select_row(const double* row, int n, int kk, double* sd, unsigned* si, int P,
+                                 long long* out_ids, double* out_d) {
+    __shared__ unsigned hist[256];
+    __shared__ unsigned long long s_prefix;
+    __shared__ int s_want;
+    using Scan = cub::BlockScan<int, BT>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_base, s_eqseen;
+    const int tid = threadIdx.x;
+    unsigned long long prefix = 0, mask = 0;
+    int want = kk - 1;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int b = tid; b < 256; b += BT) hist[b] = 0;
+        __syncthreads();
+        for (int j = tid; j < n; j += BT) {
+            unsigned long long key = dbits(row[j]);
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0, b = 0;
+            for (; b < 256; ++b) {
+                if (acc + (int)hist[b] > want) break;
+                acc += hist[b];
+            }
+            s_want = want - acc;
+            s_prefix = prefix | ((unsigned long long)b << shift);
+        }
+        __syncthreads();
+        want = s_want;
+        prefix = s_prefix;
+        mask |= 255ull << shift;
+        __syncthreads();
+    }
+    const unsigned long long th = prefix;
+    const int need_eq = want + 1;  // equal keys admitted, smallest ids first
+    if (tid == 0) { s_base = 0; s_eqseen = 0; }
+    __syncthreads();
+    for (int base = 0; base < n; base += BT) {
+        int j = base + tid;
+        unsigned long long key = j < n ? dbits(row[j]) : ~0ull;
+        int eq = (j < n && key == th) ? 1 : 0;
+        int eq_before, eq_total;
+        Scan(scan_tmp).ExclusiveSum(eq, eq_before, eq_total);
+        __syncthreads();
+        int keep = (j < n) && (key < th || (eq && s_eqseen + eq_before < need_eq));
+        int pos, tot;
+        Scan(scan_tmp).ExclusiveSum(keep, pos, tot);
+        if (keep) {
+            sd[s_base + pos] = row[j];
+            si[s_base + pos] = (unsigned)j;
+        }
+        __syncthreads();
+        if (tid == 0) { s_base += tot; s_eqseen += eq_total; }
+        __syncthreads();
+    }
+    for (int i = kk + tid; i < P; i += BT) {
+        sd[i] = __longlong_as_double(0x7ff0000000000000LL);
+        si[i] = 0xffffffffu;
+    }
+    __syncthreads();
+    for (int k2 = 2; k2 <= P; k2 <<= 1) {
+        for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+            for (int i = tid; i < P; i += BT) {
+                int x = i ^ j2;
+                if (x > i) {
+                    double a = sd[i], b = sd[x];
+                    unsigned ia = si[i], ib = si[x];
+                    bool asc = (i & k2) == 0;
+                    if (key_lt(b, ib, a, ia) == asc) {
+                        sd[i] = b; sd[x] = a;
+                        si[i] = ib; si[x] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = tid; i < kk; i += BT) {
+        out_ids[i] = si[i];
+        out_d[i] = sd[i];
+    }
+    __syncthreads();
+}
+
+// rows: either rowlist (indexes into qids, count in *nrows) or all m rows
+__global__ void __launch_bounds__(BT) brute_rows_kernel(const float* __restrict__ X, int n, int dp,
+                                                        const long long* __restrict__ qids, const double* qvec,
+                                                        const int* rowlist, const int* nrows, int m, int kk,
+                                                        double* scratch, double* sbuf_d, unsigned* sbuf_i, int P,
+                                                        long long* out_ids, double* out_d) {
+    double* row = scratch + (size_t)blockIdx.x * n;
+    double* sd = sbuf_d + (size_t)blockIdx.x * P;
+    unsigned* si = sbuf_i + (size_t)blockIdx.x * P;
+    const int rows = rowlist ? *nrows : m;
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int t = rowlist ? rowlist[r] : r;
+        RowQuery q;
+        if (qvec) {
+            q.qf = nullptr; q.qd = qvec; q.self = -1;
+        } else {
+            int i = (int)qids[t];
+            q.qf = X + (size_t)i * dp; q.qd = nullptr; q.self = i;
+        }
+        for (int j = threadIdx.x; j < n; j += BT)
+            row[j] = j == q.self ? __longlong_as_double(0x7ff0000000000000LL) : row_dist(X, dp, q, j);
+        __syncthreads();
+        block_select_row(row, n, kk, sd, si, P, out_ids + (size_t)t * kk, out_d + (size_t)t * kk);
+    }
+}
+
+// ---- dependent-point scan (_kernels.py:442-462) ------------------------------------------
+constexpr int DQ = 8;     // queries per block
+constexpr int DPT = 4;    // points per thread
+
+__global__ void __launch_bounds__(BT) dp_scan_kernel(const float* __restrict__ X, int n, int dp,
+                                                     const long long* __restrict__ rank,
+                                                     const long long* __restrict__ qids, int m,
+                                                     double* part_d, int* part_i) {
+    extern __shared__ __align__(16) float qs[];  // DQ * dp
+    __shared__ long long qr[DQ];
+    const int q0 = blockIdx.x * DQ;
+    const int nq = min(DQ, m - q0);
+    for (int x = threadIdx.x; x < DQ * dp; x += BT) {
+        int qq = x / dp, t = x % dp;
+        qs[x] = qq < nq ? X[(size_t)qids[q0 + qq] * dp + t] : 0.f;
+    }
+    if (threadIdx.x < DQ) qr[threadIdx.x] = threadIdx.x < nq ? rank[qids[q0 + threadIdx.x]] : 0x7fffffffffffffffLL;
+    __syncthreads();
+    long long rmin = qr[0];
+    for (int qq = 1; qq < DQ; ++qq) rmin = min(rmin, qr[qq]);
+    double best[DQ];
+    int bid[DQ];
+#pragma unroll
+    for (int qq = 0; qq < DQ; ++qq) {
+        best[qq] = __longlong_as_double(0x7ff0000000000000LL);
+        bid[qq] = -1;
+    }
+    const int chunk = BT * DPT;
+    const int j0 = blockIdx.y * chunk;
+    for (int jj = threadIdx.x; jj < chunk; jj += BT) {
+        int j = j0 + jj;
+        if (j >= n) break;
+        long long rj = __ldg(rank + j);
+        if (rj <= rmin) continue;
+        const float* r = X + (size_t)j * dp;
+        double acc[DQ];
+#pragma unroll
+        for (int qq = 0; qq < DQ; ++qq) acc[qq] = 0.0;
+        for (int t = 0; t < dp; t += 4) {
+            float4 x = ldg4(r + t);
+#pragma unroll
+            for (int qq = 0; qq < DQ; ++qq) {
+                const float* qv = qs + qq * dp + t;
+                double a = (double)qv[0] - (double)x.x; acc[qq] = fma(a, a, acc[qq]);
+                double b = (double)qv[1] - (double)x.y; acc[qq] = fma(b, b, acc[qq]);
+                double c = (double)qv[2] - (double)x.z; acc[qq] = fma(c, c, acc[qq]);
+                double e = (double)qv[3] - (double)x.w; acc[qq] = fma(e, e, acc[qq]);
+            }
+        }
+#pragma unroll
+        for (int qq = 0; qq < DQ; ++qq)
+            if (rj > qr[qq] && key_lt(acc[qq], (unsigned)j, best[qq], (unsigned)bid[qq])) {
+                best[qq] = acc[qq];
+                bid[qq] = j;
+            }
+    }
+    // block argmin per query
+    __shared__ double rd[BT / 32][DQ];
+    __shared__ int ri[BT / 32][DQ];
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+#pragma unroll
+    for (int qq = 0; qq < DQ; ++qq) {
+        double d = best[qq];
+        unsigned i = (unsigned)bid[qq];
+        for (int s = 16; s; s >>= 1) {
+            double od = __shfl_xor_sync(PK_FULL, d, s);
+            unsigned oi = __shfl_xor_sync(PK_FULL, i, s);
+            if (key_lt(od, oi, d, i)) { d = od; i = oi; }
+        }
+        if (lane == 0) { rd[w][qq] = d; ri[w][qq] = (int)i; }
+    }
+    __syncthreads();
+    if (threadIdx.x < nq) {
+        int qq = threadIdx.x;
+        double d = rd[0][qq];
+        unsigned i = (unsigned)ri[0][qq];
+        for (int ww = 1; ww < BT / 32; ++ww)
+            if (key_lt(rd[ww][qq], (unsigned)ri[ww][qq], d, i)) { d = rd[ww][qq]; i = (unsigned)ri[ww][qq]; }
+        part_d[(size_t)(q0 + qq) * gridDim.y + blockIdx.y] = d;
+        part_i[(size_t)(q0 + qq) * gridDim.y + blockIdx.y] = (int)i;
+    }
+}
+
+__global__ void dp_scan_reduce_kernel(const double* part_d, const int* part_i, int m, int nchunk,
+                                      long long* out_id, double* out_d) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    double d = __longlong_as_double(0x7ff0000000000000LL);
+    unsigned i = 0xffffffffu;
+    for (int c = 0; c < nchunk; ++c) {
+        double od = part_d[(size_t)t * nchunk + c];
+        unsigned oi = (unsigned)part_i[(size_t)t * nchunk + c];
+        if (key_lt(od, oi, d, i)) { d = od; i = oi; }
+    }
+    out_id[t] = i == 0xffffffffu ? -1 : (long long)i;
+    out_d[t] = d;
+}
+
+// ---- misc small kernels ----------------------------------------------------------------------
+__global__ void fill_ids_kernel(long long* ids, double* d, long long count) {
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < count; x += (long long)gridDim.x * blockDim.x) {
+        ids[x] = -1;
+        d[x] = __longlong_as_double(0x7ff0000000000000LL);
+    }
+}
+
+__global__ void check_exact32_kernel(const float* x, long long total, int dp, int d, int* bad, float* maxabs) {
+    float mx = 0.f;
+    int b = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        if ((int)(i % dp) >= d) continue;
+        float v = x[i];
+        if (v != rintf(v)) b = 1;
+        mx = fmaxf(mx, fabsf(v));
+    }
+    if (b) atomicOr(bad, 1);
+    for (int s = 16; s; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(PK_FULL, mx, s));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(maxabs), __float_as_int(mx));
+}
+
+__global__ void finish_exact32_kernel(const int* bad, const float* maxabs, int d, int* flag) {
+    double m = (double)*maxabs;
+    double bound = (double)d * (2.0 * m) * (2.0 * m);
+    *flag = (*bad == 0 && bound < 16777216.0) ? 1 : 0;
+}
+
+__global__ void sqrt_kernel(const double* a, long long count, double* out) {
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < count; x += (long long)gridDim.x * blockDim.x)
+        out[x] = sqrt(a[x]);
+}
+
+__global__ void to_i32_kernel(const long long* a, long long count, int* out) {
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < count; x += (long long)gridDim.x * blockDim.x)
+        out[x] = (int)a[x];
+}
+
+__global__ void start_bitmap_kernel(const int* starts, int s, unsigned* bm) {
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < s; x += gridDim.x * blockDim.x)
+        atomicOr(bm + (starts[x] >> 5), 1u << (starts[x] & 31));
+}
+
+int grid_for(long long work, int block) {
+    long long g = (work + block - 1) / block;
+    long long cap = (long long)sm_count() * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// ---- launch helpers --------------------------------------------------------------------------
+int choose_hash(int L, int hash_bits) {
+    if (hash_bits > 0) return 1 << hash_bits;
+    int h = next_pow2(16 * L);
+    if (h < 512) h = 512;
+    if (h > 8192) h = 8192;
+    return h;
+}
+
+template <int MODE, int QV>
+int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, int kk, int H,
+                    long long* out_ids, double* out_d, long long* counts, long long* evals, cudaStream_t st) {
+    size_t wb = align16(beam_smem_bytes(L, H));
+    int wpb = 4;
+    while (wpb > 1 && wb * wpb > (size_t)max_smem_optin()) wpb >>= 1;
+    if (wb * wpb > (size_t)max_smem_optin()) {
+        set_error("beam width too large for shared memory");
+        return 2;
+    }
+    auto kern = beam_knn_kernel<MODE, QV>;
+    PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wb * wpb)));
+    int per_sm = 0;
+    PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, wb * wpb));
+    if (per_sm < 1) per_sm = 1;
+    long long blocks = ((long long)m + wpb - 1) / wpb;
+    long long cap = (long long)sm_count() * per_sm;
+    int grid = (int)(blocks < cap ? blocks : cap);
+    if (grid < 1) grid = 1;
+    kern<<<grid, 32 * wpb, wb * wpb, st>>>(P, qids, m, L, kk, H, wb, out_ids, out_d, counts, evals);
+    PK_CHECK_LAUNCH("beam_knn_kernel");
+    return 0;
+}
+
+template <int MODE>
+int dispatch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, int kk, int H,
+                      long long* out_ids, double* out_d, long long* counts, long long* evals, cudaStream_t st) {
+    if (MODE == PK_MODE_SEQ64) return launch_beam_knn<MODE, 1>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
+    int qv = (P.dp + 127) / 128;
+    if (qv <= 1) return launch_beam_knn<MODE, 1>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
+    if (qv <= 2) return launch_beam_knn<MODE, 2>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
+    if (qv <= 4) return launch_beam_knn<MODE, 4>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
+    if (qv <= 8) return launch_beam_knn<MODE, 8>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
+    set_error("EXACT32 mode supports d <= 1024");
+    return 2;
+}
+
+// exact kNN over a row list (or all rows), chunked scratch
+int run_brute(const float* x, int n, int dp, const long long* qids, const double* qvec, const int* rowlist,
+              const int* nrows, int m, int kk, long long* out_ids, double* out_d, cudaStream_t st) {
+    if (kk <= 0 || m <= 0) return 0;
+    int P = next_pow2(kk);
+    int grid = sm_count();
+    // scratch budget: keep the per-block row buffers <= ~2 GiB
+    long long per_block = (long long)n * 8 + (long long)P * 12;
+    long long maxg = (2ll << 30) / (per_block > 0 ? per_block : 1);
+    if (maxg < 1) maxg = 1;
+    if (grid > maxg) grid = (int)maxg;
+    if (!rowlist && grid > m) grid = m;
+    double* scr = nullptr;
+    double* sd = nullptr;
+    unsigned* si = nullptr;
+    PK_CHECK(scratch(&scr, (size_t)grid * n, st));
+    PK_CHECK(scratch(&sd, (size_t)grid * P, st));
+    PK_CHECK(scratch(&si, (size_t)grid * P, st));
+    brute_rows_kernel<<<grid, BT, 0, st>>>(x, n, dp, qids, qvec, rowlist, nrows, m, kk, scr, sd, si, P, out_ids, out_d);
+    cudaError_t e = cudaGetLastError();
+    release(scr, st);
+    release(sd, st);
+    release(si, st);
+    if (e != cudaSuccess) return fail("brute_rows_kernel", e);
+    return 0;
+}
+
+}  // namespace pk
+
+using namespace pk;
+
+extern "C" int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d, int* out_flag, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    int* bad = nullptr;
+    float* mx = nullptr;
+    PK_CHECK(scratch(&bad, 1, st));
+    PK_CHECK(scratch(&mx, 1, st));
+    PK_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    PK_CHECK(cudaMemsetAsync(mx, 0, sizeof(float), st));
+    long long total = n * dp;
+    check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx);
+    finish_exact32_kernel<<<1, 1, 0, st>>>(bad, mx, (int)d, out_flag);
+    PK_CHECK_LAUNCH("check_exact32");
+    release(bad, st);
+    release(mx, st);
+    return 0;
+}
+
+extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, const int32_t* adj, int64_t R,
+                           const int32_t* deg, const int32_t* starts, int64_t s, const int64_t* qids, int64_t m,
+                           int64_t L, int64_t k, int64_t* out_ids, double* out_sqd, int64_t* out_counts,
+                           int brute_fallback, int64_t* out_evals, int hash_bits, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    int64_t kk = k < n - 1 ? k : n - 1;
+    if (kk <= 0 || m <= 0) {
+        if (m > 0) PK_CHECK(cudaMemsetAsync(out_counts, 0, sizeof(int64_t) * m, st));
+        return 0;
+    }
+    if (L < kk) {
+        set_error("beam width L must be >= k");
+        return 2;
+    }
+    unsigned* bm = nullptr;
+    size_t words = (size_t)(n + 31) / 32;
+    PK_CHECK(scratch(&bm, words, st));
+    PK_CHECK(cudaMemsetAsync(bm, 0, words * 4, st));
+    start_bitmap_kernel<<<grid_for(s, 256), 256, 0, st>>>(starts, (int)s, bm);
+    SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, bm};
+    int H = choose_hash((int)L, hash_bits);
+    const long long* q = reinterpret_cast<const long long*>(qids);
+    long long* oi = reinterpret_cast<long long*>(out_ids);
+    long long* oc = reinterpret_cast<long long*>(out_counts);
+    long long* ev = reinterpret_cast<long long*>(out_evals);
+    int rc = mode == PK_MODE_EXACT32
+                 ? dispatch_beam_knn<PK_MODE_EXACT32>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st)
+                 : dispatch_beam_knn<PK_MODE_SEQ64>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st);
+    if (rc) return rc;
+    release(bm, st);
+    if (brute_fallback) {
+        int* list = nullptr;
+        int* nl = nullptr;
+        PK_CHECK(scratch(&list, (size_t)m, st));
+        PK_CHECK(scratch(&nl, 1, st));
+        PK_CHECK(cudaMemsetAsync(nl, 0, sizeof(int), st));
+        short_rows_kernel<<<grid_for(m, 256), 256, 0, st>>>(oc, (int)m, (int)kk, list, nl);
+        PK_CHECK_LAUNCH("short_rows_kernel");
+        rc = run_brute(x, (int)n, (int)dp, q, nullptr, list, nl, (int)m, (int)kk, oi, out_sqd, st);
+        release(list, st);
+        release(nl, st);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+extern "C" int pk_beam_search_single(const float* x, int64_t n, int64_t dp, const int32_t* adj, int64_t R,
+                                     const int32_t* deg, const int32_t* starts, int64_t s, int64_t qid,
+                                     const double* qvec, int64_t L, int64_t k, int64_t* top_ids, double* top_sqd,
+                                     int64_t* top_count, int64_t* vis_ids, double* vis_sqd, int64_t vcap,
+                                     int64_t* vis_count, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (L < k) {
+        set_error("beam width L must be >= k");
+        return 2;
+    }
+    SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, nullptr};
+    int H = choose_hash((int)L, 0);
+    size_t bytes = align16(beam_smem_bytes((int)L, H));
+    unsigned* vi = nullptr;
+    double* vd = nullptr;
+    PK_CHECK(scratch(&vi, (size_t)vcap, st));
+    PK_CHECK(scratch(&vd, (size_t)vcap, st));
+    unsigned self = qid >= 0 ? (unsigned)qid : 0xffffffffu;
+    if (qid >= 0) {
+        auto kern = single_search_kernel<Seq64Member>;
+        PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        kern<<<1, 32, bytes, st>>>(P, Seq64Member{x + (size_t)qid * dp, (int)dp}, self, (int)L, (int)k, H,
+                                   reinterpret_cast<long long*>(top_ids), top_sqd, reinterpret_cast<long long*>(top_count),
+                                   reinterpret_cast<long long*>(vis_ids), vis_sqd, (int)vcap,
+                                   reinterpret_cast<long long*>(vis_count), vi, vd);
+    } else {
+        auto kern = single_search_kernel<Seq64Vector>;
+        PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        kern<<<1, 32, bytes, st>>>(P, Seq64Vector{qvec, (int)dp}, self, (int)L, (int)k, H,
+                                   reinterpret_cast<long long*>(top_ids), top_sqd, reinterpret_cast<long long*>(top_count),
+                                   reinterpret_cast<long long*>(vis_ids), vis_sqd, (int)vcap,
+                                   reinterpret_cast<long long*>(vis_count), vi, vd);
+    }
+    PK_CHECK_LAUNCH("single_search_kernel");
+    release(vi, st);
+    release(vd, st);
+    return 0;
+}
+
+extern "C" int pk_brute_knn(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
+                            int64_t* out_ids, double* out_sqd, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    int64_t kk = k < n - 1 ? k : n - 1;
+    if (kk <= 0 || m <= 0) return 0;
+    return run_brute(x, (int)n, (int)dp, reinterpret_cast<const long long*>(qids), nullptr, nullptr, nullptr, (int)m,
+                     (int)kk, reinterpret_cast<long long*>(out_ids), out_sqd, st);
+}
+
+extern "C" int pk_brute_knn_vector(const float* x, int64_t n, int64_t dp, const double* qvec, int64_t k,
+                                   int64_t* out_ids, double* out_sqd, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    int64_t kk = k < n ? k : n;
+    if (kk <= 0) return 0;
+    return run_brute(x, (int)n, (int)dp, nullptr, qvec, nullptr, nullptr, 1, (int)kk,
+                     reinterpret_cast<long long*>(out_ids), out_sqd, st);
+}
+
+extern "C" int pk_dp_scan(const float* x, int64_t n, int64_t dp, const int64_t* rank, const int64_t* qids, int64_t m,
+                          int64_t* out_id, double* out_sqd, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (m <= 0) return 0;
+    int nchunk = (int)((n + BT * DPT - 1) / (BT * DPT));
+    dim3 grid((unsigned)((m + DQ - 1) / DQ), (unsigned)nchunk);
+    double* pd = nullptr;
+    int* pi = nullptr;
+    PK_CHECK(scratch(&pd, (size_t)m * nchunk, st));
+    PK_CHECK(scratch(&pi, (size_t)m * nchunk, st));
+    size_t sm = (size_t)DQ * dp * sizeof(float);
+    if (sm > 48 * 1024) PK_CHECK(cudaFuncSetAttribute(dp_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dp_scan_kernel<<<grid, BT, sm, st>>>(x, (int)n, (int)dp, reinterpret_cast<const long long*>(rank),
+                                         reinterpret_cast<const long long*>(qids), (int)m, pd, pi);
+    PK_CHECK_LAUNCH("dp_scan_kernel");
+    dp_scan_reduce_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(pd, pi, (int)m, nchunk,
+                                                                     reinterpret_cast<long long*>(out_id), out_sqd);
+    PK_CHECK_LAUNCH("dp_scan_reduce_kernel");
+    release(pd, st);
+    release(pi, st);
+    return 0;
+}
+
+extern "C" int pk_sqrt(const double* sqd, int64_t count, double* out, void* stream) {
+    if (count <= 0) return 0;
+    cudaStream_t st = as_stream(stream);
+    sqrt_kernel<<<grid_for(count, 256), 256, 0, st>>>(sqd, count, out);
+    PK_CHECK_LAUNCH("sqrt_kernel");
+    return 0;
+}

@@ -1,0 +1,191 @@
+"""CUDA path vs the reference's golden vectors and the CPU oracle (GPU only).
+
+Bit-exact comparisons everywhere except exp-based densities (exp_sum,
+sum_exp), which are compared within 1e-12 relative (CUDA exp vs host libm)."""
+
+import hashlib
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import FIG_COORDS, golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2312_03940_b200 as pk  # noqa: E402
+from paper_2312_03940_b200 import _lib, vamana, workloads  # noqa: E402
+
+KINDS = ["kth", "kth_normalized", "exp_sum", "sum_exp", "sum"]
+
+
+def digest(a) -> str:
+    a = np.ascontiguousarray(a)
+    h = hashlib.sha256(f"{a.dtype.str}{a.shape}".encode())
+    h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def _tags(z, suffix):
+    return sorted({k.split("__")[0] for k in z.files if k.endswith(suffix)})
+
+
+def points(data, mode=None):
+    p = pk.PointSet(data)
+    if mode == "seq64":
+        p._mode = _lib.MODE_SEQ64
+    return p
+
+
+@pytest.mark.parametrize("mode", [None, "seq64"])
+def test_brute_knn_golden(mode):
+    z = golden("brute")
+    for tag in _tags(z, "__data"):
+        data = z[f"{tag}__data"]
+        p = points(data, mode)
+        idx = pk.build_bruteforce(p)
+        for key in z.files:
+            if key.startswith(f"{tag}__k") and key.endswith("__ids"):
+                k = int(key.split("__")[1][1:])
+                nb = idx.knn_batch(np.arange(p.n), k)
+                assert np.array_equal(nb.ids, z[key]), (tag, k)
+                assert np.array_equal(nb.dists, np.sqrt(z[key.replace("__ids", "__sqd")])), (tag, k)
+        nl = idx.find_knn(z[f"{tag}__vec__q"], 7)
+        assert np.array_equal(nl.ids, z[f"{tag}__vec__ids"]), tag
+        assert np.array_equal(nl.dists, np.sqrt(z[f"{tag}__vec__sqd"])), tag
+
+
+@pytest.mark.parametrize("mode", [None, "seq64"])
+def test_build_matches_reference_graph(mode):
+    z = golden("graphs")
+    for tag in _tags(z, "__adj"):
+        data = z[f"{tag}__data"]
+        R, L, seed, ns, medoid = (int(v) for v in z[f"{tag}__params"])
+        alpha = float(z[f"{tag}__alpha"][0])
+        p = points(data, mode)
+        idx = pk.build_vamana(p, R=R, L_build=L, alpha=alpha, num_starts=None if ns < 0 else ns, seed=seed,
+                              medoid_start=bool(medoid))
+        g = idx.graph
+        assert np.array_equal(g.start_points, z[f"{tag}__starts"]), tag
+        assert np.array_equal(g.degrees, z[f"{tag}__deg"]), tag
+        assert np.array_equal(g.adjacency, z[f"{tag}__adj"]), tag
+
+
+@pytest.mark.parametrize("mode", [None, "seq64"])
+def test_beam_knn_on_reference_graphs(mode):
+    z = golden("graphs")
+    for tag in _tags(z, "__adj"):
+        data = z[f"{tag}__data"]
+        p = points(data, mode)
+        g = pk.GraphIndex(p, z[f"{tag}__adj"], z[f"{tag}__deg"], int(z[f"{tag}__params"][0]), z[f"{tag}__starts"], 1.0)
+        qids = z[f"{tag}__qids"]
+        qt = _lib.to_dev(qids)
+        for key in z.files:
+            if key.startswith(f"{tag}__beam_") and key.endswith("__ids"):
+                _, spec, _ = key.split("__")
+                Lq, k = (int(x[1:]) for x in spec.split("_")[1:])
+                ids, sqd, counts = vamana.beam_knn_raw(g, qt, Lq, k)
+                pre = key[: -len("__ids")]
+                assert np.array_equal(_lib.to_host(ids), z[pre + "__ids"]), key
+                assert np.array_equal(_lib.to_host(sqd), z[pre + "__sqd"]), key
+                assert np.array_equal(_lib.to_host(counts), z[pre + "__counts"]), key
+        vi = pk.VamanaIndex(g, int(z[f"{tag}__params"][1]))
+        nb = vi.knn_batch(qids, 5)
+        assert np.array_equal(nb.ids, z[f"{tag}__knn5__ids"]), tag
+        assert np.array_equal(nb.dists, z[f"{tag}__knn5__dists"]), tag
+        # single vector-query search: first L candidates + visit log
+        L = int(z[f"{tag}__params"][1])
+        cand = z[f"{tag}__single__cand_ids"]
+        kk = min(L, cand.shape[0])
+        nl, visited = pk.beam_search(g, z[f"{tag}__single__q"], g.start_points, L, kk)
+        assert np.array_equal(nl.ids, cand[:kk]), tag
+        assert np.array_equal(nl.dists, np.sqrt(z[f"{tag}__single__cand_sqd"][:kk])), tag
+        assert [v.id for v in visited] == list(z[f"{tag}__single__vis_ids"]), tag
+        assert np.array_equal(np.array([v.dist for v in visited]), np.sqrt(z[f"{tag}__single__vis_sqd"])), tag
+
+
+def test_robust_prune_golden():
+    z = golden("prune")
+    data = z["data"]
+    p = pk.PointSet(data)
+    for c in range(4):
+        pp, R, ncur = (int(v) for v in z[f"c{c}__args"])
+        adj = np.full((40, max(R, 8)), -1, np.int32)
+        deg = np.zeros(40, np.int32)
+        cur = z[f"c{c}__cur"]
+        adj[pp, : cur.shape[0]] = cur
+        deg[pp] = cur.shape[0]
+        g = pk.GraphIndex(p, adj, deg, adj.shape[1], np.array([0]), 1.0)
+        cands = [pk.Neighbor(int(i), float(np.sqrt(d))) for i, d in zip(z[f"c{c}__cand"], z[f"c{c}__cand_sqd"])]
+        out = pk.robust_prune(g, pp, cands, float(z[f"c{c}__alpha"][0]), R)
+        assert np.array_equal(out, z[f"c{c}__out"]), c
+    idx = pk.build_vamana(pk.PointSet(z["line"]), R=3, L_build=4, medoid_start=True, seed=0)
+    assert idx.graph.start_points[0] == int(z["line_centroid"][0])
+
+
+def _policy(meta, fmeta):
+    code, arg = int(meta[4]), int(meta[5])
+    return [pk.ThresholdCenter(float(fmeta[0])), pk.ProductCenter(arg), pk.LocalCenter()][code]
+
+
+def test_small_pipelines_golden():
+    z = golden("pipelines")
+    res = pk.run_pipeline(pk.PointSet(FIG_COORDS), pk.BruteForceConfig(), k=1, density_kind="kth",
+                          center_policy=pk.ThresholdCenter(2.5), noise_policy=pk.NoisePolicy(1 / np.sqrt(2.0)),
+                          doubling_params=pk.DoublingParams(initial_k=2, threshold=0))
+    assert np.array_equal(res.state.rho, z["fig__rho"])
+    assert np.array_equal(res.state.lam, z["fig__lam"])
+    assert np.array_equal(res.clustering.labels, z["fig__labels"])
+    assert np.array_equal(res.clustering.centers, z["fig__centers"])
+    assert np.array_equal(res.clustering.noise, z["fig__noise"])
+    for t in range(15):
+        meta = z[f"t{t}__meta"]
+        k, vam, thr, kind = int(meta[0]), int(meta[1]), int(meta[2]), KINDS[int(meta[3])]
+        icfg = pk.VamanaConfig(R=8, L_build=12, L=12, alpha=1.1, seed=t) if vam else pk.BruteForceConfig()
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            res = pk.run_pipeline(pk.PointSet(z[f"t{t}__data"]), icfg, k=k, density_kind=kind,
+                                  center_policy=_policy(meta, z[f"t{t}__fmeta"]), noise_policy=pk.NoisePolicy(0.0),
+                                  doubling_params=pk.DoublingParams(initial_k=2 * k, threshold=thr))
+        st = res.state
+        assert np.array_equal(st.neighbors.ids, z[f"t{t}__nbr_ids"]), t
+        assert np.array_equal(st.neighbors.dists, z[f"t{t}__nbr_dists"]), t
+        if kind in ("exp_sum", "sum_exp"):
+            np.testing.assert_allclose(st.rho, z[f"t{t}__rho"], rtol=1e-12, atol=0)
+        else:
+            assert np.array_equal(st.rho, z[f"t{t}__rho"]), t
+        assert np.array_equal(st.lam, z[f"t{t}__lam"]), t
+        assert np.array_equal(st.delta, z[f"t{t}__delta"]), t
+        assert np.array_equal(res.clustering.labels, z[f"t{t}__labels"]), t
+        assert np.array_equal(res.clustering.centers, z[f"t{t}__centers"]), t
+
+
+@pytest.mark.parametrize("tag,name,n,comps,brute", [
+    ("c1", "C1", 10_000, 10, False),
+    ("c1brute", "C1", 4_000, 10, True),
+    ("c2s", "C2", 20_000, 20, False),
+    ("c3s", "C3", 30_000, 300, False),
+])
+def test_config_pipelines_golden(tag, name, n, comps, brute):
+    z = golden(tag)
+    data, _ = workloads.generate(name, n=n, components=comps)
+    kw = workloads.pipeline_args(name, pk, n_centers=comps, brute=brute)
+    res = pk.run_pipeline(pk.PointSet(data), **kw)
+    st = res.state
+    got = dict(rho=st.rho, lam=st.lam, delta=st.delta, nbr_ids=st.neighbors.ids, nbr_dists=st.neighbors.dists,
+               labels=res.clustering.labels, centers=res.clustering.centers, noise=res.clustering.noise)
+    bad = [key for key, val in got.items() if digest(val) != str(z[f"digest__{key}"])]
+    if bad:
+        head = {key: np.flatnonzero(got[key][:1000] != z[f"head__{key}"])[:5].tolist() for key in bad
+                if got[key][:1000].shape == z[f"head__{key}"].shape}
+        raise AssertionError(f"{tag}: digests differ for {bad}; first mismatching rows in head: {head}")
+    if not brute:
+        w = workloads.WORKLOADS[name]
+        idx = pk.build_vamana(pk.PointSet(data), R=w.R, L_build=w.L, alpha=w.alpha, seed=0, query_beam=w.L)
+        assert digest(idx.graph.adjacency) == str(z["digest__adj"])
