@@ -64,10 +64,12 @@ __device__ __forceinline__ unsigned seen_slot(unsigned id, unsigned mask) {
 // bit-identical to the reference's sequential float64 accumulation
 // (_kernels.py:21-28):
 //
-//  * Seq64: each lane walks its candidate's coordinates t = 0..d-1 in order
-//    with float64 fused multiply-adds.  (f64(a)-f64(b)) is exact and its square
-//    fits 50 bits, so fma(diff, diff, acc) == acc + diff*diff: the result is the
-//    reference's value for any float32 data.
+//  * Seq64: each lane walks its candidate's coordinates t = 0..d-1 in order,
+//    acc = acc + diff*diff with the product and the sum rounded separately
+//    (__dmul_rn / __dadd_rn, never contracted to an FMA: for coordinates of
+//    different magnitude diff carries more than 26 bits and its square is not
+//    exact, so an FMA would round differently from the reference's numba code).
+//    The result is the reference's value for any float32 data.
 //  * Exact32: lanes split the dimensions and reduce float32 partial sums across
 //    the warp.  Only used when the point set is integer-valued with
 //    d * (2*max|x|)^2 < 2^24 (checked on upload): every partial sum is then an
@@ -88,10 +90,10 @@ struct Seq64Member {
         for (int t = 0; t < dp; t += 4) {
             float4 x = ldg4(r + t);
             float4 y = ldg4(q + t);
-            double a = (double)y.x - (double)x.x; acc = fma(a, a, acc);
-            double b = (double)y.y - (double)x.y; acc = fma(b, b, acc);
-            double c = (double)y.z - (double)x.z; acc = fma(c, c, acc);
-            double e = (double)y.w - (double)x.w; acc = fma(e, e, acc);
+            double a = (double)y.x - (double)x.x; acc = __dadd_rn(acc, __dmul_rn(a, a));
+            double b = (double)y.y - (double)x.y; acc = __dadd_rn(acc, __dmul_rn(b, b));
+            double c = (double)y.z - (double)x.z; acc = __dadd_rn(acc, __dmul_rn(c, c));
+            double e = (double)y.w - (double)x.w; acc = __dadd_rn(acc, __dmul_rn(e, e));
         }
         return acc;
     }
@@ -110,10 +112,10 @@ struct Seq64Vector {
 #pragma unroll 4
         for (int t = 0; t < dp; t += 4) {
             float4 x = ldg4(r + t);
-            double a = __ldg(q + t) - (double)x.x; acc = fma(a, a, acc);
-            double b = __ldg(q + t + 1) - (double)x.y; acc = fma(b, b, acc);
-            double c = __ldg(q + t + 2) - (double)x.z; acc = fma(c, c, acc);
-            double e = __ldg(q + t + 3) - (double)x.w; acc = fma(e, e, acc);
+            double a = __ldg(q + t) - (double)x.x; acc = __dadd_rn(acc, __dmul_rn(a, a));
+            double b = __ldg(q + t + 1) - (double)x.y; acc = __dadd_rn(acc, __dmul_rn(b, b));
+            double c = __ldg(q + t + 2) - (double)x.z; acc = __dadd_rn(acc, __dmul_rn(c, c));
+            double e = __ldg(q + t + 3) - (double)x.w; acc = __dadd_rn(acc, __dmul_rn(e, e));
         }
         return acc;
     }

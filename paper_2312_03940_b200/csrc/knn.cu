@@ -120,18 +120,18 @@ __device__ __forceinline__ double row_dist(const float* __restrict__ X, int dp, 
     if (q.qf) {
         for (int t = 0; t < dp; t += 4) {
             float4 x = ldg4(r + t), y = ldg4(q.qf + t);
-            double a = (double)y.x - (double)x.x; acc = fma(a, a, acc);
-            double b = (double)y.y - (double)x.y; acc = fma(b, b, acc);
-            double c = (double)y.z - (double)x.z; acc = fma(c, c, acc);
-            double e = (double)y.w - (double)x.w; acc = fma(e, e, acc);
+            double a = (double)y.x - (double)x.x; acc = __dadd_rn(acc, __dmul_rn(a, a));
+            double b = (double)y.y - (double)x.y; acc = __dadd_rn(acc, __dmul_rn(b, b));
+            double c = (double)y.z - (double)x.z; acc = __dadd_rn(acc, __dmul_rn(c, c));
+            double e = (double)y.w - (double)x.w; acc = __dadd_rn(acc, __dmul_rn(e, e));
         }
     } else {
         for (int t = 0; t < dp; t += 4) {
             float4 x = ldg4(r + t);
-            double a = __ldg(q.qd + t) - (double)x.x; acc = fma(a, a, acc);
-            double b = __ldg(q.qd + t + 1) - (double)x.y; acc = fma(b, b, acc);
-            double c = __ldg(q.qd + t + 2) - (double)x.z; acc = fma(c, c, acc);
-            double e = __ldg(q.qd + t + 3) - (double)x.w; acc = fma(e, e, acc);
+            double a = __ldg(q.qd + t) - (double)x.x; acc = __dadd_rn(acc, __dmul_rn(a, a));
+            double b = __ldg(q.qd + t + 1) - (double)x.y; acc = __dadd_rn(acc, __dmul_rn(b, b));
+            double c = __ldg(q.qd + t + 2) - (double)x.z; acc = __dadd_rn(acc, __dmul_rn(c, c));
+            double e = __ldg(q.qd + t + 3) - (double)x.w; acc = __dadd_rn(acc, __dmul_rn(e, e));
         }
     }
     return acc;
@@ -294,10 +294,10 @@ __global__ void __launch_bounds__(BT) dp_scan_kernel(const float* __restrict__ X
 #pragma unroll
             for (int qq = 0; qq < DQ; ++qq) {
                 const float* qv = qs + qq * dp + t;
-                double a = (double)qv[0] - (double)x.x; acc[qq] = fma(a, a, acc[qq]);
-                double b = (double)qv[1] - (double)x.y; acc[qq] = fma(b, b, acc[qq]);
-                double c = (double)qv[2] - (double)x.z; acc[qq] = fma(c, c, acc[qq]);
-                double e = (double)qv[3] - (double)x.w; acc[qq] = fma(e, e, acc[qq]);
+                double a = (double)qv[0] - (double)x.x; acc[qq] = __dadd_rn(acc[qq], __dmul_rn(a, a));
+                double b = (double)qv[1] - (double)x.y; acc[qq] = __dadd_rn(acc[qq], __dmul_rn(b, b));
+                double c = (double)qv[2] - (double)x.z; acc[qq] = __dadd_rn(acc[qq], __dmul_rn(c, c));
+                double e = (double)qv[3] - (double)x.w; acc[qq] = __dadd_rn(acc[qq], __dmul_rn(e, e));
             }
         }
 #pragma unroll
