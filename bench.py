@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark: end-to-end ANN density-peaks clustering (points/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C2] [--n N_POINTS] [--no-cpu-baseline]
+
+A step is one full pass of the hot path over the configuration's synthetic
+point set (BASELINE.json configs[1] = C2 by default: n=100,000 d=128
+SIFT-shaped, Vamana R=64 L=128 alpha=1.1, kth_normalized k=16, doubling from
+2k, 100 product centers): graph build, kNN densities, dependent points,
+policies + union-find labels, all on the GPU.  `value` = points/s with the
+points already resident in HBM; L2 is flushed (a 256 MiB write) before every
+timed step because C2 (51 MB) fits in the 126 MB L2.  `e2e` = the same
+through the public API (`run_pipeline(PointSet(host array))`) with the
+host->device upload of the points and the device->host read of every result
+array inside the timed region.
+
+Multi-GPU (torchrun, one rank per GPU): each rank runs its own replica of the
+workload (replicas only in this round -- see DESIGN.md, multi-GPU), so per-GPU
+work is fixed ("scaling": "weak"); times are the max over ranks.
+
+--impl reference times the reference algorithm's CPU implementation on the
+host cores: the oracle/ C restatement of the reference's numba kernels
+(OpenMP over all host threads) driving the same pipeline; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "points/sec end-to-end ANN-DPC at 1/2/4/8 B200; dep-point queries/s; % roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        pk = json.load(open(path))
+        return pk["hbm_gbs"], pk["bf16_tflops"], "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- CPU baseline
+
+
+def cpu_pipeline(name, n_override=None):
+    """The reference algorithm on the host cores via the oracle C restatement."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    from paper_2312_03940_b200 import workloads
+
+    w = workloads.WORKLOADS[name]
+    cores = os.cpu_count() or 1
+    if n_override is not None:
+        n = n_override
+    else:
+        # bounded sample: the full configuration when the host has many cores,
+        # otherwise a smaller instance of the same generator (~10-30 s)
+        n = w.n if cores >= 48 else max(10_000, int(w.n * cores / 64))
+    comps = max(1, int(round(w.components * n / w.n)))
+    data, _ = workloads.generate(name, n=n, components=comps)
+    oracle.build()
+    oracle.set_num_threads(cores)
+    t = time.perf_counter()
+    out = oracle.pipeline(data, index="vamana", R=w.R, L_build=w.L, L=w.L, alpha=w.alpha, seed=0, k=w.k,
+                          density_kind=w.density, center_policy=("product", max(1, min(w.n_centers, comps))),
+                          rho_min=0.0, initial_k=2 * w.k, threshold=300)
+    secs = time.perf_counter() - t
+    sample = (f"full {name} pipeline" if n == w.n else f"{name}-generator instance n={n} ({comps} comps)") + \
+        f" through oracle/ (C restatement of _kernels.py + numpy stages), OpenMP {cores} threads"
+    return n / secs, cores, sample, secs, out["timings"]
+
+
+# ---------------------------------------------------------------------------- reference arm
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2312_03940_b200 import workloads
+
+    w = workloads.WORKLOADS[args.config]
+    for _ in range(args.warmup):
+        cpu_pipeline(args.config, n_override=min(w.n, 5_000))
+    vals, total = [], 0.0
+    info = None
+    for _ in range(args.steps):
+        v, cores, sample, secs, timings = cpu_pipeline(args.config, args.n)
+        vals.append(v)
+        total += secs
+        info = (cores, sample, timings)
+    value = float(np.mean(vals))
+    cores, sample, timings = info
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args.config, args.n, 1),
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "stage_seconds": timings,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(name, n_override, n_gpus):
+    from paper_2312_03940_b200 import workloads
+
+    w = workloads.WORKLOADS[name]
+    n = n_override or w.n
+    return {"workload": f"{name}: n={n} d={w.d} Vamana R={w.R} L={w.L} alpha={w.alpha} {w.density} k={w.k} "
+                        f"ProductCenter({w.n_centers}) doubling from {2 * w.k}, threshold 300",
+            "n": n, "d": w.d, "R": w.R, "L": w.L, "k": w.k, "density": w.density,
+            "parallelism": f"replicas x{n_gpus}", "l2": "flushed (256 MiB write) before every timed step"}
+
+
+# ---------------------------------------------------------------------------- our arm
+
+
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_03940_b200 as pk
+    from paper_2312_03940_b200 import _lib, vamana, workloads
+    from paper_2312_03940_b200.cluster import run_pipeline_device
+    from paper_2312_03940_b200.core import upload_points
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    name = args.config
+    w = workloads.WORKLOADS[name]
+    n = args.n or w.n
+    comps = w.components if args.n is None else max(1, int(round(w.components * n / w.n)))
+    data, truth = workloads.generate(name, n=n, components=comps)
+    kw = workloads.pipeline_args(name, pk, n_centers=min(w.n_centers, comps))
+
+    dev_pts = upload_points(data)
+    p = pk.PointSet(data).attach_device(dev_pts)
+    _ = p.mode
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (untimed)
+    for _ in range(args.warmup):
+        run_pipeline_device(p, **kw)
+    torch.cuda.synchronize()
+
+    build_stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    beam_stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    vamana.STATS["build"] = build_stats
+    vamana.STATS["beam"] = beam_stats
+    _lib.prof_collect(reset=True)
+    _lib.prof_enable(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    total_ms = 0.0
+    stage = {"index": 0.0, "density": 0.0, "dependent": 0.0, "unionfind": 0.0}
+    rounds = []
+    last = None
+    stream = torch.cuda.current_stream()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        trace = []
+        last = run_pipeline_device(p, **kw, trace=trace)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        total_ms += e0.elapsed_time(e1)
+        for kk_, v in last["timings"].items():
+            stage[kk_] += v
+        rounds = trace
+    clk = clocks.stop()
+    _lib.prof_enable(False)
+    prof = _lib.prof_collect(reset=True)
+    vamana.STATS["build"] = None
+    vamana.STATS["beam"] = None
+
+    t_local = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_step = float(t_local.item()) / args.steps
+    value = world * n / (ms_step / 1e3)
+
+    # quality of the last timed run (ARI vs generator labels)
+    labels = _lib.to_host(last["labels"])
+    ari_truth = pk.ari(labels, truth)
+
+    # end-to-end through the public API with host buffers
+    pinned = torch.from_numpy(np.ascontiguousarray(data)).pin_memory()
+    host_view = pinned.numpy()
+    e2e_ms = 0.0
+    h2d = d2h = 0
+    for _ in range(args.e2e_steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = pk.run_pipeline(pk.PointSet(host_view), **kw)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms += e0.elapsed_time(e1)
+        h2d = n * w.d * 4
+        st = res.state
+        d2h = sum(a.nbytes for a in (st.rho, st.lam, st.delta, st.neighbors.ids, st.neighbors.dists,
+                                     res.clustering.labels, res.clustering.centers, res.clustering.noise))
+    t_e2e = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = world * n / (float(t_e2e.item()) / args.e2e_steps / 1e3)
+
+    # roofline of the dominant kernel
+    hbm, tflops, peak_kind = peaks()
+    launches = sum(c for c, _ in prof.values())
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    dom_name, (dom_cnt, dom_ms) = dom
+    bs = _lib.to_host(build_stats) / args.steps
+    be = _lib.to_host(beam_stats) / args.steps
+    s = int(np.ceil(np.sqrt(n)))
+    d4 = w.d * 4
+    if dom_name.startswith("build_batch"):
+        # per inserted point: non-seed unique search evaluations + adjacency rows + current out-row
+        evals_nonseed = bs[0] - n * s
+        alg_bytes = evals_nonseed * d4 + bs[3] * w.R * 4
+        unit_desc = "search gather bytes (unique non-seed evals x 4d + expansions x 4R) over all inserted points"
+    elif dom_name.startswith("beam_knn"):
+        evals_nonseed = be[0] - (n * s)
+        alg_bytes = evals_nonseed * d4 + be[1] * w.R * 4
+        unit_desc = "gather bytes (unique non-seed evals x 4d + expansions x 4R) over all queries"
+    else:
+        alg_bytes = None
+        unit_desc = "n/a"
+    per_launch_ms = dom_ms / max(dom_cnt, 1)
+    per_step_launches = dom_cnt / args.steps
+    achieved = None
+    if alg_bytes is not None:
+        achieved = (alg_bytes / 1e9) / (dom_ms / args.steps / 1e3)  # GB/s averaged over the step's launches
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample, secs, timings = cpu_pipeline(name, args.n)
+        cpu = {"value": v, "unit": "points/s", "cores": cores, "kind": "port", "sample": sample,
+               "seconds": secs}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if p.mode == 0 else "f32 (exact: integer data)",
+            "data": f"synthetic ({name} generator, seed 0)",
+            "config": workload_config(name, args.n, world),
+            "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                         "peak_source": peak_kind, "algorithmic_bytes_per_step": alg_bytes,
+                         "launches_per_step": per_step_launches, "avg_launch_ms": per_launch_ms,
+                         "kernel_share_of_step": dom_ms / args.steps / ms_step, "definition": unit_desc},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches / args.steps) * args.steps,
+            "gpu_launches_per_step": launches / args.steps,
+            "clocks": clk,
+            "stage_ms": {k_: v / args.steps * 1e3 for k_, v in stage.items()},
+            "dependent_rounds": rounds,
+            "kernels_ms_per_step": {k_: round(v[1] / args.steps, 4) for k_, v in sorted(prof.items(),
+                                                                                      key=lambda kv: -kv[1][1])},
+            "counters_per_step": {"build": bs.tolist(), "beam": be.tolist()},
+            "ari_vs_generator": ari_truth,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -41,6 +41,14 @@ const char* pk_last_error(void);
 /* number of SMs / opt-in shared memory per block of the current device (host out) */
 int pk_device_info(int* sm_count, int* smem_optin);
 
+/* Launch accounting (no reference counterpart; used by bench.py): every
+ * kernel launch is counted per kernel name; with pk_prof_enable(1) each launch
+ * is also bracketed by CUDA events on its stream.  pk_prof_collect writes
+ * "name count total_ms\n" lines into buf (host) and returns the full length;
+ * reset != 0 clears the counters. */
+void pk_prof_enable(int on);
+int pk_prof_collect(char* buf, int len, int reset);
+
 /* 1 in *out_flag (device int) when the data is integer-valued with
  * d * (2 max|x|)^2 < 2^24, i.e. PK_MODE_EXACT32 is bit-exact.
  * Replaces: nothing (reference always uses _kernels.py:21-38). */
@@ -51,7 +59,8 @@ int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d, int* out_
  * recompute of VamanaIndex.knn_batch (vamana.py:220-225).
  * out_ids (m,kk) int64 (-1 pad), out_sqd (m,kk) float64 (+inf pad),
  * out_counts (m,) int64 (counts BEFORE the fallback), kk = min(k, n-1).
- * out_evals (device int64, may be null) accumulates distance evaluations.
+ * out_evals (device int64[2], may be null) accumulates distance evaluations
+ * and expansions (adjacency rows read).
  * hash_bits: log2 of the per-query seen-table size (0 = automatic). */
 int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, const int32_t* adj, int64_t R,
                 const int32_t* deg, const int32_t* starts, int64_t s, const int64_t* qids, int64_t m,

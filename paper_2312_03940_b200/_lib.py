@@ -78,6 +78,10 @@ def lib():
         L.pk_last_error.restype = ctypes.c_char_p
         L.pk_version.restype = ctypes.c_int
         L.pk_device_info.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        L.pk_prof_enable.argtypes = [ctypes.c_int]
+        L.pk_prof_enable.restype = None
+        L.pk_prof_collect.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
+        L.pk_prof_collect.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -121,3 +125,18 @@ def to_dev(a: np.ndarray, dtype=None) -> torch.Tensor:
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
+
+
+def prof_enable(on: bool) -> None:
+    lib().pk_prof_enable(1 if on else 0)
+
+
+def prof_collect(reset: bool = True) -> dict:
+    """{kernel name: (launches, total device ms)} since the last reset."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    lib().pk_prof_collect(buf, len(buf), 1 if reset else 0)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split()
+        out[name] = (int(cnt), float(ms))
+    return out

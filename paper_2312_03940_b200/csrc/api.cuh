@@ -54,4 +54,16 @@ inline size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
 
 int choose_hash(int L, int hash_bits);
 
+// ---- launch accounting -------------------------------------------------------
+// Every kernel launch site opens a ProfScope: launches are always counted per
+// kernel name; with pk_prof_enable(1) a CUDA event pair brackets the launch on
+// its stream so the host can read per-kernel device time (bench.py roofline).
+struct ProfScope {
+    const char* name;
+    cudaStream_t st;
+    int slot;
+    ProfScope(const char* n, cudaStream_t s);
+    ~ProfScope();
+};
+
 }  // namespace pk

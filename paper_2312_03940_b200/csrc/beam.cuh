@@ -174,7 +174,7 @@ struct WarpBeam {
         for (int b = 0; b < P.s; b += 32) {
             const int cnt = min(32, P.s - b);
             unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
-            if (!P.start_bm && lane < cnt) sm.hash[seen_slot(id, sm.hmask)] = id;
+            if (!P.start_bm && lane < cnt) seen_or_insert(sm.hash, sm.hmask, id);
             double dd = dist.eval(P.X, (int)id, cnt);
             if (lane == 0) evals += cnt;
             merge(dd, id, lane < cnt);
@@ -223,11 +223,7 @@ struct WarpBeam {
                 int w = e0 + lane < nd ? __ldg(row + e0 + lane) : -1;
                 bool cand = w >= 0;
                 if (cand && P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u)) cand = false;
-                if (cand) {
-                    unsigned sl = seen_slot((unsigned)w, sm.hmask);
-                    if (sm.hash[sl] == (unsigned)w) cand = false;
-                    else sm.hash[sl] = (unsigned)w;
-                }
+                if (cand && seen_or_insert(sm.hash, sm.hmask, (unsigned)w)) cand = false;
                 unsigned b = __ballot_sync(PK_FULL, cand);
                 const int c = __popc(b);
                 if (!c) continue;

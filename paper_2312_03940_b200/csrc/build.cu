@@ -539,7 +539,10 @@ int run_build(const float* x, int n, int dp, int R, int L, double alpha, const i
     PK_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)n, st));
     PK_CHECK(cudaMemsetAsync(err, 0, sizeof(unsigned), st));
     PK_CHECK(cudaMemsetAsync(bm, 0, words * 4, st));
-    starts_bitmap_kernel2<<<grid_for(s, 256), 256, 0, st>>>(starts, s, bm);
+    {
+        ProfScope _ps("starts_bitmap_kernel2", st);
+        starts_bitmap_kernel2<<<grid_for(s, 256), 256, 0, st>>>(starts, s, bm);
+    }
 
     BuildArgs A;
     A.P = SearchParams{x, dp, adj, R, deg, starts, s, bm};
@@ -580,23 +583,41 @@ int run_build(const float* x, int n, int dp, int R, int L, double alpha, const i
         A.bids = order + lo;
         A.m = m;
         const int g = std::min(max_grid, (m + wpb - 1) / wpb);
-        bk<<<g, 32 * wpb, wb * wpb, st>>>(A);
+        {
+            ProfScope _ps("build_batch_kernel", st);
+            bk<<<g, 32 * wpb, wb * wpb, st>>>(A);
+        }
         PK_CHECK_LAUNCH("build_batch_kernel");
         const int ubb = (int)std::min<long long>(n, (long long)m * R);
         PK_CHECK(cudaMemsetAsync(ntargets, 0, sizeof(int), st));
         PK_CHECK(cudaMemsetAsync(sizes, 0, sizeof(int) * ((size_t)ubb + 1), st));
         PK_CHECK(cudaMemsetAsync(fill, 0, sizeof(int) * (size_t)ubb, st));
-        commit_kernel<<<grid_for((long long)m * 32, 256), 256, 0, st>>>(order + lo, m, R, new_ids, new_len, adj, deg,
-                                                                         cnt, tslot, targets, ntargets);
+        {
+            ProfScope _ps("commit_kernel", st);
+            commit_kernel<<<grid_for((long long)m * 32, 256), 256, 0, st>>>(order + lo, m, R, new_ids, new_len, adj, deg,
+                                                                             cnt, tslot, targets, ntargets);
+        }
         PK_CHECK_LAUNCH("commit_kernel");
-        sizes_kernel<<<grid_for(ubb, 256), 256, 0, st>>>(targets, ntargets, cnt, sizes);
+        {
+            ProfScope _ps("sizes_kernel", st);
+            sizes_kernel<<<grid_for(ubb, 256), 256, 0, st>>>(targets, ntargets, cnt, sizes);
+        }
         PK_CHECK_LAUNCH("sizes_kernel");
-        PK_CHECK(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, sizes, offs, ubb + 1, st));
-        scatter_kernel<<<grid_for((long long)m * R, 256), 256, 0, st>>>(order + lo, m, R, new_ids, new_len, tslot,
-                                                                         offs, fill, adds);
+        {
+            ProfScope _ps("cub_DeviceScan_ExclusiveSum", st);
+            PK_CHECK(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, sizes, offs, ubb + 1, st));
+        }
+        {
+            ProfScope _ps("scatter_kernel", st);
+            scatter_kernel<<<grid_for((long long)m * R, 256), 256, 0, st>>>(order + lo, m, R, new_ids, new_len, tslot,
+                                                                             offs, fill, adds);
+        }
         PK_CHECK_LAUNCH("scatter_kernel");
         const int gr = std::min(grid_r, (ubb + wpbr - 1) / wpbr);
-        rk<<<gr, 32 * wpbr, wbr * wpbr, st>>>(B);
+        {
+            ProfScope _ps("reverse_kernel", st);
+            rk<<<gr, 32 * wpbr, wbr * wpbr, st>>>(B);
+        }
         PK_CHECK_LAUNCH("reverse_kernel");
     }
     unsigned herr = 0;
@@ -657,11 +678,14 @@ extern "C" int pk_robust_prune(const float* x, int64_t n, int64_t dp, int64_t p,
     int* so = nullptr;
     PK_CHECK(scratch(&so, (size_t)(R > 0 ? R : 1), st));
     PK_CHECK(cudaFuncSetAttribute(robust_prune_api_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    robust_prune_api_kernel<<<1, 32, bytes, st>>>(x, (int)dp, (unsigned)p, reinterpret_cast<const long long*>(cand_ids),
-                                                  cand_sqd, (int)m, reinterpret_cast<const long long*>(cur_ids),
-                                                  (int)dcount, alpha * alpha, (int)R, cap,
-                                                  reinterpret_cast<long long*>(out),
-                                                  reinterpret_cast<long long*>(out_count), so);
+    {
+        ProfScope _ps("robust_prune_api_kernel", st);
+        robust_prune_api_kernel<<<1, 32, bytes, st>>>(x, (int)dp, (unsigned)p, reinterpret_cast<const long long*>(cand_ids),
+                                                      cand_sqd, (int)m, reinterpret_cast<const long long*>(cur_ids),
+                                                      (int)dcount, alpha * alpha, (int)R, cap,
+                                                      reinterpret_cast<long long*>(out),
+                                                      reinterpret_cast<long long*>(out_count), so);
+    }
     PK_CHECK_LAUNCH("robust_prune_api_kernel");
     release(so, st);
     return 0;
@@ -676,9 +700,18 @@ extern "C" int pk_nearest_to_centroid(const float* x, int64_t n, int64_t dp, int
     PK_CHECK(scratch(&cen, (size_t)dp, st));
     PK_CHECK(scratch(&bd, g, st));
     PK_CHECK(scratch(&bi, g, st));
-    centroid_kernel<<<(unsigned)((dp + 127) / 128), 128, 0, st>>>(x, (int)n, (int)dp, cen);
-    nearest_kernel<<<g, 256, 0, st>>>(x, (int)n, (int)dp, cen, bd, bi);
-    nearest_final_kernel<<<1, 1, 0, st>>>(bd, bi, g, reinterpret_cast<long long*>(out));
+    {
+        ProfScope _ps("centroid_kernel", st);
+        centroid_kernel<<<(unsigned)((dp + 127) / 128), 128, 0, st>>>(x, (int)n, (int)dp, cen);
+    }
+    {
+        ProfScope _ps("nearest_kernel", st);
+        nearest_kernel<<<g, 256, 0, st>>>(x, (int)n, (int)dp, cen, bd, bi);
+    }
+    {
+        ProfScope _ps("nearest_final_kernel", st);
+        nearest_final_kernel<<<1, 1, 0, st>>>(bd, bi, g, reinterpret_cast<long long*>(out));
+    }
     PK_CHECK_LAUNCH("nearest_to_centroid");
     release(cen, st);
     release(bd, st);

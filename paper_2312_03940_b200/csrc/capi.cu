@@ -1,6 +1,10 @@
 // C-ABI plumbing: error strings, device properties.
 #include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/peakann_b200.h"
 #include "api.cuh"
@@ -38,7 +42,78 @@ int max_smem_optin() {
     return g_smem;
 }
 
+// ---- launch accounting ---------------------------------------------------------
+struct ProfRecord {
+    std::string name;
+    cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::map<std::string, long long> g_counts;
+static std::vector<ProfRecord> g_records;
+static std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t take_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(const char* n, cudaStream_t s) : name(n), st(s), slot(-1) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_counts[name] += 1;
+    if (g_prof_on) {
+        ProfRecord r{name, take_event(), take_event()};
+        cudaEventRecord(r.a, st);
+        g_records.push_back(r);
+        slot = (int)g_records.size() - 1;
+    }
+}
+
+ProfScope::~ProfScope() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEventRecord(g_records[slot].b, st);
+}
+
 }  // namespace pk
+
+extern "C" void pk_prof_enable(int on) {
+    std::lock_guard<std::mutex> lk(pk::g_prof_mu);
+    pk::g_prof_on = on != 0;
+}
+
+// "name count total_ms\n" per kernel; counts since the last reset, times of the
+// event-bracketed launches since the last collect.  reset != 0 clears both.
+extern "C" int pk_prof_collect(char* buf, int len, int reset) {
+    std::lock_guard<std::mutex> lk(pk::g_prof_mu);
+    std::map<std::string, double> ms;
+    for (auto& r : pk::g_records) {
+        cudaEventSynchronize(r.b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        ms[r.name] += t;
+        pk::g_event_pool.push_back(r.a);
+        pk::g_event_pool.push_back(r.b);
+    }
+    pk::g_records.clear();
+    std::string out;
+    for (auto& kv : pk::g_counts) {
+        char line[256];
+        snprintf(line, sizeof line, "%s %lld %.6f\n", kv.first.c_str(), kv.second, ms[kv.first]);
+        out += line;
+    }
+    if (reset) pk::g_counts.clear();
+    int n = (int)out.size() < len - 1 ? (int)out.size() : len - 1;
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+    return (int)out.size();
+}
 
 extern "C" int pk_version(void) { return 1; }
 

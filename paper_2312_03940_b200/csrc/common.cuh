@@ -52,9 +52,26 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-// hash for the per-query "seen" table (lossy, direct-mapped)
+// per-query "seen" table: open addressing, linear probe window of 8 slots,
+// lossy when the window is full (the id then overwrites its home slot).  A
+// lost id only costs a re-evaluation; ids are never reported seen falsely.
 __device__ __forceinline__ unsigned seen_slot(unsigned id, unsigned mask) {
     return (id * 2654435761u >> 7) & mask;
+}
+__device__ __forceinline__ bool seen_or_insert(unsigned* hash, unsigned mask, unsigned id) {
+    const unsigned h = seen_slot(id, mask);
+#pragma unroll
+    for (unsigned i = 0; i < 8; ++i) {
+        const unsigned s = (h + i) & mask;
+        const unsigned v = hash[s];
+        if (v == id) return true;
+        if (v == 0xffffffffu) {
+            hash[s] = id;
+            return false;
+        }
+    }
+    hash[h] = id;
+    return false;
 }
 
 // ---- distance policies ---------------------------------------------------------

@@ -267,7 +267,10 @@ int sort_pairs_u64(const unsigned long long* kin, unsigned long long* kout, cons
     PK_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0, 64, st));
     void* tmp = nullptr;
     PK_CHECK(cudaMallocAsync(&tmp, bytes + 16, st));
-    PK_CHECK(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, 64, st));
+    {
+        ProfScope _ps("cub_DeviceRadixSort_SortPairs", st);
+        PK_CHECK(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, 64, st));
+    }
     release(tmp, st);
     return 0;
 }
@@ -279,7 +282,10 @@ int compact_flagged(const long long* in, const unsigned char* flags, long long n
     PK_CHECK(cub::DeviceSelect::Flagged(nullptr, bytes, in, flags, out, count, (int)n, st));
     void* tmp = nullptr;
     PK_CHECK(cudaMallocAsync(&tmp, bytes + 16, st));
-    PK_CHECK(cub::DeviceSelect::Flagged(tmp, bytes, in, flags, out, count, (int)n, st));
+    {
+        ProfScope _ps("cub_DeviceSelect_Flagged", st);
+        PK_CHECK(cub::DeviceSelect::Flagged(tmp, bytes, in, flags, out, count, (int)n, st));
+    }
     release(tmp, st);
     return 0;
 }
@@ -307,11 +313,20 @@ extern "C" int pk_densities(int kind, const int64_t* ids, const double* dists, i
     if (kind == PK_DENSITY_KTH_NORMALIZED) {
         double* base = nullptr;
         PK_CHECK(scratch(&base, (size_t)n, st));
-        density_rows_kernel<<<g, 128, 0, st>>>(PK_DENSITY_KTH, dists, n, (int)k, base, tmp);
-        normalize_kernel<<<g, 128, 0, st>>>(base, reinterpret_cast<const long long*>(ids), n, (int)k, rho, tmp);
+        {
+            ProfScope _ps("density_rows_kernel", st);
+            density_rows_kernel<<<g, 128, 0, st>>>(PK_DENSITY_KTH, dists, n, (int)k, base, tmp);
+        }
+        {
+            ProfScope _ps("normalize_kernel", st);
+            normalize_kernel<<<g, 128, 0, st>>>(base, reinterpret_cast<const long long*>(ids), n, (int)k, rho, tmp);
+        }
         release(base, st);
     } else {
-        density_rows_kernel<<<g, 128, 0, st>>>(kind, dists, n, (int)k, rho, tmp);
+        {
+            ProfScope _ps("density_rows_kernel", st);
+            density_rows_kernel<<<g, 128, 0, st>>>(kind, dists, n, (int)k, rho, tmp);
+        }
     }
     PK_CHECK_LAUNCH("density kernels");
     release(tmp, st);
@@ -324,8 +339,11 @@ extern "C" int pk_normalize_rho(const double* base, const int64_t* ids, int64_t 
     if (n <= 0) return 0;
     double* tmp = nullptr;
     PK_CHECK(scratch(&tmp, (size_t)n * k, st));
-    normalize_kernel<<<grid_for(n, 128), 128, 0, st>>>(base, reinterpret_cast<const long long*>(ids), n, (int)k, out,
-                                                      tmp);
+    {
+        ProfScope _ps("normalize_kernel", st);
+        normalize_kernel<<<grid_for(n, 128), 128, 0, st>>>(base, reinterpret_cast<const long long*>(ids), n, (int)k, out,
+                                                          tmp);
+    }
     PK_CHECK_LAUNCH("normalize_kernel");
     release(tmp, st);
     return 0;
@@ -342,12 +360,18 @@ extern "C" int pk_rank_order(const double* rho, int64_t n, int64_t* rank, int* n
     PK_CHECK(scratch(&v1, (size_t)n, st));
     PK_CHECK(cudaMemsetAsync(nan_flag, 0, sizeof(int), st));
     int g = grid_for(n, 256);
-    rank_keys_kernel<<<g, 256, 0, st>>>(rho, n, k0, v0, nan_flag);
+    {
+        ProfScope _ps("rank_keys_kernel", st);
+        rank_keys_kernel<<<g, 256, 0, st>>>(rho, n, k0, v0, nan_flag);
+    }
     PK_CHECK_LAUNCH("rank_keys_kernel");
     // stable LSD radix sort: equal densities keep ascending ids (lexsort, density.py:126)
     int rc = sort_pairs_u64(k0, k1, v0, v1, n, st);
     if (rc) return rc;
-    rank_scatter_kernel<<<g, 256, 0, st>>>(v1, n, reinterpret_cast<long long*>(rank));
+    {
+        ProfScope _ps("rank_scatter_kernel", st);
+        rank_scatter_kernel<<<g, 256, 0, st>>>(v1, n, reinterpret_cast<long long*>(rank));
+    }
     PK_CHECK_LAUNCH("rank_scatter_kernel");
     for (void* p : {(void*)k0, (void*)k1, (void*)v0, (void*)v1}) release(p, st);
     return 0;
@@ -368,9 +392,12 @@ extern "C" int pk_resolve_lists(const int64_t* rank, const int64_t* qids, int64_
     if (k == 0) {
         PK_CHECK(cudaMemsetAsync(fl, 1, (size_t)m, st));
     } else {
-        resolve_kernel<<<grid_for(m, 256), 256, 0, st>>>(
-            reinterpret_cast<const long long*>(rank), reinterpret_cast<const long long*>(qids), m,
-            reinterpret_cast<const long long*>(ids), dists, (int)k, reinterpret_cast<long long*>(lam), delta, fl, skip);
+        {
+            ProfScope _ps("resolve_kernel", st);
+            resolve_kernel<<<grid_for(m, 256), 256, 0, st>>>(
+                reinterpret_cast<const long long*>(rank), reinterpret_cast<const long long*>(qids), m,
+                reinterpret_cast<const long long*>(ids), dists, (int)k, reinterpret_cast<long long*>(lam), delta, fl, skip);
+        }
         PK_CHECK_LAUNCH("resolve_kernel");
     }
     // unresolved qids, input order preserved
@@ -385,9 +412,12 @@ extern "C" int pk_scatter_dependents(const int64_t* qids, int64_t m, const int64
                                      int64_t* lam, double* delta, void* stream) {
     if (m <= 0) return 0;
     cudaStream_t st = as_stream(stream);
-    scatter_dep_kernel<<<grid_for(m, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(qids), m,
-                                                        reinterpret_cast<const long long*>(src_id), src_sqd,
-                                                        reinterpret_cast<long long*>(lam), delta);
+    {
+        ProfScope _ps("scatter_dep_kernel", st);
+        scatter_dep_kernel<<<grid_for(m, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(qids), m,
+                                                            reinterpret_cast<const long long*>(src_id), src_sqd,
+                                                            reinterpret_cast<long long*>(lam), delta);
+    }
     PK_CHECK_LAUNCH("scatter_dep_kernel");
     return 0;
 }
@@ -395,8 +425,11 @@ extern "C" int pk_scatter_dependents(const int64_t* qids, int64_t m, const int64
 extern "C" int pk_argmax_rank(const int64_t* rank, int64_t n, int64_t* out, void* stream) {
     if (n <= 0) return 0;
     cudaStream_t st = as_stream(stream);
-    argmax_rank_kernel<<<grid_for(n, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(rank), n,
-                                                        reinterpret_cast<long long*>(out));
+    {
+        ProfScope _ps("argmax_rank_kernel", st);
+        argmax_rank_kernel<<<grid_for(n, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(rank), n,
+                                                            reinterpret_cast<long long*>(out));
+    }
     PK_CHECK_LAUNCH("argmax_rank_kernel");
     return 0;
 }
@@ -405,14 +438,20 @@ extern "C" int pk_flag_noise(const double* rho, int64_t n, double rho_min, uint8
                              void* stream) {
     if (n <= 0) return 0;
     cudaStream_t st = as_stream(stream);
-    noise_kernel<<<grid_for(n, 256), 256, 0, st>>>(rho, n, rho_min, noise);
+    {
+        ProfScope _ps("noise_kernel", st);
+        noise_kernel<<<grid_for(n, 256), 256, 0, st>>>(rho, n, rho_min, noise);
+    }
     PK_CHECK_LAUNCH("noise_kernel");
     if (n_noise) {
         size_t bytes = 0;
         PK_CHECK(cub::DeviceReduce::Sum(nullptr, bytes, noise, reinterpret_cast<long long*>(n_noise), (int)n, st));
         void* tmp = nullptr;
         PK_CHECK(cudaMallocAsync(&tmp, bytes + 16, st));
-        PK_CHECK(cub::DeviceReduce::Sum(tmp, bytes, noise, reinterpret_cast<long long*>(n_noise), (int)n, st));
+        {
+            ProfScope _ps("cub_DeviceReduce_Sum", st);
+            PK_CHECK(cub::DeviceReduce::Sum(tmp, bytes, noise, reinterpret_cast<long long*>(n_noise), (int)n, st));
+        }
         release(tmp, st);
     }
     return 0;
@@ -422,7 +461,10 @@ extern "C" int pk_centers_threshold(const double* delta, const uint8_t* noise, i
                                     uint8_t* center, void* stream) {
     if (n <= 0) return 0;
     cudaStream_t st = as_stream(stream);
-    threshold_kernel<<<grid_for(n, 256), 256, 0, st>>>(delta, noise, n, delta_min, center);
+    {
+        ProfScope _ps("threshold_kernel", st);
+        threshold_kernel<<<grid_for(n, 256), 256, 0, st>>>(delta, noise, n, delta_min, center);
+    }
     PK_CHECK_LAUNCH("threshold_kernel");
     return 0;
 }
@@ -440,16 +482,25 @@ extern "C" int pk_centers_product(const double* rho, const double* delta, const 
     PK_CHECK(scratch(&v0, (size_t)n, st));
     PK_CHECK(scratch(&v1, (size_t)n, st));
     int g = grid_for(n, 256);
-    product_keys_kernel<<<g, 256, 0, st>>>(rho, delta, noise, n, kp, kdl, v0);
+    {
+        ProfScope _ps("product_keys_kernel", st);
+        product_keys_kernel<<<g, 256, 0, st>>>(rho, delta, noise, n, kp, kdl, v0);
+    }
     PK_CHECK_LAUNCH("product_keys_kernel");
     // lexsort((id, -delta, -prod)): stable sort by -delta, then stable sort by -prod
     int rc = sort_pairs_u64(kdl, ka, v0, v1, n, st);
     if (rc) return rc;
-    gather_keys_kernel<<<g, 256, 0, st>>>(kp, v1, n, ka);
+    {
+        ProfScope _ps("gather_keys_kernel", st);
+        gather_keys_kernel<<<g, 256, 0, st>>>(kp, v1, n, ka);
+    }
     rc = sort_pairs_u64(ka, kb, v1, v0, n, st);
     if (rc) return rc;
     PK_CHECK(cudaMemsetAsync(center, 0, (size_t)n, st));
-    mark_first_kernel<<<grid_for(n_c, 256), 256, 0, st>>>(v0, n_c, center);
+    {
+        ProfScope _ps("mark_first_kernel", st);
+        mark_first_kernel<<<grid_for(n_c, 256), 256, 0, st>>>(v0, n_c, center);
+    }
     PK_CHECK_LAUNCH("mark_first_kernel");
     for (void* p : {(void*)kp, (void*)kdl, (void*)ka, (void*)kb, (void*)v0, (void*)v1}) release(p, st);
     return 0;
@@ -459,8 +510,11 @@ extern "C" int pk_centers_local(const int64_t* rank, const int64_t* nbr_ids, int
                                 int64_t n, uint8_t* center, void* stream) {
     if (n <= 0) return 0;
     cudaStream_t st = as_stream(stream);
-    local_kernel<<<grid_for(n, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(rank),
-                                                  reinterpret_cast<const long long*>(nbr_ids), (int)k, noise, n, center);
+    {
+        ProfScope _ps("local_kernel", st);
+        local_kernel<<<grid_for(n, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(rank),
+                                                      reinterpret_cast<const long long*>(nbr_ids), (int)k, noise, n, center);
+    }
     PK_CHECK_LAUNCH("local_kernel");
     return 0;
 }
@@ -468,7 +522,10 @@ extern "C" int pk_centers_local(const int64_t* rank, const int64_t* nbr_ids, int
 extern "C" int pk_promote_orphans(const int64_t* lam, const uint8_t* noise, int64_t n, uint8_t* center, void* stream) {
     if (n <= 0) return 0;
     cudaStream_t st = as_stream(stream);
-    orphan_kernel<<<grid_for(n, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(lam), noise, n, center);
+    {
+        ProfScope _ps("orphan_kernel", st);
+        orphan_kernel<<<grid_for(n, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(lam), noise, n, center);
+    }
     PK_CHECK_LAUNCH("orphan_kernel");
     return 0;
 }
@@ -484,16 +541,28 @@ extern "C" int pk_assign_clusters(const int64_t* lam, const uint8_t* center, con
     PK_CHECK(cudaMemcpyAsync(status, init, sizeof(init), cudaMemcpyHostToDevice, st));
     int g = grid_for(n, 256);
     long long* s = reinterpret_cast<long long*>(status);
-    parent_init_kernel<<<g, 256, 0, st>>>(reinterpret_cast<const long long*>(lam), center, noise, n, a, s);
+    {
+        ProfScope _ps("parent_init_kernel", st);
+        parent_init_kernel<<<g, 256, 0, st>>>(reinterpret_cast<const long long*>(lam), center, noise, n, a, s);
+    }
     // ceil(log2 n) + 1 rounds of pointer jumping reach every root of a forest
     int rounds = 1;
     while ((1ll << rounds) < n) ++rounds;
     for (int r = 0; r <= rounds; ++r) {
-        jump_kernel<<<g, 256, 0, st>>>(a, n, b);
+        {
+            ProfScope _ps("jump_kernel", st);
+            jump_kernel<<<g, 256, 0, st>>>(a, n, b);
+        }
         std::swap(a, b);
     }
-    label_kernel<<<g, 256, 0, st>>>(a, center, noise, n, reinterpret_cast<long long*>(labels), s);
-    status_final_kernel<<<1, 1, 0, st>>>(s);
+    {
+        ProfScope _ps("label_kernel", st);
+        label_kernel<<<g, 256, 0, st>>>(a, center, noise, n, reinterpret_cast<long long*>(labels), s);
+    }
+    {
+        ProfScope _ps("status_final_kernel", st);
+        status_final_kernel<<<1, 1, 0, st>>>(s);
+    }
     PK_CHECK_LAUNCH("assign kernels");
     // the memcpy source is a host stack array: make sure it was consumed
     PK_CHECK(cudaStreamSynchronize(st));
@@ -510,7 +579,10 @@ extern "C" int pk_flags_to_ids(const uint8_t* flags, int64_t n, int64_t* out, in
     }
     long long* iota = nullptr;
     PK_CHECK(scratch(&iota, (size_t)n, st));
-    iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
+    {
+        ProfScope _ps("iota_kernel", st);
+        iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
+    }
     int rc = compact_flagged(iota, flags, n, reinterpret_cast<long long*>(out), reinterpret_cast<long long*>(count), st);
     release(iota, st);
     return rc;

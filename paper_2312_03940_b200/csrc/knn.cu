@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(128) beam_knn_kernel(SearchParams P, const lon
     const int lane = lane_id();
     unsigned char* mine = smem + (size_t)wib * warp_bytes;
     BeamSmem sm = carve_beam(mine, L, H);
-    long long ev = 0;
+    long long ev = 0, ex = 0;
     for (long long t = (long long)blockIdx.x * wpb + wib; t < m; t += (long long)gridDim.x * wpb) {
         const unsigned qi = (unsigned)qids[t];
         auto dist = DistOf<MODE, QV>::make(P.X, P.dp, qi);
@@ -67,9 +67,13 @@ __global__ void __launch_bounds__(128) beam_knn_kernel(SearchParams P, const lon
         }
         if (lane == 0) counts[t] = got;
         ev += wb.evals;
+        ex += wb.vl;
         __syncwarp();
     }
-    if (evals_out && lane == 0 && ev) atomicAdd(reinterpret_cast<unsigned long long*>(evals_out), (unsigned long long)ev);
+    if (evals_out && lane == 0 && ev) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(evals_out), (unsigned long long)ev);
+        atomicAdd(reinterpret_cast<unsigned long long*>(evals_out + 1), (unsigned long long)ex);
+    }
 }
 
 // rows with counts < kk -> list for the exact fallback
@@ -357,23 +361,42 @@ __global__ void fill_ids_kernel(long long* ids, double* d, long long count) {
     }
 }
 
-__global__ void check_exact32_kernel(const float* x, long long total, int dp, int d, int* bad, float* maxabs) {
-    float mx = 0.f;
+__device__ __forceinline__ unsigned ordered_key(float f) {
+    unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float from_ordered(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// range[0] = ordered max, range[1] = ordered min over the real coordinates
+__global__ void check_exact32_kernel(const float* x, long long total, int dp, int d, int* bad, unsigned* range) {
+    unsigned hi = 0u, lo = 0xffffffffu;
     int b = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         if ((int)(i % dp) >= d) continue;
         float v = x[i];
         if (v != rintf(v)) b = 1;
-        mx = fmaxf(mx, fabsf(v));
+        unsigned k = ordered_key(v);
+        hi = max(hi, k);
+        lo = min(lo, k);
     }
     if (b) atomicOr(bad, 1);
-    for (int s = 16; s; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(PK_FULL, mx, s));
-    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(maxabs), __float_as_int(mx));
+    for (int s = 16; s; s >>= 1) {
+        hi = max(hi, __shfl_xor_sync(PK_FULL, hi, s));
+        lo = min(lo, __shfl_xor_sync(PK_FULL, lo, s));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(range, hi);
+        atomicMin(range + 1, lo);
+    }
 }
 
-__global__ void finish_exact32_kernel(const int* bad, const float* maxabs, int d, int* flag) {
-    double m = (double)*maxabs;
-    double bound = (double)d * (2.0 * m) * (2.0 * m);
+// integer coordinates spanning [lo, hi]: every squared distance and every
+// partial sum is an integer <= d * (hi - lo)^2; below 2^24 float32 is exact
+__global__ void finish_exact32_kernel(const int* bad, const unsigned* range, int d, int* flag) {
+    double span = (double)from_ordered(range[0]) - (double)from_ordered(range[1]);
+    double bound = (double)d * span * span;
     *flag = (*bad == 0 && bound < 16777216.0) ? 1 : 0;
 }
 
@@ -428,7 +451,10 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     long long cap = (long long)sm_count() * per_sm;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
-    kern<<<grid, 32 * wpb, wb * wpb, st>>>(P, qids, m, L, kk, H, wb, out_ids, out_d, counts, evals);
+    {
+        ProfScope _ps("beam_knn_kernel", st);
+        kern<<<grid, 32 * wpb, wb * wpb, st>>>(P, qids, m, L, kk, H, wb, out_ids, out_d, counts, evals);
+    }
     PK_CHECK_LAUNCH("beam_knn_kernel");
     return 0;
 }
@@ -464,7 +490,10 @@ int run_brute(const float* x, int n, int dp, const long long* qids, const double
     PK_CHECK(scratch(&scr, (size_t)grid * n, st));
     PK_CHECK(scratch(&sd, (size_t)grid * P, st));
     PK_CHECK(scratch(&si, (size_t)grid * P, st));
-    brute_rows_kernel<<<grid, BT, 0, st>>>(x, n, dp, qids, qvec, rowlist, nrows, m, kk, scr, sd, si, P, out_ids, out_d);
+    {
+        ProfScope _ps("brute_rows_kernel", st);
+        brute_rows_kernel<<<grid, BT, 0, st>>>(x, n, dp, qids, qvec, rowlist, nrows, m, kk, scr, sd, si, P, out_ids, out_d);
+    }
     cudaError_t e = cudaGetLastError();
     release(scr, st);
     release(sd, st);
@@ -480,14 +509,21 @@ using namespace pk;
 extern "C" int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d, int* out_flag, void* stream) {
     cudaStream_t st = as_stream(stream);
     int* bad = nullptr;
-    float* mx = nullptr;
+    unsigned* mx = nullptr;
     PK_CHECK(scratch(&bad, 1, st));
-    PK_CHECK(scratch(&mx, 1, st));
+    PK_CHECK(scratch(&mx, 2, st));
     PK_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), st));
-    PK_CHECK(cudaMemsetAsync(mx, 0, sizeof(float), st));
+    PK_CHECK(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
+    PK_CHECK(cudaMemsetAsync(mx + 1, 0xff, sizeof(unsigned), st));
     long long total = n * dp;
-    check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx);
-    finish_exact32_kernel<<<1, 1, 0, st>>>(bad, mx, (int)d, out_flag);
+    {
+        ProfScope _ps("check_exact32_kernel", st);
+        check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx);
+    }
+    {
+        ProfScope _ps("finish_exact32_kernel", st);
+        finish_exact32_kernel<<<1, 1, 0, st>>>(bad, mx, (int)d, out_flag);
+    }
     PK_CHECK_LAUNCH("check_exact32");
     release(bad, st);
     release(mx, st);
@@ -512,7 +548,10 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, cons
     size_t words = (size_t)(n + 31) / 32;
     PK_CHECK(scratch(&bm, words, st));
     PK_CHECK(cudaMemsetAsync(bm, 0, words * 4, st));
-    start_bitmap_kernel<<<grid_for(s, 256), 256, 0, st>>>(starts, (int)s, bm);
+    {
+        ProfScope _ps("start_bitmap_kernel", st);
+        start_bitmap_kernel<<<grid_for(s, 256), 256, 0, st>>>(starts, (int)s, bm);
+    }
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, bm};
     int H = choose_hash((int)L, hash_bits);
     const long long* q = reinterpret_cast<const long long*>(qids);
@@ -530,7 +569,10 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, cons
         PK_CHECK(scratch(&list, (size_t)m, st));
         PK_CHECK(scratch(&nl, 1, st));
         PK_CHECK(cudaMemsetAsync(nl, 0, sizeof(int), st));
-        short_rows_kernel<<<grid_for(m, 256), 256, 0, st>>>(oc, (int)m, (int)kk, list, nl);
+        {
+            ProfScope _ps("short_rows_kernel", st);
+            short_rows_kernel<<<grid_for(m, 256), 256, 0, st>>>(oc, (int)m, (int)kk, list, nl);
+        }
         PK_CHECK_LAUNCH("short_rows_kernel");
         rc = run_brute(x, (int)n, (int)dp, q, nullptr, list, nl, (int)m, (int)kk, oi, out_sqd, st);
         release(list, st);
@@ -561,17 +603,23 @@ extern "C" int pk_beam_search_single(const float* x, int64_t n, int64_t dp, cons
     if (qid >= 0) {
         auto kern = single_search_kernel<Seq64Member>;
         PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        kern<<<1, 32, bytes, st>>>(P, Seq64Member{x + (size_t)qid * dp, (int)dp}, self, (int)L, (int)k, H,
-                                   reinterpret_cast<long long*>(top_ids), top_sqd, reinterpret_cast<long long*>(top_count),
-                                   reinterpret_cast<long long*>(vis_ids), vis_sqd, (int)vcap,
-                                   reinterpret_cast<long long*>(vis_count), vi, vd);
+        {
+            ProfScope _ps("single_search_kernel", st);
+            kern<<<1, 32, bytes, st>>>(P, Seq64Member{x + (size_t)qid * dp, (int)dp}, self, (int)L, (int)k, H,
+                                       reinterpret_cast<long long*>(top_ids), top_sqd, reinterpret_cast<long long*>(top_count),
+                                       reinterpret_cast<long long*>(vis_ids), vis_sqd, (int)vcap,
+                                       reinterpret_cast<long long*>(vis_count), vi, vd);
+        }
     } else {
         auto kern = single_search_kernel<Seq64Vector>;
         PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        kern<<<1, 32, bytes, st>>>(P, Seq64Vector{qvec, (int)dp}, self, (int)L, (int)k, H,
-                                   reinterpret_cast<long long*>(top_ids), top_sqd, reinterpret_cast<long long*>(top_count),
-                                   reinterpret_cast<long long*>(vis_ids), vis_sqd, (int)vcap,
-                                   reinterpret_cast<long long*>(vis_count), vi, vd);
+        {
+            ProfScope _ps("single_search_kernel", st);
+            kern<<<1, 32, bytes, st>>>(P, Seq64Vector{qvec, (int)dp}, self, (int)L, (int)k, H,
+                                       reinterpret_cast<long long*>(top_ids), top_sqd, reinterpret_cast<long long*>(top_count),
+                                       reinterpret_cast<long long*>(vis_ids), vis_sqd, (int)vcap,
+                                       reinterpret_cast<long long*>(vis_count), vi, vd);
+        }
     }
     PK_CHECK_LAUNCH("single_search_kernel");
     release(vi, st);
@@ -609,11 +657,17 @@ extern "C" int pk_dp_scan(const float* x, int64_t n, int64_t dp, const int64_t* 
     PK_CHECK(scratch(&pi, (size_t)m * nchunk, st));
     size_t sm = (size_t)DQ * dp * sizeof(float);
     if (sm > 48 * 1024) PK_CHECK(cudaFuncSetAttribute(dp_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dp_scan_kernel<<<grid, BT, sm, st>>>(x, (int)n, (int)dp, reinterpret_cast<const long long*>(rank),
-                                         reinterpret_cast<const long long*>(qids), (int)m, pd, pi);
+    {
+        ProfScope _ps("dp_scan_kernel", st);
+        dp_scan_kernel<<<grid, BT, sm, st>>>(x, (int)n, (int)dp, reinterpret_cast<const long long*>(rank),
+                                             reinterpret_cast<const long long*>(qids), (int)m, pd, pi);
+    }
     PK_CHECK_LAUNCH("dp_scan_kernel");
-    dp_scan_reduce_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(pd, pi, (int)m, nchunk,
-                                                                     reinterpret_cast<long long*>(out_id), out_sqd);
+    {
+        ProfScope _ps("dp_scan_reduce_kernel", st);
+        dp_scan_reduce_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(pd, pi, (int)m, nchunk,
+                                                                         reinterpret_cast<long long*>(out_id), out_sqd);
+    }
     PK_CHECK_LAUNCH("dp_scan_reduce_kernel");
     release(pd, st);
     release(pi, st);
@@ -623,7 +677,10 @@ extern "C" int pk_dp_scan(const float* x, int64_t n, int64_t dp, const int64_t* 
 extern "C" int pk_sqrt(const double* sqd, int64_t count, double* out, void* stream) {
     if (count <= 0) return 0;
     cudaStream_t st = as_stream(stream);
-    sqrt_kernel<<<grid_for(count, 256), 256, 0, st>>>(sqd, count, out);
+    {
+        ProfScope _ps("sqrt_kernel", st);
+        sqrt_kernel<<<grid_for(count, 256), 256, 0, st>>>(sqd, count, out);
+    }
     PK_CHECK_LAUNCH("sqrt_kernel");
     return 0;
 }

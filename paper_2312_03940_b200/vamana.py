@@ -43,6 +43,11 @@ __all__ = [
 
 GRAPH_MAGIC = b"PECG"
 
+# Optional device counters (set by bench.py): "build" -> int64[4] (search
+# evals, prune evals, reverse evals, expansions), "beam" -> int64[2]
+# (evals, expansions) accumulated over every pipeline kNN query.
+STATS = {"build": None, "beam": None}
+
 
 def _digest(*arrays) -> bytes:
     h = hashlib.blake2b(digest_size=16)
@@ -231,6 +236,8 @@ def build_graph_device(p: PointSet, R: int, L_build: int, alpha: float, starts: 
     deg = torch.empty(p.n, dtype=torch.int32, device=dev)
     st = starts_t if starts_t is not None else _lib.to_dev(starts.astype(np.int32))
     od = order_t if order_t is not None else _lib.to_dev(order.astype(np.int32))
+    if stats is None:
+        stats = STATS["build"]
     _lib.call("pk_build_vamana", p.device(), p.n, p.dp, p.mode, R, L_build, float(alpha), st, st.shape[0], od, adj,
               deg, stats, 0, _lib.stream())
     return adj, deg
@@ -284,6 +291,8 @@ def beam_knn_device(g: GraphIndex, qids_t, k: int, L: int, evals=None):
     (_kernels.beam_knn_batch + vamana.py:220-225).  Returns (ids_t, sqd_t)."""
     import torch
 
+    if evals is None:
+        evals = STATS["beam"]
     p = g.points
     adj, deg, st = g.device_arrays()
     m = qids_t.shape[0]

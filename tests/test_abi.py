@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "peakann_b200.h")
 def declared():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return re.findall(r"^\s*(?:int|const char\*)\s+(pk_\w+)\s*\(", src, flags=re.M)
+    return re.findall(r"^\s*(?:int|void|const char\*)\s+(pk_\w+)\s*\(", src, flags=re.M)
 
 
 def test_header_declares_entry_points():
@@ -35,7 +35,8 @@ def test_library_exports_every_declared_symbol():
 def test_ctypes_table_covers_header():
     from paper_2312_03940_b200 import _lib
 
-    names = set(declared()) - {"pk_version", "pk_last_error", "pk_device_info"}
+    names = set(declared()) - {"pk_version", "pk_last_error", "pk_device_info", "pk_prof_enable",
+                               "pk_prof_collect"}
     assert names == set(_lib.SIGNATURES), names ^ set(_lib.SIGNATURES)
 
 
