@@ -346,7 +346,7 @@ def main_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64" if p.mode == 0 else "f32 (exact: integer data)",
+            "vs_baseline": None, "dtype": {0: "f64", 1: "f32 (exact: integer data)", 2: "u8/int32 (exact: integer data)"}[p.mode],
             "data": f"synthetic ({name} generator, seed 0)",
             "config": workload_config(name, args.n, world),
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

@@ -14,9 +14,12 @@
  * Point layout: row-major float32 (n, dp) with dp = d rounded up to a
  * multiple of 4 and zero padding (adds exactly +0.0 to squared distances).
  * `mode` selects the distance policy: PK_MODE_SEQ64 (per-lane sequential
- * float64 in index order -- bit-identical to _kernels.py:21-38 for any data)
- * or PK_MODE_EXACT32 (warp-split float32, legal only when pk_check_exact32
- * proved every partial sum is an exactly representable integer).
+ * float64 in index order -- bit-identical to _kernels.py:21-38 for any data),
+ * PK_MODE_EXACT32 (warp-split float32, legal only when pk_check_exact32
+ * proved every partial sum is an exactly representable integer) or
+ * PK_MODE_EXACT_U8 (integer data spanning <= 255 packed as bytes in x8 by
+ * pk_pack_u8, rows of dw words; exact integer dp4a arithmetic).  x8 may be
+ * null in the other modes.
  */
 #ifndef PEAKANN_B200_H
 #define PEAKANN_B200_H
@@ -29,6 +32,7 @@ extern "C" {
 
 #define PK_MODE_SEQ64 0
 #define PK_MODE_EXACT32 1
+#define PK_MODE_EXACT_U8 2
 
 #define PK_DENSITY_KTH 0
 #define PK_DENSITY_KTH_NORMALIZED 1
@@ -49,10 +53,16 @@ int pk_device_info(int* sm_count, int* smem_optin);
 void pk_prof_enable(int on);
 int pk_prof_collect(char* buf, int len, int reset);
 
-/* 1 in *out_flag (device int) when the data is integer-valued with
- * d * (2 max|x|)^2 < 2^24, i.e. PK_MODE_EXACT32 is bit-exact.
- * Replaces: nothing (reference always uses _kernels.py:21-38). */
+/* Distance-policy classification into *out_flag (device int): 2 when every
+ * coordinate is an integer and max - min <= 255 (PK_MODE_EXACT_U8 is exact),
+ * 1 when integer with d * (max - min)^2 < 2^24 (PK_MODE_EXACT32 is exact),
+ * else 0 (PK_MODE_SEQ64).  Replaces: nothing (the reference always uses the
+ * float64 loop of _kernels.py:21-38; the exact modes reproduce its values). */
 int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d, int* out_flag, void* stream);
+
+/* Pack integer coordinates as bytes (x - min), 4 per uint32 word, rows of dw
+ * = ceil(d/4) words (zero padded).  Only valid when pk_check_exact32 gave 2. */
+int pk_pack_u8(const float* x, int64_t n, int64_t dp, int64_t d, uint32_t* out, int64_t dw, void* stream);
 
 /* Beam-search kNN of member queries.  Replaces _kernels.beam_knn_batch
  * (_kernels.py:230-262); with brute_fallback=1 also the short-row exact
@@ -62,7 +72,8 @@ int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d, int* out_
  * out_evals (device int64[2], may be null) accumulates distance evaluations
  * and expansions (adjacency rows read).
  * hash_bits: log2 of the per-query seen-table size (0 = automatic). */
-int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, const int32_t* adj, int64_t R,
+int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                const int32_t* adj, int64_t R,
                 const int32_t* deg, const int32_t* starts, int64_t s, const int64_t* qids, int64_t m,
                 int64_t L, int64_t k, int64_t* out_ids, double* out_sqd, int64_t* out_counts,
                 int brute_fallback, int64_t* out_evals, int hash_bits, void* stream);
@@ -100,7 +111,8 @@ int pk_brute_knn_vector(const float* x, int64_t n, int64_t dp, const double* qve
  * host from the reference's PCG64 stream, vamana.py:132-143).
  * stats (device int64[4], may be null): search evals, prune evals,
  * reverse evals, expansions. */
-int pk_build_vamana(const float* x, int64_t n, int64_t dp, int mode, int64_t R, int64_t L, double alpha,
+int pk_build_vamana(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                    int64_t R, int64_t L, double alpha,
                     const int32_t* starts, int64_t s, const int32_t* order, int32_t* adj_out,
                     int32_t* deg_out, int64_t* stats, int hash_bits, void* stream);
 

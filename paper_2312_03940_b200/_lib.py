@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libpeakann_b200.so")
 
 MODE_SEQ64 = 0
 MODE_EXACT32 = 1
+MODE_EXACT_U8 = 2
 
 DENSITY_CODES = {"kth": 0, "kth_normalized": 1, "exp_sum": 2, "sum_exp": 3, "sum": 4}
 
@@ -29,11 +30,12 @@ _D = ctypes.c_double
 # name -> argtypes (every entry returns int status)
 SIGNATURES = {
     "pk_check_exact32": [_P, _I, _I, _I, _P, _P],
-    "pk_beam_knn": [_P, _I, _I, _i, _P, _I, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _i, _P, _i, _P],
+    "pk_pack_u8": [_P, _I, _I, _I, _P, _I, _P],
+    "pk_beam_knn": [_P, _I, _I, _P, _I, _i, _P, _I, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _i, _P, _i, _P],
     "pk_beam_search_single": [_P, _I, _I, _P, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P],
     "pk_brute_knn": [_P, _I, _I, _P, _I, _I, _P, _P, _P],
     "pk_brute_knn_vector": [_P, _I, _I, _P, _I, _P, _P, _P],
-    "pk_build_vamana": [_P, _I, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P],
+    "pk_build_vamana": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P],
     "pk_robust_prune": [_P, _I, _I, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P],
     "pk_nearest_to_centroid": [_P, _I, _I, _P, _P],
     "pk_sqrt": [_P, _I, _P, _P],

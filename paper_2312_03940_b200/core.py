@@ -8,11 +8,14 @@ aligned for 128-bit loads) and decides the distance policy:
 * "exact32" when the coordinates are integers with d*(2 max|x|)^2 < 2^24
   (e.g. the SIFT-shaped configurations): warp-split float32 arithmetic is
   then exact and equals the reference's float64 values bit for bit;
+* "u8" when the coordinates are integers spanning at most 255: rows are
+  also packed as bytes (x - min) and distances are exact integer dp4a sums
+  (4x fewer bytes per gathered vector than float32);
 * "seq64" otherwise: per-lane sequential float64 accumulation in the
   reference's coordinate order (_kernels.py:21-38), also bit-identical.
 
-PEAKANN_B200_MODE=seq64 forces the float64 path (used by tests to exercise
-both policies on the same data).
+PEAKANN_B200_MODE=seq64 / exact32 forces a wider path (used by tests to
+exercise every policy on the same data).
 """
 
 from __future__ import annotations
@@ -41,6 +44,7 @@ class PointSet:
         self.data = arr
         self._dev = None
         self._mode = None
+        self._x8 = None
 
     @property
     def n(self) -> int:
@@ -95,8 +99,29 @@ class PointSet:
 
                 flag = torch.zeros(1, dtype=torch.int32, device=_lib.device())
                 _lib.call("pk_check_exact32", self.device(), self.n, self.dp, self.d, flag, _lib.stream())
-                self._mode = _lib.MODE_EXACT32 if int(flag.item()) == 1 else _lib.MODE_SEQ64
+                f = int(flag.item())
+                if f == 2 and forced == "exact32":
+                    f = 1
+                self._mode = {2: _lib.MODE_EXACT_U8, 1: _lib.MODE_EXACT32}.get(f, _lib.MODE_SEQ64)
         return self._mode
+
+    @property
+    def dw(self) -> int:
+        """32-bit words per packed u8 row."""
+        return (self.d + 3) // 4
+
+    def packed(self):
+        """(n, dw) int32 tensor of u8-packed rows in the u8 mode, else None."""
+        from . import _lib
+
+        if self.mode != _lib.MODE_EXACT_U8:
+            return None
+        if self._x8 is None:
+            import torch
+
+            self._x8 = torch.empty((self.n, self.dw), dtype=torch.int32, device=_lib.device())
+            _lib.call("pk_pack_u8", self.device(), self.n, self.dp, self.d, self._x8, self.dw, _lib.stream())
+        return self._x8
 
 
 def upload_points(data: np.ndarray):

@@ -38,6 +38,19 @@ struct BeamSmem {
     unsigned* cbuf;   // [32] scratch: compacted candidate ids
 };
 
+constexpr int kCbuf = 64;  // compacted-candidate buffer (ids) per warp
+
+__device__ __forceinline__ BeamSmem carve_beam(unsigned char* base, int L, int H) {
+    BeamSmem s;
+    s.bd = reinterpret_cast<double*>(base);
+    s.bi = reinterpret_cast<unsigned*>(base + (size_t)L * 8);
+    s.hash = reinterpret_cast<unsigned*>(base + (size_t)L * 12);
+    s.hmask = (unsigned)H - 1u;
+    s.spos = reinterpret_cast<int*>(base + (size_t)L * 12 + (size_t)H * 4);
+    s.cbuf = reinterpret_cast<unsigned*>(base + (size_t)L * 12 + (size_t)H * 4 + 128);
+    return s;
+}
+
 struct SearchParams {
     const float* X;          // (n, dp)
     int dp;
@@ -47,6 +60,9 @@ struct SearchParams {
     const int* starts;       // (s,)
     int s;
     const unsigned* start_bm;  // bitmap of the start set (may be null)
+    const unsigned* X8;        // packed u8 rows (u8 mode only)
+    int dw;
+    __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
 template <class Dist>
@@ -83,13 +99,20 @@ struct WarpBeam {
     }
 
     // Merge the candidates held by lanes with `valid` into the beam.
+    // CheckDups: equal keys inside the batch are possible (duplicate start ids
+    // in a user start list) -- keep the lowest lane.  Graph neighbours of one
+    // expansion are distinct, so the walk skips that pass.
+    template <bool CheckDups>
     __device__ void merge(double cd, unsigned cid, bool valid) {
         const int lane = lane_id();
         double* bd = sm.bd;
         unsigned* bi = sm.bi;
         int pos = 0;
         bool keep = valid;
-        if (valid) {
+        // a full beam rejects anything not better than its worst entry
+        if (keep && bl == L && !key_lt(cd, cid, bd[L - 1], bi[L - 1] & PK_IDMASK)) keep = false;
+        if (!__any_sync(PK_FULL, keep)) return;
+        if (keep) {
             int lo = 0, hi = bl;
             while (lo < hi) {
                 int mid = (lo + hi) >> 1;
@@ -99,20 +122,20 @@ struct WarpBeam {
             pos = lo;
             if (pos < bl && bd[pos] == cd && (bi[pos] & PK_IDMASK) == cid) keep = false;
         }
-        unsigned vb = __ballot_sync(PK_FULL, keep);
-        if (!vb) return;
-        // equal keys inside the batch (duplicate start ids): keep the lowest lane;
-        // then rank every survivor among the survivors
-        int rank = 0;
-        bool dupl = false;
-        for (unsigned b = vb; b; b &= b - 1) {
-            int j = __ffs(b) - 1;
-            double dj = __shfl_sync(PK_FULL, cd, j);
-            unsigned ij = __shfl_sync(PK_FULL, cid, j);
-            if (j < lane && key_eq(dj, ij, cd, cid)) dupl = true;
+        unsigned fb = __ballot_sync(PK_FULL, keep);
+        if (!fb) return;
+        if (CheckDups) {
+            bool dupl = false;
+            for (unsigned b = fb; b; b &= b - 1) {
+                int j = __ffs(b) - 1;
+                double dj = __shfl_sync(PK_FULL, cd, j);
+                unsigned ij = __shfl_sync(PK_FULL, cid, j);
+                if (j < lane && key_eq(dj, ij, cd, cid)) dupl = true;
+            }
+            keep = keep && !dupl;
+            fb = __ballot_sync(PK_FULL, keep);
         }
-        unsigned fb = __ballot_sync(PK_FULL, keep && !dupl);
-        keep = keep && !dupl;
+        int rank = 0;
         for (unsigned b = fb; b; b &= b - 1) {
             int j = __ffs(b) - 1;
             double dj = __shfl_sync(PK_FULL, cd, j);
@@ -169,15 +192,15 @@ struct WarpBeam {
 
     // Seed with the start set (batch insert of ceil(s/32) chunks).
     template <class D>
-    __device__ void seed(const SearchParams& P, const D& dist) {
+    __device__ void seed(const SearchParams& P, const D& dist, bool hash_starts) {
         const int lane = lane_id();
         for (int b = 0; b < P.s; b += 32) {
             const int cnt = min(32, P.s - b);
             unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
-            if (!P.start_bm && lane < cnt) seen_or_insert(sm.hash, sm.hmask, id);
+            if (hash_starts && lane < cnt) seen_or_insert(sm.hash, sm.hmask, id);
             double dd = dist.eval(P.X, (int)id, cnt);
             if (lane == 0) evals += cnt;
-            merge(dd, id, lane < cnt);
+            merge<true>(dd, id, lane < cnt);
         }
     }
 
@@ -219,23 +242,39 @@ struct WarpBeam {
             __syncwarp();
             const int nd = __ldg(P.deg + p);
             const int* row = P.adj + (size_t)p * P.R;
+            int c = 0;
             for (int e0 = 0; e0 < nd; e0 += 32) {
                 int w = e0 + lane < nd ? __ldg(row + e0 + lane) : -1;
                 bool cand = w >= 0;
                 if (cand && P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u)) cand = false;
                 if (cand && seen_or_insert(sm.hash, sm.hmask, (unsigned)w)) cand = false;
                 unsigned b = __ballot_sync(PK_FULL, cand);
-                const int c = __popc(b);
-                if (!c) continue;
-                if (cand) sm.cbuf[warp_excl_prefix(b)] = (unsigned)w;
-                __syncwarp();
-                unsigned cid = lane < c ? sm.cbuf[lane] : 0u;
-                __syncwarp();
-                double dd = dist.eval(P.X, (int)cid, c);
-                if (lane == 0) evals += c;
-                merge(dd, cid, lane < c);
+                const int nb = __popc(b);
+                if (c + nb > kCbuf) {  // very wide rows: flush before the buffer overflows
+                    flush(P, dist, c);
+                    c = 0;
+                }
+                if (cand) sm.cbuf[c + warp_excl_prefix(b)] = (unsigned)w;
+                c += nb;
             }
+            __syncwarp();
+            flush(P, dist, c);
         }
+    }
+
+    // evaluate and merge the c candidates staged in cbuf
+    template <class D>
+    __device__ void flush(const SearchParams& P, const D& dist, int c) {
+        const int lane = lane_id();
+        __syncwarp();
+        for (int g = 0; g < c; g += 32) {
+            const int cnt = min(32, c - g);
+            unsigned cid = lane < cnt ? sm.cbuf[g + lane] : 0u;
+            double dd = dist.eval(P.X, (int)cid, cnt);
+            if (lane == 0) evals += cnt;
+            merge<false>(dd, cid, lane < cnt);
+        }
+        __syncwarp();
     }
 
     // Member-query output: first kk entries of the beam without `self`, then
@@ -370,6 +409,87 @@ __device__ int warp_prune(const float* __restrict__ X, const double* kd, const u
             if (lane < cnt && alpha2 * duv <= kd[uu]) alive[uu] = 0;
             __syncwarp();
         }
+        ++t;
+    }
+    __syncwarp();
+    return sel;
+}
+
+// Copy the u8 rows of candidates ki[0..S) into shared memory (row stride rs
+// words, rs = dw + 1 so lanes reading different rows hit different banks).
+__device__ __forceinline__ void stage_u8_rows(const unsigned* __restrict__ X8, int dw, const unsigned* ki, int S,
+                                              unsigned* rows, int rs) {
+    const int lane = lane_id();
+    int x = 0;
+    for (; x + 4 <= S; x += 4) {
+        const unsigned i0 = ki[x], i1 = ki[x + 1], i2 = ki[x + 2], i3 = ki[x + 3];
+        for (int w = lane; w < dw; w += 32) {
+            unsigned a = __ldg(X8 + (size_t)i0 * dw + w);
+            unsigned b = __ldg(X8 + (size_t)i1 * dw + w);
+            unsigned c = __ldg(X8 + (size_t)i2 * dw + w);
+            unsigned d = __ldg(X8 + (size_t)i3 * dw + w);
+            rows[(x + 0) * rs + w] = a;
+            rows[(x + 1) * rs + w] = b;
+            rows[(x + 2) * rs + w] = c;
+            rows[(x + 3) * rs + w] = d;
+        }
+    }
+    for (; x < S; ++x)
+        for (int w = lane; w < dw; w += 32) rows[x * rs + w] = __ldg(X8 + (size_t)ki[x] * dw + w);
+    __syncwarp();
+}
+
+// RobustPrune on u8 rows staged in shared memory (rows >= S come from
+// global memory).  Same picks as warp_prune: one lane per candidate u, the
+// whole row pair evaluated sequentially with exact integer dp4a arithmetic.
+// Alive candidates after the current pick are queued 32 at a time so every
+// lane has work.
+static __device__ int warp_prune_u8(const unsigned* __restrict__ X8, int dw, const double* kd, const unsigned* ki, int c,
+                             double alpha2, int R, unsigned char* alive, unsigned* cbuf, int* out,
+                             const unsigned* rows, int rs, int S, long long* evals) {
+    const int lane = lane_id();
+    for (int i = lane; i < c; i += 32) alive[i] = 1;
+    __syncwarp();
+    int sel = 0;
+    int t = 0;
+    while (sel < R) {
+        int nt = -1;
+        for (int base = t; base < c; base += 32) {
+            int i = base + lane;
+            unsigned b = __ballot_sync(PK_FULL, i < c && alive[i]);
+            if (b) { nt = base + __ffs(b) - 1; break; }
+        }
+        if (nt < 0) break;
+        t = nt;
+        if (lane == 0) out[sel] = (int)ki[t];
+        ++sel;
+        if (sel >= R) break;
+        const unsigned* rt = t < S ? rows + (size_t)t * rs : X8 + (size_t)ki[t] * dw;
+        int nq = 0;
+        auto run = [&](int cnt) {
+            __syncwarp();
+            if (lane < cnt) {
+                const int u = (int)cbuf[lane];
+                const unsigned* ru = u < S ? rows + (size_t)u * rs : X8 + (size_t)ki[u] * dw;
+                const unsigned duv = u8_row_dist(rt, ru, dw);
+                if (alpha2 * (double)duv <= kd[u]) alive[u] = 0;
+            }
+            if (lane == 0) *evals += cnt;
+            __syncwarp();
+        };
+        for (int base = t + 1; base < c; base += 32) {
+            const int u = base + lane;
+            const bool a = u < c && alive[u];
+            const unsigned b = __ballot_sync(PK_FULL, a);
+            const int k = __popc(b);
+            if (nq + k > 32) {
+                run(nq);
+                nq = 0;
+            }
+            if (a) cbuf[nq + warp_excl_prefix(b)] = (unsigned)u;
+            nq += k;
+        }
+        if (nq) run(nq);
         ++t;
     }
     __syncwarp();

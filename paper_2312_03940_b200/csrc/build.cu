@@ -26,104 +26,127 @@ namespace pk {
 
 int grid_for(long long work, int block);
 
-template <int MODE, int QV>
-struct BDist;
-template <int QV>
-struct BDist<PK_MODE_SEQ64, QV> {
-    using T = Seq64Member;
-    __device__ static T make(const float* X, int dp, unsigned id) { return T{X + (size_t)id * dp, dp}; }
-};
-template <int QV>
-struct BDist<PK_MODE_EXACT32, QV> {
-    using T = Exact32<QV>;
-    __device__ static T make(const float* X, int dp, unsigned id) {
-        T t;
-        t.load(X + (size_t)id * dp, dp);
-        return t;
-    }
-};
-
-template <int MODE, int QV>
-struct MakeAt {
-    const float* X;
-    int dp;
-    __device__ typename BDist<MODE, QV>::T operator()(unsigned id) const { return BDist<MODE, QV>::make(X, dp, id); }
-};
-
 struct BuildArgs {
     SearchParams P;
+    DataRef D;
     const int* bids;
     int m;
     int L;
     int H;
     int cap;           // candidate capacity (power of two)
-    int vcap;          // visit-log capacity
+    int vcap;          // visit-log capacity per point
+    int S;             // u8 rows staged in shared memory per warp
     double alpha2;
-    size_t warp_bytes;
-    unsigned* vlog_i;  // [total_warps * vcap]
+    size_t search_bytes;  // per-warp shared memory, search kernel
+    size_t prune_bytes;   // per-warp shared memory, prune kernel
+    unsigned* vlog_i;  // [m * vcap]
     double* vlog_d;
+    int* vlen;         // [m]
     int* new_ids;      // [m * R]
     int* new_len;      // [m]
     unsigned* err;
     long long* stats;  // [4]
 };
 
+// phase 1: one warp per inserted point searches the adjacency snapshot and
+// logs its visited set (_kernels.py:349-358)
 template <int MODE, int QV>
-__global__ void __launch_bounds__(128) build_batch_kernel(BuildArgs A) {
+__global__ void __launch_bounds__(128) build_search_kernel(BuildArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int lane = lane_id();
-    const int gw = blockIdx.x * wpb + wib;
-    unsigned char* mine = smem + (size_t)wib * A.warp_bytes;
-    // search view
-    BeamSmem sm;
-    sm.bd = reinterpret_cast<double*>(mine);
-    sm.bi = reinterpret_cast<unsigned*>(mine + (size_t)A.L * 8);
-    sm.hash = reinterpret_cast<unsigned*>(mine + (size_t)A.L * 12);
-    sm.hmask = (unsigned)A.H - 1u;
-    sm.spos = reinterpret_cast<int*>(mine + (size_t)A.L * 12 + (size_t)A.H * 4);
-    sm.cbuf = reinterpret_cast<unsigned*>(mine + (size_t)A.L * 12 + (size_t)A.H * 4 + 128);
-    // prune view (aliases the search view once the walk is over)
-    double* kd = reinterpret_cast<double*>(mine);
-    unsigned* ki = reinterpret_cast<unsigned*>(mine + (size_t)A.cap * 8);
-    unsigned* pcbuf = reinterpret_cast<unsigned*>(mine + (size_t)A.cap * 12);
-    unsigned char* alive = mine + (size_t)A.cap * 12 + 128;
-
-    unsigned* vi = A.vlog_i + (size_t)gw * A.vcap;
-    double* vd = A.vlog_d + (size_t)gw * A.vcap;
-    const MakeAt<MODE, QV> make{A.P.X, A.P.dp};
-    long long ev_search = 0, ev_prune = 0, expansions = 0;
-    const int R = A.P.R;
-    for (int t = gw; t < A.m; t += gridDim.x * wpb) {
+    BeamSmem sm = carve_beam(smem + (size_t)wib * A.search_bytes, A.L, A.H);
+    const MakeAt<MODE, QV> make{A.D};
+    long long ev = 0, expansions = 0;
+    for (int t = blockIdx.x * wpb + wib; t < A.m; t += gridDim.x * wpb) {
         const unsigned p = (unsigned)A.bids[t];
         auto dist = make(p);
         WarpBeam<decltype(dist)> wb;
-        wb.init(sm, A.L, vi, vd, A.vcap, A.err);
-        wb.seed(A.P, dist);
+        wb.init(sm, A.L, A.vlog_i + (size_t)t * A.vcap, A.vlog_d + (size_t)t * A.vcap, A.vcap, A.err);
+        wb.seed(A.P, dist, false);
         wb.walk(A.P, dist);
-        ev_search += wb.evals;
+        ev += wb.evals;
         expansions += wb.vl;
-        const int vl = min(wb.vl, A.vcap);
+        if (lane == 0) A.vlen[t] = min(wb.vl, A.vcap);
         __syncwarp();
-        // candidates: visit log + current out-row (distances recomputed, _kernels.py:359-368)
+    }
+    if (lane == 0 && A.stats) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 0), (unsigned long long)ev);
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 3), (unsigned long long)expansions);
+    }
+}
+
+// shared-memory view of the candidate buffers of one warp
+struct CandSmem {
+    double* kd;
+    unsigned* ki;
+    unsigned* cbuf;
+    unsigned char* alive;
+    unsigned* rows;
+};
+
+__device__ __forceinline__ CandSmem carve_cand(unsigned char* base, int cap) {
+    CandSmem c;
+    c.kd = reinterpret_cast<double*>(base);
+    c.ki = reinterpret_cast<unsigned*>(base + (size_t)cap * 8);
+    c.cbuf = reinterpret_cast<unsigned*>(base + (size_t)cap * 12);
+    c.alive = base + (size_t)cap * 12 + 128;
+    c.rows = reinterpret_cast<unsigned*>(base + (((size_t)cap * 13 + 128 + 15) & ~(size_t)15));
+    return c;
+}
+
+// sorted, de-duplicated candidates kd/ki[0..c) -> RobustPrune picks in out[]
+template <int MODE, int QV>
+__device__ __forceinline__ int prune_candidates(const DataRef& D, const CandSmem& C, int c, double alpha2, int R,
+                                                int S, int* out, long long* ev) {
+    if (MODE == MODE_EXACT_U8) {
+        const int rs = D.dw + 1;
+        const int st = min(c, S);
+        stage_u8_rows(D.X8, D.dw, C.ki, st, C.rows, rs);
+        return warp_prune_u8(D.X8, D.dw, C.kd, C.ki, c, alpha2, R, C.alive, C.cbuf, out, C.rows, rs, st, ev);
+    }
+    const MakeAt<MODE, QV> make{D};
+    return warp_prune(D.X, C.kd, C.ki, c, alpha2, R, C.alive, C.cbuf, out, make, ev);
+}
+
+// phase 2: candidates = visited U current out-row (distances recomputed,
+// _kernels.py:359-368), canonicalise, RobustPrune -> staged out-list
+template <int MODE, int QV>
+__global__ void __launch_bounds__(128) build_prune_kernel(BuildArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const int lane = lane_id();
+    const CandSmem C = carve_cand(smem + (size_t)wib * A.prune_bytes, A.cap);
+    const MakeAt<MODE, QV> make{A.D};
+    long long ev_search = 0, ev_prune = 0;
+    const int R = A.P.R;
+    for (int t = blockIdx.x * wpb + wib; t < A.m; t += gridDim.x * wpb) {
+        const unsigned p = (unsigned)A.bids[t];
+        const int vl = A.vlen[t];
+        const unsigned* vi = A.vlog_i + (size_t)t * A.vcap;
+        const double* vd = A.vlog_d + (size_t)t * A.vcap;
         for (int x = lane; x < vl; x += 32) {
-            kd[x] = vd[x];
-            ki[x] = vi[x];
+            C.kd[x] = vd[x];
+            C.ki[x] = vi[x];
         }
         const int nd = __ldg(A.P.deg + p);
         const int* row = A.P.adj + (size_t)p * R;
         int c = vl;
-        for (int e0 = 0; e0 < nd; e0 += 32) {
-            const int cnt = min(32, nd - e0);
-            unsigned w = lane < cnt ? (unsigned)__ldg(row + e0 + lane) : 0u;
-            double dd = dist.eval(A.P.X, (int)w, cnt);
-            if (lane == 0) ev_search += cnt;
-            if (lane < cnt && c + lane < A.cap) {
-                kd[c + lane] = dd;
-                ki[c + lane] = w;
+        if (nd > 0) {
+            auto dist = make(p);
+            for (int e0 = 0; e0 < nd; e0 += 32) {
+                const int cnt = min(32, nd - e0);
+                unsigned w = lane < cnt ? (unsigned)__ldg(row + e0 + lane) : 0u;
+                double dd = dist.eval(A.D.X, (int)w, cnt);
+                if (lane == 0) ev_search += cnt;
+                if (lane < cnt && c + lane < A.cap) {
+                    C.kd[c + lane] = dd;
+                    C.ki[c + lane] = w;
+                }
+                c += cnt;
             }
-            c += cnt;
         }
         if (c > A.cap) {
             if (lane == 0) atomicOr(A.err, ERR_CAND_OVERFLOW);
@@ -131,14 +154,14 @@ __global__ void __launch_bounds__(128) build_batch_kernel(BuildArgs A) {
         }
         const int Pw = next_pow2_dev(c);
         for (int x = c + lane; x < Pw; x += 32) {
-            kd[x] = __longlong_as_double(0x7ff0000000000000LL);
-            ki[x] = 0xffffffffu;
+            C.kd[x] = __longlong_as_double(0x7ff0000000000000LL);
+            C.ki[x] = 0xffffffffu;
         }
         __syncwarp();
-        warp_sort(kd, ki, Pw);
-        c = warp_unique(kd, ki, c, p);
+        warp_sort(C.kd, C.ki, Pw);
+        c = warp_unique(C.kd, C.ki, c, p);
         int* out = A.new_ids + (size_t)t * R;
-        int sel = warp_prune(A.P.X, kd, ki, c, A.alpha2, R, alive, pcbuf, out, make, &ev_prune);
+        int sel = prune_candidates<MODE, QV>(A.D, C, c, A.alpha2, R, A.S, out, &ev_prune);
         for (int x = sel + lane; x < R; x += 32) out[x] = -1;
         if (lane == 0) A.new_len[t] = sel;
         __syncwarp();
@@ -146,7 +169,6 @@ __global__ void __launch_bounds__(128) build_batch_kernel(BuildArgs A) {
     if (lane == 0 && A.stats) {
         atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 0), (unsigned long long)ev_search);
         atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 1), (unsigned long long)ev_prune);
-        atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 3), (unsigned long long)expansions);
     }
 }
 
@@ -194,6 +216,8 @@ __global__ void scatter_kernel(const int* bids, int m, int R, const int* new_ids
 struct RevArgs {
     const float* X;
     int dp;
+    DataRef D;
+    int S;
     int* adj;
     int* deg;
     int R;
@@ -304,12 +328,12 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int lane = lane_id();
-    unsigned char* mine = smem + (size_t)wib * A.warp_bytes;
-    double* kd = reinterpret_cast<double*>(mine);
-    unsigned* ki = reinterpret_cast<unsigned*>(mine + (size_t)A.cap * 8);
-    unsigned* pcbuf = reinterpret_cast<unsigned*>(mine + (size_t)A.cap * 12);
-    unsigned char* alive = mine + (size_t)A.cap * 12 + 128;
-    const MakeAt<MODE, QV> make{A.X, A.dp};
+    const CandSmem C = carve_cand(smem + (size_t)wib * A.warp_bytes, A.cap);
+    double* kd = C.kd;
+    unsigned* ki = C.ki;
+    unsigned* pcbuf = C.cbuf;
+    unsigned char* alive = C.alive;
+    const MakeAt<MODE, QV> make{A.D};
     const int nt = *A.ntargets;
     long long ev = 0;
     for (int s = blockIdx.x * wpb + wib; s < nt; s += gridDim.x * wpb) {
@@ -346,7 +370,7 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
                 for (int x = lane; x < c; x += 32) row[x] = (int)ki[x];
                 sel = c;
             } else {
-                sel = warp_prune(A.X, kd, ki, c, A.alpha2, A.R, alive, pcbuf, row, make, &ev);
+                sel = prune_candidates<MODE, QV>(A.D, C, c, A.alpha2, A.R, A.S, row, &ev);
             }
         } else {
             sel = prune_by_selection(A, u, make, kd, ki, alive, pcbuf, nd, off, size, row, &ev);
@@ -463,43 +487,47 @@ __global__ void nearest_final_kernel(const double* bd, const int* bi, int g, lon
     *out = bid;
 }
 
-__global__ void starts_bitmap_kernel2(const int* starts, int s, unsigned* bm) {
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < s; x += gridDim.x * blockDim.x)
-        atomicOr(bm + (starts[x] >> 5), 1u << (starts[x] & 31));
+// ---- host driver -----------------------------------------------------------------------------
+template <class K>
+int config_kernel(K kern, size_t warp_bytes, int want_wpb, int* wpb_out, int* grid_out) {
+    int wpb = want_wpb;
+    while (wpb > 1 && warp_bytes * wpb > (size_t)max_smem_optin()) wpb >>= 1;
+    if (warp_bytes * wpb > (size_t)max_smem_optin()) {
+        set_error("per-warp shared memory exceeds the device limit");
+        return 2;
+    }
+    PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(warp_bytes * wpb)));
+    int per_sm = 0;
+    PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, warp_bytes * wpb));
+    *wpb_out = wpb;
+    *grid_out = sm_count() * (per_sm < 1 ? 1 : per_sm);
+    return 0;
 }
 
-// ---- host driver -----------------------------------------------------------------------------
 template <int MODE, int QV>
-int run_build(const float* x, int n, int dp, int R, int L, double alpha, const int* starts, int s, const int* order,
+int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
               int* adj, int* deg, long long* stats, int hash_bits, cudaStream_t st) {
+    const bool u8 = MODE == MODE_EXACT_U8;
     const int H = choose_hash(L, hash_bits);
     const int cap = next_pow2(2 * L + 64 + R);
     const int vcap = cap - R;
     const int capR = 1024;
-    size_t wb = align16(std::max(beam_smem_bytes(L, H), sort_smem_bytes(cap)));
-    int wpb = 4;
-    while (wpb > 1 && wb * wpb > (size_t)max_smem_optin()) wpb >>= 1;
-    if (wb * wpb > (size_t)max_smem_optin()) {
-        set_error("build beam too large for shared memory");
-        return 2;
-    }
-    auto bk = build_batch_kernel<MODE, QV>;
-    PK_CHECK(cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wb * wpb)));
-    int per_sm = 0;
-    PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bk, 32 * wpb, wb * wpb));
-    if (per_sm < 1) per_sm = 1;
-    const int max_grid = sm_count() * per_sm;
-    const int total_warps = max_grid * wpb;
+    const int S = std::min(cap, 192);
+    const int SR = std::min(capR, 192);
+    const size_t rows_b = u8 ? (size_t)S * (D.dw + 1) * 4 : 0;
+    const size_t rows_br = u8 ? (size_t)SR * (D.dw + 1) * 4 : 0;
 
-    size_t wbr = align16(sort_smem_bytes(capR));
-    int wpbr = 4;
-    while (wpbr > 1 && wbr * wpbr > (size_t)max_smem_optin()) wpbr >>= 1;
+    BuildArgs A;
+    A.search_bytes = align16(beam_smem_bytes(L, H));
+    A.prune_bytes = align16(align16(sort_smem_bytes(cap)) + rows_b);
+    auto sk = build_search_kernel<MODE, QV>;
+    auto pkk = build_prune_kernel<MODE, QV>;
     auto rk = reverse_kernel<MODE, QV>;
-    PK_CHECK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wbr * wpbr)));
-    int per_sm_r = 0;
-    PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_r, rk, 32 * wpbr, wbr * wpbr));
-    if (per_sm_r < 1) per_sm_r = 1;
-    const int grid_r = sm_count() * per_sm_r;
+    int wpb_s, grid_s, wpb_p, grid_p, wpb_r, grid_r, rc;
+    if ((rc = config_kernel(sk, A.search_bytes, 4, &wpb_s, &grid_s))) return rc;
+    if ((rc = config_kernel(pkk, A.prune_bytes, 2, &wpb_p, &grid_p))) return rc;
+    const size_t wbr = align16(align16(sort_smem_bytes(capR)) + rows_br);
+    if ((rc = config_kernel(rk, wbr, 2, &wpb_r, &grid_r))) return rc;
 
     int maxb = 1;
     while (maxb < n) maxb <<= 1;
@@ -507,13 +535,14 @@ int run_build(const float* x, int n, int dp, int R, int L, double alpha, const i
     const long long E = (long long)mb * R;      // max edges per batch
     const int ub = (int)std::min<long long>(n, E);
 
-    unsigned *vlog_i = nullptr, *bm = nullptr, *err = nullptr;
+    unsigned *vlog_i = nullptr, *err = nullptr;
     double *vlog_d = nullptr, *adist = nullptr;
-    int *new_ids = nullptr, *new_len = nullptr, *cnt = nullptr, *tslot = nullptr, *targets = nullptr;
-    int *sizes = nullptr, *offs = nullptr, *fill = nullptr, *adds = nullptr, *ntargets = nullptr;
+    int *vlen = nullptr, *new_ids = nullptr, *new_len = nullptr, *cnt = nullptr, *tslot = nullptr;
+    int *targets = nullptr, *sizes = nullptr, *offs = nullptr, *fill = nullptr, *adds = nullptr, *ntargets = nullptr;
     unsigned char* aalive = nullptr;
-    PK_CHECK(scratch(&vlog_i, (size_t)total_warps * vcap, st));
-    PK_CHECK(scratch(&vlog_d, (size_t)total_warps * vcap, st));
+    PK_CHECK(scratch(&vlog_i, (size_t)mb * vcap, st));
+    PK_CHECK(scratch(&vlog_d, (size_t)mb * vcap, st));
+    PK_CHECK(scratch(&vlen, (size_t)mb, st));
     PK_CHECK(scratch(&new_ids, (size_t)E, st));
     PK_CHECK(scratch(&new_len, (size_t)mb, st));
     PK_CHECK(scratch(&cnt, (size_t)n, st));
@@ -527,8 +556,6 @@ int run_build(const float* x, int n, int dp, int R, int L, double alpha, const i
     PK_CHECK(scratch(&aalive, (size_t)E, st));
     PK_CHECK(scratch(&ntargets, 1, st));
     PK_CHECK(scratch(&err, 1, st));
-    size_t words = (size_t)(n + 31) / 32;
-    PK_CHECK(scratch(&bm, words, st));
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, sizes, offs, ub + 1, st);
@@ -538,30 +565,28 @@ int run_build(const float* x, int n, int dp, int R, int L, double alpha, const i
     PK_CHECK(cudaMemsetAsync(deg, 0, sizeof(int) * (size_t)n, st));
     PK_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)n, st));
     PK_CHECK(cudaMemsetAsync(err, 0, sizeof(unsigned), st));
-    PK_CHECK(cudaMemsetAsync(bm, 0, words * 4, st));
-    {
-        ProfScope _ps("starts_bitmap_kernel2", st);
-        starts_bitmap_kernel2<<<grid_for(s, 256), 256, 0, st>>>(starts, s, bm);
-    }
 
-    BuildArgs A;
-    A.P = SearchParams{x, dp, adj, R, deg, starts, s, bm};
+    A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s, nullptr};
+    A.D = D;
     A.L = L;
     A.H = H;
     A.cap = cap;
     A.vcap = vcap;
+    A.S = S;
     A.alpha2 = alpha * alpha;
-    A.warp_bytes = wb;
     A.vlog_i = vlog_i;
     A.vlog_d = vlog_d;
+    A.vlen = vlen;
     A.new_ids = new_ids;
     A.new_len = new_len;
     A.err = err;
     A.stats = stats;
 
     RevArgs B;
-    B.X = x;
-    B.dp = dp;
+    B.X = D.X;
+    B.dp = D.dp;
+    B.D = D;
+    B.S = SR;
     B.adj = adj;
     B.deg = deg;
     B.R = R;
@@ -582,12 +607,16 @@ int run_build(const float* x, int n, int dp, int R, int L, double alpha, const i
         const int m = std::min(batch, n - lo);
         A.bids = order + lo;
         A.m = m;
-        const int g = std::min(max_grid, (m + wpb - 1) / wpb);
         {
-            ProfScope _ps("build_batch_kernel", st);
-            bk<<<g, 32 * wpb, wb * wpb, st>>>(A);
+            ProfScope _ps("build_search_kernel", st);
+            sk<<<std::min(grid_s, (m + wpb_s - 1) / wpb_s), 32 * wpb_s, A.search_bytes * wpb_s, st>>>(A);
         }
-        PK_CHECK_LAUNCH("build_batch_kernel");
+        PK_CHECK_LAUNCH("build_search_kernel");
+        {
+            ProfScope _ps("build_prune_kernel", st);
+            pkk<<<std::min(grid_p, (m + wpb_p - 1) / wpb_p), 32 * wpb_p, A.prune_bytes * wpb_p, st>>>(A);
+        }
+        PK_CHECK_LAUNCH("build_prune_kernel");
         const int ubb = (int)std::min<long long>(n, (long long)m * R);
         PK_CHECK(cudaMemsetAsync(ntargets, 0, sizeof(int), st));
         PK_CHECK(cudaMemsetAsync(sizes, 0, sizeof(int) * ((size_t)ubb + 1), st));
@@ -613,18 +642,17 @@ int run_build(const float* x, int n, int dp, int R, int L, double alpha, const i
                                                                              offs, fill, adds);
         }
         PK_CHECK_LAUNCH("scatter_kernel");
-        const int gr = std::min(grid_r, (ubb + wpbr - 1) / wpbr);
         {
             ProfScope _ps("reverse_kernel", st);
-            rk<<<gr, 32 * wpbr, wbr * wpbr, st>>>(B);
+            rk<<<std::min(grid_r, (ubb + wpb_r - 1) / wpb_r), 32 * wpb_r, wbr * wpb_r, st>>>(B);
         }
         PK_CHECK_LAUNCH("reverse_kernel");
     }
     unsigned herr = 0;
     PK_CHECK(cudaMemcpyAsync(&herr, err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)new_ids, (void*)new_len, (void*)cnt, (void*)tslot,
-                    (void*)targets, (void*)sizes, (void*)offs, (void*)fill, (void*)adds, (void*)adist,
-                    (void*)aalive, (void*)ntargets, (void*)err, (void*)bm, cub_tmp})
+    for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)new_ids, (void*)new_len, (void*)cnt, (void*)tslot,
+                    (void*)targets, (void*)sizes, (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive,
+                    (void*)ntargets, (void*)err, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {
@@ -634,33 +662,42 @@ int run_build(const float* x, int n, int dp, int R, int L, double alpha, const i
     return 0;
 }
 
+template <int MODE>
+int dispatch_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
+                   int* adj, int* deg, long long* stats, int hash_bits, cudaStream_t st) {
+    if (MODE == MODE_SEQ64) return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
+    const int qv = MODE == MODE_EXACT_U8 ? (D.dw + 31) / 32 : (D.dp + 127) / 128;
+    if (qv <= 1) return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
+    if (qv <= 2) return run_build<MODE, 2>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
+    if (qv <= 4) return run_build<MODE, 4>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
+    if (qv <= 8) return run_build<MODE, 8>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
+    set_error("exact integer modes support d <= 1024");
+    return 2;
+}
+
 }  // namespace pk
 
 using namespace pk;
 
-extern "C" int pk_build_vamana(const float* x, int64_t n, int64_t dp, int mode, int64_t R, int64_t L, double alpha,
-                               const int32_t* starts, int64_t s, const int32_t* order, int32_t* adj_out,
-                               int32_t* deg_out, int64_t* stats, int hash_bits, void* stream) {
+extern "C" int pk_build_vamana(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                               int64_t R, int64_t L, double alpha, const int32_t* starts, int64_t s,
+                               const int32_t* order, int32_t* adj_out, int32_t* deg_out, int64_t* stats,
+                               int hash_bits, void* stream) {
     cudaStream_t st = as_stream(stream);
     long long* ls = reinterpret_cast<long long*>(stats);
-    if (mode == PK_MODE_SEQ64)
-        return run_build<PK_MODE_SEQ64, 1>(x, (int)n, (int)dp, (int)R, (int)L, alpha, starts, (int)s, order, adj_out,
-                                           deg_out, ls, hash_bits, st);
-    int qv = (int)((dp + 127) / 128);
-    if (qv <= 1)
-        return run_build<PK_MODE_EXACT32, 1>(x, (int)n, (int)dp, (int)R, (int)L, alpha, starts, (int)s, order,
-                                             adj_out, deg_out, ls, hash_bits, st);
-    if (qv <= 2)
-        return run_build<PK_MODE_EXACT32, 2>(x, (int)n, (int)dp, (int)R, (int)L, alpha, starts, (int)s, order,
-                                             adj_out, deg_out, ls, hash_bits, st);
-    if (qv <= 4)
-        return run_build<PK_MODE_EXACT32, 4>(x, (int)n, (int)dp, (int)R, (int)L, alpha, starts, (int)s, order,
-                                             adj_out, deg_out, ls, hash_bits, st);
-    if (qv <= 8)
-        return run_build<PK_MODE_EXACT32, 8>(x, (int)n, (int)dp, (int)R, (int)L, alpha, starts, (int)s, order,
-                                             adj_out, deg_out, ls, hash_bits, st);
-    set_error("EXACT32 mode supports d <= 1024");
-    return 2;
+    const DataRef D{x, (int)dp, x8, (int)dw};
+    if (mode == MODE_EXACT_U8 && !x8) {
+        set_error("u8 mode needs the packed rows");
+        return 2;
+    }
+    if (mode == MODE_EXACT_U8)
+        return dispatch_build<MODE_EXACT_U8>(D, (int)n, (int)R, (int)L, alpha, starts, (int)s, order, adj_out, deg_out,
+                                             ls, hash_bits, st);
+    if (mode == MODE_EXACT32)
+        return dispatch_build<MODE_EXACT32>(D, (int)n, (int)R, (int)L, alpha, starts, (int)s, order, adj_out, deg_out,
+                                            ls, hash_bits, st);
+    return dispatch_build<MODE_SEQ64>(D, (int)n, (int)R, (int)L, alpha, starts, (int)s, order, adj_out, deg_out, ls,
+                                      hash_bits, st);
 }
 
 extern "C" int pk_robust_prune(const float* x, int64_t n, int64_t dp, int64_t p, const int64_t* cand_ids,

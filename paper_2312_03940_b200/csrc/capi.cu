@@ -26,6 +26,13 @@ static void query_device() {
     if (g_sms > 0) return;
     int dev = 0;
     cudaGetDevice(&dev);
+    // keep freed scratch in the stream-ordered pool instead of returning it to
+    // the driver at every synchronisation (the kernels allocate per call)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&g_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (g_sms <= 0) g_sms = 148;

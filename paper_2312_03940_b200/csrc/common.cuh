@@ -209,6 +209,137 @@ struct Exact32 {
     }
 };
 
+// ExactU8: integer coordinates spanning at most 255 are stored as bytes
+// (x - min), four per 32-bit word, rows of `dw` words.  |a - b| per byte
+// (__vabsdiffu4) and its square summed by __dp4a are exact integer
+// arithmetic, identical to the reference's float64 value (every term and sum
+// is an integer far below 2^53).  QW words per lane: dims [4*(lane + 32*v)].
+template <int QW>
+struct ExactU8 {
+    const unsigned* X8;
+    unsigned q[QW];
+    int dw;
+
+    __device__ __forceinline__ void load(const unsigned* X8_, int dw_, unsigned id) {
+        X8 = X8_;
+        dw = dw_;
+        const int lane = lane_id();
+#pragma unroll
+        for (int v = 0; v < QW; ++v) {
+            int col = lane + 32 * v;
+            q[v] = col < dw ? __ldg(X8 + (size_t)id * dw + col) : 0u;
+        }
+    }
+
+    __device__ __forceinline__ unsigned partial(int id) const {
+        const unsigned* r = X8 + (size_t)id * dw;
+        const int lane = lane_id();
+        unsigned acc = 0u;
+#pragma unroll
+        for (int v = 0; v < QW; ++v) {
+            int col = lane + 32 * v;
+            if (col < dw) {
+                unsigned x = __vabsdiffu4(q[v], __ldg(r + col));
+                acc = __dp4a(x, x, acc);
+            }
+        }
+        return acc;
+    }
+
+    // same transposed butterfly as Exact32, on exact unsigned integers
+    __device__ __forceinline__ double eval(const float* __restrict__, int cid, int c) const {
+        const int lane = lane_id();
+        double mine = 0.0;
+        for (int g = 0; g < c; g += 8) {
+            unsigned v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int id = __shfl_sync(PK_FULL, cid, (g + j) & 31);
+                v[j] = (g + j < c) ? partial(id) : 0u;
+            }
+#pragma unroll
+            for (int s = 16, h = 4; s >= 4; s >>= 1, h >>= 1) {
+                const bool up = lane & s;
+#pragma unroll
+                for (int j = 0; j < h; ++j) {
+                    unsigned send = up ? v[j] : v[j + h];
+                    unsigned keep = up ? v[j + h] : v[j];
+                    v[j] = keep + __shfl_xor_sync(PK_FULL, send, s);
+                }
+            }
+            v[0] += __shfl_xor_sync(PK_FULL, v[0], 2);
+            v[0] += __shfl_xor_sync(PK_FULL, v[0], 1);
+            unsigned got = __shfl_sync(PK_FULL, v[0], ((lane - g) & 7) << 2);
+            if (lane >= g && lane < g + 8 && lane < c) mine = (double)got;
+        }
+        return mine;
+    }
+};
+
+// one full u8 row pair, sequential over words (prune on staged rows)
+__device__ __forceinline__ unsigned u8_row_dist(const unsigned* a, const unsigned* b, int dw) {
+    unsigned acc0 = 0u, acc1 = 0u;
+    int w = 0;
+    for (; w + 1 < dw; w += 2) {
+        unsigned x = __vabsdiffu4(a[w], b[w]);
+        unsigned y = __vabsdiffu4(a[w + 1], b[w + 1]);
+        acc0 = __dp4a(x, x, acc0);
+        acc1 = __dp4a(y, y, acc1);
+    }
+    if (w < dw) {
+        unsigned x = __vabsdiffu4(a[w], b[w]);
+        acc0 = __dp4a(x, x, acc0);
+    }
+    return acc0 + acc1;
+}
+
+// ---- policy selection --------------------------------------------------------------
+// point data as seen by the kernels: float32 rows (always) and, in the u8
+// mode, the packed byte rows
+struct DataRef {
+    const float* X;
+    int dp;
+    const unsigned* X8;
+    int dw;
+};
+
+constexpr int MODE_SEQ64 = 0;
+constexpr int MODE_EXACT32 = 1;
+constexpr int MODE_EXACT_U8 = 2;
+
+template <int MODE, int QV>
+struct DistFor;
+template <int QV>
+struct DistFor<MODE_SEQ64, QV> {
+    using T = Seq64Member;
+    __device__ static T make(const DataRef& D, unsigned id) { return T{D.X + (size_t)id * D.dp, D.dp}; }
+};
+template <int QV>
+struct DistFor<MODE_EXACT32, QV> {
+    using T = Exact32<QV>;
+    __device__ static T make(const DataRef& D, unsigned id) {
+        T t;
+        t.load(D.X + (size_t)id * D.dp, D.dp);
+        return t;
+    }
+};
+template <int QV>
+struct DistFor<MODE_EXACT_U8, QV> {
+    using T = ExactU8<QV>;
+    __device__ static T make(const DataRef& D, unsigned id) {
+        T t;
+        t.load(D.X8, D.dw, id);
+        return t;
+    }
+};
+
+// functor: id -> distance policy object for that query row
+template <int MODE, int QV>
+struct MakeAt {
+    DataRef D;
+    __device__ typename DistFor<MODE, QV>::T operator()(unsigned id) const { return DistFor<MODE, QV>::make(D, id); }
+};
+
 // ---- warp utilities --------------------------------------------------------------
 __device__ __forceinline__ int warp_excl_prefix(unsigned ballot) {
     return __popc(ballot & ((1u << lane_id()) - 1u));

@@ -1,4 +1,6 @@
 // Beam-search kNN, single searches, exact kNN and the dependent-point scan.
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "../../include/peakann_b200.h"
@@ -6,37 +8,6 @@
 #include "beam.cuh"
 
 namespace pk {
-
-// ---- distance factories ------------------------------------------------------------
-template <int MODE, int QV>
-struct DistOf;
-
-template <int QV>
-struct DistOf<PK_MODE_SEQ64, QV> {
-    using T = Seq64Member;
-    __device__ static T make(const float* X, int dp, unsigned id) { return T{X + (size_t)id * dp, dp}; }
-};
-
-template <int QV>
-struct DistOf<PK_MODE_EXACT32, QV> {
-    using T = Exact32<QV>;
-    __device__ static T make(const float* X, int dp, unsigned id) {
-        T t;
-        t.load(X + (size_t)id * dp, dp);
-        return t;
-    }
-};
-
-__device__ __forceinline__ BeamSmem carve_beam(unsigned char* base, int L, int H) {
-    BeamSmem s;
-    s.bd = reinterpret_cast<double*>(base);
-    s.bi = reinterpret_cast<unsigned*>(base + (size_t)L * 8);
-    s.hash = reinterpret_cast<unsigned*>(base + (size_t)L * 12);
-    s.hmask = (unsigned)H - 1u;
-    s.spos = reinterpret_cast<int*>(base + (size_t)L * 12 + (size_t)H * 4);
-    s.cbuf = reinterpret_cast<unsigned*>(base + (size_t)L * 12 + (size_t)H * 4 + 128);
-    return s;
-}
 
 // ---- beam kNN of member queries (_kernels.py:230-262) --------------------------------
 template <int MODE, int QV>
@@ -53,10 +24,10 @@ __global__ void __launch_bounds__(128) beam_knn_kernel(SearchParams P, const lon
     long long ev = 0, ex = 0;
     for (long long t = (long long)blockIdx.x * wpb + wib; t < m; t += (long long)gridDim.x * wpb) {
         const unsigned qi = (unsigned)qids[t];
-        auto dist = DistOf<MODE, QV>::make(P.X, P.dp, qi);
+        auto dist = DistFor<MODE, QV>::make(P.data(), qi);
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, L, nullptr, nullptr, 0, nullptr);
-        wb.seed(P, dist);
+        wb.seed(P, dist, false);
         wb.walk(P, dist);
         long long* oi = out_ids + t * kk;
         double* od = out_d + t * kk;
@@ -95,7 +66,7 @@ __global__ void single_search_kernel(SearchParams P, Dist dist, unsigned self, i
     __syncwarp();
     WarpBeam<Dist> wb;
     wb.init(sm, L, vtmp_i, vtmp_d, vcap, &s_err);
-    wb.seed(P, dist);
+    wb.seed(P, dist, true);
     wb.walk(P, dist);
     int got = wb.emit(self, k, top_ids, top_d);
     const int lane = lane_id();
@@ -397,7 +368,24 @@ __global__ void check_exact32_kernel(const float* x, long long total, int dp, in
 __global__ void finish_exact32_kernel(const int* bad, const unsigned* range, int d, int* flag) {
     double span = (double)from_ordered(range[0]) - (double)from_ordered(range[1]);
     double bound = (double)d * span * span;
-    *flag = (*bad == 0 && bound < 16777216.0) ? 1 : 0;
+    // 2: bytes (x - min) hold every coordinate exactly; 1: float32 sums exact
+    *flag = *bad ? 0 : span <= 255.0 ? 2 : bound < 16777216.0 ? 1 : 0;
+}
+
+__global__ void pack_u8_kernel(const float* x, long long n, int dp, int d, const unsigned* range, int dw,
+                               unsigned* out) {
+    const float lo = from_ordered(range[1]);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n * dw; i += (long long)gridDim.x * blockDim.x) {
+        long long r = i / dw;
+        int w = (int)(i % dw);
+        unsigned v = 0;
+        for (int b = 0; b < 4; ++b) {
+            int t = 4 * w + b;
+            unsigned byte = t < d ? (unsigned)(x[r * dp + t] - lo) : 0u;
+            v |= byte << (8 * b);
+        }
+        out[i] = v;
+    }
 }
 
 __global__ void sqrt_kernel(const double* a, long long count, double* out) {
@@ -462,8 +450,8 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
 template <int MODE>
 int dispatch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, int kk, int H,
                       long long* out_ids, double* out_d, long long* counts, long long* evals, cudaStream_t st) {
-    if (MODE == PK_MODE_SEQ64) return launch_beam_knn<MODE, 1>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
-    int qv = (P.dp + 127) / 128;
+    if (MODE == MODE_SEQ64) return launch_beam_knn<MODE, 1>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
+    int qv = MODE == MODE_EXACT_U8 ? (P.dw + 31) / 32 : (P.dp + 127) / 128;
     if (qv <= 1) return launch_beam_knn<MODE, 1>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
     if (qv <= 2) return launch_beam_knn<MODE, 2>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
     if (qv <= 4) return launch_beam_knn<MODE, 4>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
@@ -483,7 +471,7 @@ int run_brute(const float* x, int n, int dp, const long long* qids, const double
     long long maxg = (2ll << 30) / (per_block > 0 ? per_block : 1);
     if (maxg < 1) maxg = 1;
     if (grid > maxg) grid = (int)maxg;
-    if (!rowlist && grid > m) grid = m;
+    if (grid > m) grid = m;
     double* scr = nullptr;
     double* sd = nullptr;
     unsigned* si = nullptr;
@@ -530,7 +518,32 @@ extern "C" int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d
     return 0;
 }
 
-extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, const int32_t* adj, int64_t R,
+extern "C" int pk_pack_u8(const float* x, int64_t n, int64_t dp, int64_t d, uint32_t* out, int64_t dw, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    int* bad = nullptr;
+    unsigned* mx = nullptr;
+    PK_CHECK(scratch(&bad, 1, st));
+    PK_CHECK(scratch(&mx, 2, st));
+    PK_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    PK_CHECK(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
+    PK_CHECK(cudaMemsetAsync(mx + 1, 0xff, sizeof(unsigned), st));
+    long long total = n * dp;
+    {
+        ProfScope _ps("check_exact32_kernel", st);
+        check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx);
+    }
+    {
+        ProfScope _ps("pack_u8_kernel", st);
+        pack_u8_kernel<<<grid_for(n * dw, 256), 256, 0, st>>>(x, n, (int)dp, (int)d, mx, (int)dw, out);
+    }
+    PK_CHECK_LAUNCH("pack_u8");
+    release(bad, st);
+    release(mx, st);
+    return 0;
+}
+
+extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                           const int32_t* adj, int64_t R,
                            const int32_t* deg, const int32_t* starts, int64_t s, const int64_t* qids, int64_t m,
                            int64_t L, int64_t k, int64_t* out_ids, double* out_sqd, int64_t* out_counts,
                            int brute_fallback, int64_t* out_evals, int hash_bits, void* stream) {
@@ -544,25 +557,25 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, cons
         set_error("beam width L must be >= k");
         return 2;
     }
-    unsigned* bm = nullptr;
-    size_t words = (size_t)(n + 31) / 32;
-    PK_CHECK(scratch(&bm, words, st));
-    PK_CHECK(cudaMemsetAsync(bm, 0, words * 4, st));
-    {
-        ProfScope _ps("start_bitmap_kernel", st);
-        start_bitmap_kernel<<<grid_for(s, 256), 256, 0, st>>>(starts, (int)s, bm);
-    }
-    SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, bm};
+    // Start points re-met as neighbours are simply re-evaluated (and dropped
+    // by the key-equality check when already in the beam): cheaper than a
+    // dependent bitmap load on every neighbour.
+    SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, nullptr, x8, (int)dw};
     int H = choose_hash((int)L, hash_bits);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);
     long long* oc = reinterpret_cast<long long*>(out_counts);
     long long* ev = reinterpret_cast<long long*>(out_evals);
-    int rc = mode == PK_MODE_EXACT32
-                 ? dispatch_beam_knn<PK_MODE_EXACT32>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st)
-                 : dispatch_beam_knn<PK_MODE_SEQ64>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st);
+    if (mode == MODE_EXACT_U8 && !x8) {
+        set_error("u8 mode needs the packed rows");
+        return 2;
+    }
+    int rc = mode == MODE_EXACT_U8
+                 ? dispatch_beam_knn<MODE_EXACT_U8>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st)
+             : mode == MODE_EXACT32
+                 ? dispatch_beam_knn<MODE_EXACT32>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st)
+                 : dispatch_beam_knn<MODE_SEQ64>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st);
     if (rc) return rc;
-    release(bm, st);
     if (brute_fallback) {
         int* list = nullptr;
         int* nl = nullptr;
@@ -574,7 +587,14 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, int mode, cons
             short_rows_kernel<<<grid_for(m, 256), 256, 0, st>>>(oc, (int)m, (int)kk, list, nl);
         }
         PK_CHECK_LAUNCH("short_rows_kernel");
-        rc = run_brute(x, (int)n, (int)dp, q, nullptr, list, nl, (int)m, (int)kk, oi, out_sqd, st);
+        // short rows are rare (disconnected or duplicate-heavy regions): read
+        // the count so the exact pass and its row scratch run only when needed
+        int hshort = 0;
+        PK_CHECK(cudaMemcpyAsync(&hshort, nl, sizeof(int), cudaMemcpyDeviceToHost, st));
+        PK_CHECK(cudaStreamSynchronize(st));
+        if (hshort > 0)
+            rc = run_brute(x, (int)n, (int)dp, q, nullptr, list, nl, std::min<int>((int)m, hshort), (int)kk, oi,
+                           out_sqd, st);
         release(list, st);
         release(nl, st);
         if (rc) return rc;

@@ -238,7 +238,7 @@ def build_graph_device(p: PointSet, R: int, L_build: int, alpha: float, starts: 
     od = order_t if order_t is not None else _lib.to_dev(order.astype(np.int32))
     if stats is None:
         stats = STATS["build"]
-    _lib.call("pk_build_vamana", p.device(), p.n, p.dp, p.mode, R, L_build, float(alpha), st, st.shape[0], od, adj,
+    _lib.call("pk_build_vamana", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, R, L_build, float(alpha), st, st.shape[0], od, adj,
               deg, stats, 0, _lib.stream())
     return adj, deg
 
@@ -281,7 +281,7 @@ def beam_knn_raw(g: GraphIndex, qids_t, L: int, k: int, evals=None, hash_bits: i
     sqd = torch.empty((m, kk), dtype=torch.float64, device=dev)
     counts = torch.zeros(m, dtype=torch.int64, device=dev)
     if kk > 0 and m > 0:
-        _lib.call("pk_beam_knn", p.device(), p.n, p.dp, p.mode, adj, g.R, deg, st, st.shape[0], qids_t, m, L, k, ids,
+        _lib.call("pk_beam_knn", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, adj, g.R, deg, st, st.shape[0], qids_t, m, L, k, ids,
                   sqd, counts, 0, evals, hash_bits, _lib.stream())
     return ids, sqd, counts
 
@@ -302,7 +302,7 @@ def beam_knn_device(g: GraphIndex, qids_t, k: int, L: int, evals=None):
     sqd = torch.empty((m, kk), dtype=torch.float64, device=dev)
     counts = torch.empty(m, dtype=torch.int64, device=dev)
     if kk > 0 and m > 0:
-        _lib.call("pk_beam_knn", p.device(), p.n, p.dp, p.mode, adj, g.R, deg, st, st.shape[0], qids_t, m, L, k, ids,
+        _lib.call("pk_beam_knn", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, adj, g.R, deg, st, st.shape[0], qids_t, m, L, k, ids,
                   sqd, counts, 1, evals, 0, _lib.stream())
     return ids, sqd
 

@@ -40,10 +40,12 @@ def points(data, mode=None):
     p = pk.PointSet(data)
     if mode == "seq64":
         p._mode = _lib.MODE_SEQ64
+    elif mode == "exact32" and p.mode == _lib.MODE_EXACT_U8:
+        p._mode = _lib.MODE_EXACT32
     return p
 
 
-@pytest.mark.parametrize("mode", [None, "seq64"])
+@pytest.mark.parametrize("mode", [None, "exact32", "seq64"])
 def test_brute_knn_golden(mode):
     z = golden("brute")
     for tag in _tags(z, "__data"):
@@ -61,7 +63,7 @@ def test_brute_knn_golden(mode):
         assert np.array_equal(nl.dists, np.sqrt(z[f"{tag}__vec__sqd"])), tag
 
 
-@pytest.mark.parametrize("mode", [None, "seq64"])
+@pytest.mark.parametrize("mode", [None, "exact32", "seq64"])
 def test_build_matches_reference_graph(mode):
     z = golden("graphs")
     for tag in _tags(z, "__adj"):
@@ -77,7 +79,7 @@ def test_build_matches_reference_graph(mode):
         assert np.array_equal(g.adjacency, z[f"{tag}__adj"]), tag
 
 
-@pytest.mark.parametrize("mode", [None, "seq64"])
+@pytest.mark.parametrize("mode", [None, "exact32", "seq64"])
 def test_beam_knn_on_reference_graphs(mode):
     z = golden("graphs")
     for tag in _tags(z, "__adj"):
