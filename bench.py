@@ -139,7 +139,7 @@ def cpu_pipeline(name, n_override=None):
     else:
         # bounded sample: the full configuration when the host has many cores,
         # otherwise a smaller instance of the same generator (~10-30 s)
-        n = w.n if cores >= 48 else max(10_000, int(w.n * cores / 64))
+        n = min(w.n, max(10_000, cores * 3_000))
     comps = max(1, int(round(w.components * n / w.n)))
     data, _ = workloads.generate(name, n=n, components=comps)
     oracle.build()
