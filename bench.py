@@ -318,7 +318,7 @@ def main_ours(args):
     be = _lib.to_host(beam_stats) / args.steps
     s = int(np.ceil(np.sqrt(n)))
     d4 = w.d * 4
-    if dom_name.startswith("build_batch"):
+    if dom_name.startswith("build_search"):
         # per inserted point: non-seed unique search evaluations + adjacency rows + current out-row
         evals_nonseed = bs[0] - n * s
         alg_bytes = evals_nonseed * d4 + bs[3] * w.R * 4

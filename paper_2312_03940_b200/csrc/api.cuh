@@ -45,14 +45,20 @@ inline void release(void* p, cudaStream_t st) {
 
 // per-warp shared memory sizes
 inline size_t beam_smem_bytes(int L, int H) {
-    return (size_t)L * 12 + (size_t)H * 4 + 128 + 4 * 64;
+    return (((size_t)L * 12 + (size_t)H * 2 + 15) & ~(size_t)15) + 128 + 4 * 64;
 }
 inline size_t sort_smem_bytes(int cap) {
     return (size_t)cap * 13 + 128;
 }
 inline size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
+// candidate buffers of the prune kernels (layout: carve_cand in build.cu)
+inline size_t cand_smem_bytes(int cap, int dw, int S, bool u8) {
+    size_t keys = align16(((((size_t)cap * 15 + 3) & ~(size_t)3) + 128));
+    if (!u8) return keys;
+    return align16(keys + (((size_t)dw + 3) & ~(size_t)3) * 4 + (size_t)S * (dw + 1) * 4);
+}
 
-int choose_hash(int L, int hash_bits);
+int choose_hash(int L, int hash_bits, long long n);
 
 // ---- launch accounting -------------------------------------------------------
 // Every kernel launch site opens a ProfScope: launches are always counted per

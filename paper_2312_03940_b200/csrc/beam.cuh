@@ -32,22 +32,27 @@ namespace pk {
 struct BeamSmem {
     double* bd;       // [Lcap] squared distances, (dist,id)-sorted
     unsigned* bi;     // [Lcap] ids | PK_VIS
-    unsigned* hash;   // [hmask+1] lossy seen table, 0xffffffff = empty
+    unsigned short* hash;  // [hmask+1] lossy seen table (common.cuh), 0xffff = empty
     unsigned hmask;
+    int hbits;
     int* spos;        // [32] scratch: sorted insert positions
-    unsigned* cbuf;   // [32] scratch: compacted candidate ids
+    unsigned* cbuf;   // [kCbuf] scratch: compacted candidate ids
 };
 
 constexpr int kCbuf = 64;  // compacted-candidate buffer (ids) per warp
 
+// per-warp layout: bd[L] | bi[L] | hash[H] (u16) | spos[32] | cbuf[kCbuf]
+// (host side: beam_smem_bytes in api.cuh)
 __device__ __forceinline__ BeamSmem carve_beam(unsigned char* base, int L, int H) {
     BeamSmem s;
     s.bd = reinterpret_cast<double*>(base);
     s.bi = reinterpret_cast<unsigned*>(base + (size_t)L * 8);
-    s.hash = reinterpret_cast<unsigned*>(base + (size_t)L * 12);
+    s.hash = reinterpret_cast<unsigned short*>(base + (size_t)L * 12);
     s.hmask = (unsigned)H - 1u;
-    s.spos = reinterpret_cast<int*>(base + (size_t)L * 12 + (size_t)H * 4);
-    s.cbuf = reinterpret_cast<unsigned*>(base + (size_t)L * 12 + (size_t)H * 4 + 128);
+    s.hbits = __ffs(H) - 1;
+    const size_t tail = ((size_t)L * 12 + (size_t)H * 2 + 15) & ~(size_t)15;
+    s.spos = reinterpret_cast<int*>(base + tail);
+    s.cbuf = reinterpret_cast<unsigned*>(base + tail + 128);
     return s;
 }
 
@@ -94,7 +99,8 @@ struct WarpBeam {
         vl = 0;
         err = err_;
         evals = 0;
-        for (unsigned h = lane_id(); h <= sm.hmask; h += 32) sm.hash[h] = 0xffffffffu;
+        unsigned* h32 = reinterpret_cast<unsigned*>(sm.hash);
+        for (unsigned h = lane_id(); h <= sm.hmask / 2; h += 32) h32[h] = 0xffffffffu;
         __syncwarp();
     }
 
@@ -197,7 +203,7 @@ struct WarpBeam {
         for (int b = 0; b < P.s; b += 32) {
             const int cnt = min(32, P.s - b);
             unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
-            if (hash_starts && lane < cnt) seen_or_insert(sm.hash, sm.hmask, id);
+            if (hash_starts && lane < cnt) seen_or_insert(sm.hash, sm.hmask, sm.hbits, id);
             double dd = dist.eval(P.X, (int)id, cnt);
             if (lane == 0) evals += cnt;
             merge<true>(dd, id, lane < cnt);
@@ -247,7 +253,7 @@ struct WarpBeam {
                 int w = e0 + lane < nd ? __ldg(row + e0 + lane) : -1;
                 bool cand = w >= 0;
                 if (cand && P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u)) cand = false;
-                if (cand && seen_or_insert(sm.hash, sm.hmask, (unsigned)w)) cand = false;
+                if (cand && seen_or_insert(sm.hash, sm.hmask, sm.hbits, (unsigned)w)) cand = false;
                 unsigned b = __ballot_sync(PK_FULL, cand);
                 const int nb = __popc(b);
                 if (c + nb > kCbuf) {  // very wide rows: flush before the buffer overflows
@@ -337,6 +343,60 @@ __device__ __forceinline__ void warp_sort(double* kd, unsigned* ki, int P) {
             __syncwarp();
         }
     }
+}
+
+// Same sort carrying a 16-bit payload (the staged-row slot of each key).
+__device__ __forceinline__ void warp_sort_pos(double* kd, unsigned* ki, unsigned short* kp, int P) {
+    const int lane = lane_id();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                int x = i ^ j;
+                if (x > i) {
+                    double a = kd[i], b = kd[x];
+                    unsigned ia = ki[i], ib = ki[x];
+                    bool asc = (i & k) == 0;
+                    if (key_lt(b, ib, a, ia) == asc) {
+                        kd[i] = b; kd[x] = a;
+                        ki[i] = ib; ki[x] = ia;
+                        unsigned short pa = kp[i];
+                        kp[i] = kp[x];
+                        kp[x] = pa;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__device__ __forceinline__ int warp_unique_pos(double* kd, unsigned* ki, unsigned short* kp, int c, unsigned self) {
+    const int lane = lane_id();
+    int out = 0;
+    for (int base = 0; base < c; base += 32) {
+        int i = base + lane;
+        double d = 0.0;
+        unsigned id = self;
+        unsigned short ps = 0;
+        bool keep = false;
+        if (i < c) {
+            d = kd[i];
+            id = ki[i];
+            ps = kp[i];
+            keep = id != self && !(i > 0 && ki[i - 1] == id && kd[i - 1] == d);
+        }
+        unsigned b = __ballot_sync(PK_FULL, keep);
+        __syncwarp();
+        if (keep) {
+            int o = out + warp_excl_prefix(b);
+            kd[o] = d;
+            ki[o] = id;
+            kp[o] = ps;
+        }
+        out += __popc(b);
+        __syncwarp();
+    }
+    return out;
 }
 
 // Drop duplicate keys (same id => same dist) and `self`, in place; returns count.
@@ -444,9 +504,11 @@ __device__ __forceinline__ void stage_u8_rows(const unsigned* __restrict__ X8, i
 // whole row pair evaluated sequentially with exact integer dp4a arithmetic.
 // Alive candidates after the current pick are queued 32 at a time so every
 // lane has work.
-static __device__ int warp_prune_u8(const unsigned* __restrict__ X8, int dw, const double* kd, const unsigned* ki, int c,
-                             double alpha2, int R, unsigned char* alive, unsigned* cbuf, int* out,
-                             const unsigned* rows, int rs, int S, long long* evals) {
+// kp[u] = staged row slot of candidate u (rows[kp[u]] if kp[u] < S, else the
+// row is read from global memory by id).
+static __device__ int warp_prune_u8(const unsigned* __restrict__ X8, int dw, const double* kd, const unsigned* ki,
+                                    const unsigned short* kp, int c, double alpha2, int R, unsigned char* alive,
+                                    unsigned* cbuf, int* out, const unsigned* rows, int rs, int S, long long* evals) {
     const int lane = lane_id();
     for (int i = lane; i < c; i += 32) alive[i] = 1;
     __syncwarp();
@@ -464,13 +526,13 @@ static __device__ int warp_prune_u8(const unsigned* __restrict__ X8, int dw, con
         if (lane == 0) out[sel] = (int)ki[t];
         ++sel;
         if (sel >= R) break;
-        const unsigned* rt = t < S ? rows + (size_t)t * rs : X8 + (size_t)ki[t] * dw;
+        const unsigned* rt = kp[t] < S ? rows + (size_t)kp[t] * rs : X8 + (size_t)ki[t] * dw;
         int nq = 0;
         auto run = [&](int cnt) {
             __syncwarp();
             if (lane < cnt) {
                 const int u = (int)cbuf[lane];
-                const unsigned* ru = u < S ? rows + (size_t)u * rs : X8 + (size_t)ki[u] * dw;
+                const unsigned* ru = kp[u] < S ? rows + (size_t)kp[u] * rs : X8 + (size_t)ki[u] * dw;
                 const unsigned duv = u8_row_dist(rt, ru, dw);
                 if (alpha2 * (double)duv <= kd[u]) alive[u] = 0;
             }

@@ -77,35 +77,59 @@ __global__ void __launch_bounds__(128) build_search_kernel(BuildArgs A) {
     }
 }
 
-// shared-memory view of the candidate buffers of one warp
+// Shared-memory view of the candidate buffers of one warp (host size:
+// cand_smem_bytes in api.cuh):
+//   kd[cap] f64 | ki[cap] u32 | kp[cap] u16 | alive[cap] u8 | cbuf[32] u32 |
+//   qrow[dw] u32 | rows[S][dw + 1] u32   (the last two in the u8 mode only)
 struct CandSmem {
     double* kd;
     unsigned* ki;
-    unsigned* cbuf;
+    unsigned short* kp;
     unsigned char* alive;
+    unsigned* cbuf;
+    unsigned* qrow;
     unsigned* rows;
 };
 
-__device__ __forceinline__ CandSmem carve_cand(unsigned char* base, int cap) {
+__device__ __forceinline__ CandSmem carve_cand(unsigned char* base, int cap, int dw) {
     CandSmem c;
     c.kd = reinterpret_cast<double*>(base);
     c.ki = reinterpret_cast<unsigned*>(base + (size_t)cap * 8);
-    c.cbuf = reinterpret_cast<unsigned*>(base + (size_t)cap * 12);
-    c.alive = base + (size_t)cap * 12 + 128;
-    c.rows = reinterpret_cast<unsigned*>(base + (((size_t)cap * 13 + 128 + 15) & ~(size_t)15));
+    c.kp = reinterpret_cast<unsigned short*>(base + (size_t)cap * 12);
+    c.alive = base + (size_t)cap * 14;
+    c.cbuf = reinterpret_cast<unsigned*>(base + (((size_t)cap * 15 + 3) & ~(size_t)3));
+    const size_t q = (((size_t)cap * 15 + 3) & ~(size_t)3) + 128;
+    c.qrow = reinterpret_cast<unsigned*>(base + ((q + 15) & ~(size_t)15));
+    c.rows = c.qrow + (((size_t)dw + 3) & ~(size_t)3);
     return c;
 }
 
-// sorted, de-duplicated candidates kd/ki[0..c) -> RobustPrune picks in out[]
+// Stage candidate rows ki[0..c) in input order (slot = position) plus the
+// query row, then compute kd[x] = d(query, ki[x]) one lane per candidate from
+// shared memory (u8 mode).  Returns the number of staged rows.
+__device__ __forceinline__ int stage_and_measure_u8(const DataRef& D, const CandSmem& C, unsigned q, int c, int S,
+                                                    int from, long long* ev) {
+    const int lane = lane_id();
+    const int rs = D.dw + 1;
+    const int st = min(c, S);
+    for (int w = lane; w < D.dw; w += 32) C.qrow[w] = __ldg(D.X8 + (size_t)q * D.dw + w);
+    stage_u8_rows(D.X8, D.dw, C.ki, st, C.rows, rs);
+    for (int x = from + lane; x < c; x += 32) {
+        const unsigned* rx = x < st ? C.rows + (size_t)x * rs : D.X8 + (size_t)C.ki[x] * D.dw;
+        C.kd[x] = (double)u8_row_dist(C.qrow, rx, D.dw);
+    }
+    if (lane == 0) *ev += c - from;
+    __syncwarp();
+    return st;
+}
+
+// sorted, de-duplicated candidates kd/ki/kp[0..c) -> RobustPrune picks in out[]
 template <int MODE, int QV>
 __device__ __forceinline__ int prune_candidates(const DataRef& D, const CandSmem& C, int c, double alpha2, int R,
-                                                int S, int* out, long long* ev) {
-    if (MODE == MODE_EXACT_U8) {
-        const int rs = D.dw + 1;
-        const int st = min(c, S);
-        stage_u8_rows(D.X8, D.dw, C.ki, st, C.rows, rs);
-        return warp_prune_u8(D.X8, D.dw, C.kd, C.ki, c, alpha2, R, C.alive, C.cbuf, out, C.rows, rs, st, ev);
-    }
+                                                int staged, int* out, long long* ev) {
+    if (MODE == MODE_EXACT_U8)
+        return warp_prune_u8(D.X8, D.dw, C.kd, C.ki, C.kp, c, alpha2, R, C.alive, C.cbuf, out, C.rows, D.dw + 1,
+                             staged, ev);
     const MakeAt<MODE, QV> make{D};
     return warp_prune(D.X, C.kd, C.ki, c, alpha2, R, C.alive, C.cbuf, out, make, ev);
 }
@@ -118,58 +142,60 @@ __global__ void __launch_bounds__(128) build_prune_kernel(BuildArgs A) {
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int lane = lane_id();
-    const CandSmem C = carve_cand(smem + (size_t)wib * A.prune_bytes, A.cap);
+    const CandSmem C = carve_cand(smem + (size_t)wib * A.prune_bytes, A.cap, A.D.dw);
     const MakeAt<MODE, QV> make{A.D};
-    long long ev_search = 0, ev_prune = 0;
+    long long ev_prune = 0;
     const int R = A.P.R;
     for (int t = blockIdx.x * wpb + wib; t < A.m; t += gridDim.x * wpb) {
         const unsigned p = (unsigned)A.bids[t];
         const int vl = A.vlen[t];
         const unsigned* vi = A.vlog_i + (size_t)t * A.vcap;
         const double* vd = A.vlog_d + (size_t)t * A.vcap;
-        for (int x = lane; x < vl; x += 32) {
-            C.kd[x] = vd[x];
-            C.ki[x] = vi[x];
-        }
         const int nd = __ldg(A.P.deg + p);
         const int* row = A.P.adj + (size_t)p * R;
-        int c = vl;
-        if (nd > 0) {
-            auto dist = make(p);
-            for (int e0 = 0; e0 < nd; e0 += 32) {
-                const int cnt = min(32, nd - e0);
-                unsigned w = lane < cnt ? (unsigned)__ldg(row + e0 + lane) : 0u;
-                double dd = dist.eval(A.D.X, (int)w, cnt);
-                if (lane == 0) ev_search += cnt;
-                if (lane < cnt && c + lane < A.cap) {
-                    C.kd[c + lane] = dd;
-                    C.ki[c + lane] = w;
-                }
-                c += cnt;
+        int c = min(vl + nd, A.cap);
+        if (vl + nd > A.cap && lane == 0) atomicOr(A.err, ERR_CAND_OVERFLOW);
+        // candidates in input order: visit log (distances known), then out-row
+        for (int x = lane; x < c; x += 32) {
+            if (x < vl) {
+                C.kd[x] = vd[x];
+                C.ki[x] = vi[x];
+            } else {
+                C.ki[x] = (unsigned)__ldg(row + x - vl);
             }
+            C.kp[x] = (unsigned short)x;
         }
-        if (c > A.cap) {
-            if (lane == 0) atomicOr(A.err, ERR_CAND_OVERFLOW);
-            c = A.cap;
+        __syncwarp();
+        int staged = 0;
+        if (MODE == MODE_EXACT_U8) {
+            staged = stage_and_measure_u8(A.D, C, p, c, A.S, min(vl, c), &ev_prune);
+        } else if (nd > 0) {
+            auto dist = make(p);
+            for (int e0 = vl; e0 < c; e0 += 32) {
+                const int cnt = min(32, c - e0);
+                unsigned w = lane < cnt ? C.ki[e0 + lane] : 0u;
+                double dd = dist.eval(A.D.X, (int)w, cnt);
+                if (lane == 0) ev_prune += cnt;
+                if (lane < cnt) C.kd[e0 + lane] = dd;
+            }
         }
         const int Pw = next_pow2_dev(c);
         for (int x = c + lane; x < Pw; x += 32) {
             C.kd[x] = __longlong_as_double(0x7ff0000000000000LL);
             C.ki[x] = 0xffffffffu;
+            C.kp[x] = 0xffffu;
         }
         __syncwarp();
-        warp_sort(C.kd, C.ki, Pw);
-        c = warp_unique(C.kd, C.ki, c, p);
+        warp_sort_pos(C.kd, C.ki, C.kp, Pw);
+        c = warp_unique_pos(C.kd, C.ki, C.kp, c, p);
         int* out = A.new_ids + (size_t)t * R;
-        int sel = prune_candidates<MODE, QV>(A.D, C, c, A.alpha2, R, A.S, out, &ev_prune);
+        int sel = prune_candidates<MODE, QV>(A.D, C, c, A.alpha2, R, staged, out, &ev_prune);
         for (int x = sel + lane; x < R; x += 32) out[x] = -1;
         if (lane == 0) A.new_len[t] = sel;
         __syncwarp();
     }
-    if (lane == 0 && A.stats) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 0), (unsigned long long)ev_search);
+    if (lane == 0 && A.stats)
         atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 1), (unsigned long long)ev_prune);
-    }
 }
 
 // write staged rows, count reverse edges, register targets (warp per point)
@@ -233,6 +259,9 @@ struct RevArgs {
     double alpha2;
     size_t warp_bytes;
     long long* stats;
+    int capB;       // largest group handled by reverse_big_kernel
+    int* biglist;   // groups with cap < candidates <= capB
+    int* nbig;
 };
 
 // Oversized group (more candidates than the shared buffer): RobustPrune by
@@ -328,7 +357,7 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int lane = lane_id();
-    const CandSmem C = carve_cand(smem + (size_t)wib * A.warp_bytes, A.cap);
+    const CandSmem C = carve_cand(smem + (size_t)wib * A.warp_bytes, A.cap, A.D.dw);
     double* kd = C.kd;
     unsigned* ki = C.ki;
     unsigned* pcbuf = C.cbuf;
@@ -345,33 +374,44 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
         const int c0 = nd + size;
         int sel;
         if (c0 <= A.cap) {
-            auto du = make(u);
-            for (int e0 = 0; e0 < c0; e0 += 32) {
-                const int cnt = min(32, c0 - e0);
-                const int x = e0 + lane;
-                unsigned w = 0u;
-                if (lane < cnt) w = x < nd ? (unsigned)row[x] : (unsigned)A.adds[off + x - nd];
-                double dd = du.eval(A.X, (int)w, cnt);
-                if (lane < cnt) {
-                    kd[x] = dd;
-                    ki[x] = w;
-                }
+            for (int x = lane; x < c0; x += 32) {
+                ki[x] = x < nd ? (unsigned)row[x] : (unsigned)A.adds[off + x - nd];
+                C.kp[x] = (unsigned short)x;
             }
-            ev += c0;
+            __syncwarp();
+            int staged = 0;
+            if (MODE == MODE_EXACT_U8) {
+                staged = stage_and_measure_u8(A.D, C, u, c0, A.S, 0, &ev);
+            } else {
+                auto du = make(u);
+                for (int e0 = 0; e0 < c0; e0 += 32) {
+                    const int cnt = min(32, c0 - e0);
+                    unsigned w = lane < cnt ? ki[e0 + lane] : 0u;
+                    double dd = du.eval(A.X, (int)w, cnt);
+                    if (lane < cnt) kd[e0 + lane] = dd;
+                }
+                ev += c0;
+            }
             const int Pw = next_pow2_dev(c0);
             for (int x = c0 + lane; x < Pw; x += 32) {
                 kd[x] = __longlong_as_double(0x7ff0000000000000LL);
                 ki[x] = 0xffffffffu;
+                C.kp[x] = 0xffffu;
             }
             __syncwarp();
-            warp_sort(kd, ki, Pw);
-            const int c = warp_unique(kd, ki, c0, u);
+            warp_sort_pos(kd, ki, C.kp, Pw);
+            const int c = warp_unique_pos(kd, ki, C.kp, c0, u);
             if (c <= A.R) {
                 for (int x = lane; x < c; x += 32) row[x] = (int)ki[x];
                 sel = c;
             } else {
-                sel = prune_candidates<MODE, QV>(A.D, C, c, A.alpha2, A.R, A.S, row, &ev);
+                sel = prune_candidates<MODE, QV>(A.D, C, c, A.alpha2, A.R, staged, row, &ev);
             }
+        } else if (c0 <= A.capB) {
+            // large group: handled by a whole block in reverse_big_kernel
+            if (lane == 0) A.biglist[atomicAdd(A.nbig, 1)] = s;
+            __syncwarp();
+            continue;
         } else {
             sel = prune_by_selection(A, u, make, kd, ki, alive, pcbuf, nd, off, size, row, &ev);
         }
@@ -384,6 +424,108 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
         __syncwarp();
     }
     if (lane == 0 && A.stats && ev) atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 2), (unsigned long long)ev);
+}
+
+// one thread, one full distance between two point ids (exact in every mode)
+template <int MODE>
+__device__ __forceinline__ double thread_dist(const DataRef& D, unsigned a, unsigned b) {
+    if (MODE == MODE_EXACT_U8) return (double)u8_row_dist(D.X8 + (size_t)a * D.dw, D.X8 + (size_t)b * D.dw, D.dw);
+    Seq64Member q{D.X + (size_t)a * D.dp, D.dp};
+    return q.eval_one(D.X, (int)b);
+}
+
+constexpr int kBigThreads = 256;
+
+// Reverse-edge groups with more than A.cap candidates (hub vertices that
+// receive hundreds of new in-edges in one batch): one block per group.
+// Candidates are sorted by (dist, id) with a block bitonic sort; duplicates
+// and the vertex itself are marked dead instead of compacted; the RobustPrune
+// picks stay sequential, each kill step runs over all block threads.
+template <int MODE>
+__global__ void __launch_bounds__(kBigThreads) reverse_big_kernel(RevArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* kd = reinterpret_cast<double*>(smem);
+    unsigned* ki = reinterpret_cast<unsigned*>(smem + (size_t)A.capB * 8);
+    unsigned char* alive = smem + (size_t)A.capB * 12;
+    __shared__ int s_t;
+    const int tid = threadIdx.x;
+    const int nb = *A.nbig;
+    long long ev = 0;
+    for (int g = blockIdx.x; g < nb; g += gridDim.x) {
+        const int s = A.biglist[g];
+        const unsigned u = (unsigned)A.targets[s];
+        const int nd = A.deg[u];
+        const int off = A.offs[s];
+        const int c0 = nd + A.sizes[s];
+        int* row = A.adj + (size_t)u * A.R;
+        const int P = next_pow2_dev(c0);
+        for (int x = tid; x < P; x += kBigThreads) {
+            if (x < c0) {
+                const unsigned w = x < nd ? (unsigned)row[x] : (unsigned)A.adds[off + x - nd];
+                ki[x] = w;
+                kd[x] = thread_dist<MODE>(A.D, u, w);
+            } else {
+                ki[x] = 0xffffffffu;
+                kd[x] = __longlong_as_double(0x7ff0000000000000LL);
+            }
+        }
+        ev += c0;
+        __syncthreads();
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < P; i += kBigThreads) {
+                    const int x = i ^ j;
+                    if (x > i) {
+                        double a = kd[i], b = kd[x];
+                        unsigned ia = ki[i], ib = ki[x];
+                        if (key_lt(b, ib, a, ia) == ((i & k) == 0)) {
+                            kd[i] = b; kd[x] = a;
+                            ki[i] = ib; ki[x] = ia;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int x = tid; x < c0; x += kBigThreads)
+            alive[x] = ki[x] != u && !(x > 0 && ki[x - 1] == ki[x] && kd[x - 1] == kd[x]);
+        __syncthreads();
+        int sel = 0, t = 0;
+        while (sel < A.R) {
+            if (tid < 32) {
+                int nt = -1;
+                for (int base = t; base < c0; base += 32) {
+                    const int i = base + tid;
+                    const unsigned bal = __ballot_sync(PK_FULL, i < c0 && alive[i]);
+                    if (bal) { nt = base + __ffs(bal) - 1; break; }
+                }
+                if (tid == 0) s_t = nt;
+            }
+            __syncthreads();
+            t = s_t;
+            if (t < 0) break;
+            if (tid == 0) row[sel] = (int)ki[t];  // the row was fully read into ki above
+            ++sel;
+            if (sel >= A.R) break;
+            const unsigned ps = ki[t];
+            for (int x = t + 1 + tid; x < c0; x += kBigThreads) {
+                if (alive[x]) {
+                    ++ev;
+                    if (A.alpha2 * thread_dist<MODE>(A.D, ps, ki[x]) <= kd[x]) alive[x] = 0;
+                }
+            }
+            ++t;
+            __syncthreads();
+        }
+        __syncthreads();
+        for (int x = sel + tid; x < A.R; x += kBigThreads) row[x] = -1;
+        if (tid == 0) {
+            A.deg[u] = sel;
+            A.cnt[u] = 0;
+        }
+        __syncthreads();
+    }
+    if (A.stats && ev) atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 2), (unsigned long long)ev);
 }
 
 __global__ void robust_prune_api_kernel(const float* X, int dp, unsigned p, const long long* cand_ids,
@@ -508,26 +650,33 @@ template <int MODE, int QV>
 int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
               int* adj, int* deg, long long* stats, int hash_bits, cudaStream_t st) {
     const bool u8 = MODE == MODE_EXACT_U8;
-    const int H = choose_hash(L, hash_bits);
+    const int H = choose_hash(L, hash_bits, n);
     const int cap = next_pow2(2 * L + 64 + R);
     const int vcap = cap - R;
-    const int capR = 1024;
+    // reverse groups: row (<= R) + incoming sources; larger groups take the
+    // selection path (prune_by_selection)
+    const int capR = next_pow2(std::max(4 * R, 256));
     const int S = std::min(cap, 192);
-    const int SR = std::min(capR, 192);
-    const size_t rows_b = u8 ? (size_t)S * (D.dw + 1) * 4 : 0;
-    const size_t rows_br = u8 ? (size_t)SR * (D.dw + 1) * 4 : 0;
+    const int SR = std::min(capR, 128);
 
     BuildArgs A;
     A.search_bytes = align16(beam_smem_bytes(L, H));
-    A.prune_bytes = align16(align16(sort_smem_bytes(cap)) + rows_b);
+    A.prune_bytes = cand_smem_bytes(cap, D.dw, S, u8);
     auto sk = build_search_kernel<MODE, QV>;
     auto pkk = build_prune_kernel<MODE, QV>;
     auto rk = reverse_kernel<MODE, QV>;
     int wpb_s, grid_s, wpb_p, grid_p, wpb_r, grid_r, rc;
     if ((rc = config_kernel(sk, A.search_bytes, 4, &wpb_s, &grid_s))) return rc;
     if ((rc = config_kernel(pkk, A.prune_bytes, 2, &wpb_p, &grid_p))) return rc;
-    const size_t wbr = align16(align16(sort_smem_bytes(capR)) + rows_br);
+    const size_t wbr = cand_smem_bytes(capR, D.dw, SR, u8);
     if ((rc = config_kernel(rk, wbr, 2, &wpb_r, &grid_r))) return rc;
+    const int capB = 8192;
+    const size_t big_bytes = (size_t)capB * 13 + 16;
+    auto bigk = reverse_big_kernel<MODE>;
+    PK_CHECK(cudaFuncSetAttribute(bigk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_bytes));
+    const int grid_big = 2 * sm_count();
+    int* biglist = nullptr;
+    int* nbig = nullptr;
 
     int maxb = 1;
     while (maxb < n) maxb <<= 1;
@@ -555,6 +704,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     PK_CHECK(scratch(&adist, (size_t)E, st));
     PK_CHECK(scratch(&aalive, (size_t)E, st));
     PK_CHECK(scratch(&ntargets, 1, st));
+    PK_CHECK(scratch(&biglist, (size_t)ub, st));
+    PK_CHECK(scratch(&nbig, 1, st));
     PK_CHECK(scratch(&err, 1, st));
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -602,6 +753,9 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     B.alpha2 = alpha * alpha;
     B.warp_bytes = wbr;
     B.stats = stats;
+    B.capB = capB;
+    B.biglist = biglist;
+    B.nbig = nbig;
 
     for (int lo = 0, batch = 1; lo < n; lo += batch, batch *= 2) {
         const int m = std::min(batch, n - lo);
@@ -619,6 +773,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         PK_CHECK_LAUNCH("build_prune_kernel");
         const int ubb = (int)std::min<long long>(n, (long long)m * R);
         PK_CHECK(cudaMemsetAsync(ntargets, 0, sizeof(int), st));
+        PK_CHECK(cudaMemsetAsync(nbig, 0, sizeof(int), st));
         PK_CHECK(cudaMemsetAsync(sizes, 0, sizeof(int) * ((size_t)ubb + 1), st));
         PK_CHECK(cudaMemsetAsync(fill, 0, sizeof(int) * (size_t)ubb, st));
         {
@@ -647,12 +802,17 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             rk<<<std::min(grid_r, (ubb + wpb_r - 1) / wpb_r), 32 * wpb_r, wbr * wpb_r, st>>>(B);
         }
         PK_CHECK_LAUNCH("reverse_kernel");
+        {
+            ProfScope _ps("reverse_big_kernel", st);
+            bigk<<<grid_big, kBigThreads, big_bytes, st>>>(B);
+        }
+        PK_CHECK_LAUNCH("reverse_big_kernel");
     }
     unsigned herr = 0;
     PK_CHECK(cudaMemcpyAsync(&herr, err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)new_ids, (void*)new_len, (void*)cnt, (void*)tslot,
                     (void*)targets, (void*)sizes, (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive,
-                    (void*)ntargets, (void*)err, cub_tmp})
+                    (void*)ntargets, (void*)err, (void*)biglist, (void*)nbig, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

@@ -52,25 +52,30 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-// per-query "seen" table: open addressing, linear probe window of 8 slots,
-// lossy when the window is full (the id then overwrites its home slot).  A
-// lost id only costs a re-evaluation; ids are never reported seen falsely.
-__device__ __forceinline__ unsigned seen_slot(unsigned id, unsigned mask) {
-    return (id * 2654435761u >> 7) & mask;
-}
-__device__ __forceinline__ bool seen_or_insert(unsigned* hash, unsigned mask, unsigned id) {
-    const unsigned h = seen_slot(id, mask);
+// Per-query "seen" table: H = 2^hbits 16-bit slots, open addressing with a
+// linear probe window of 8.  The home slot is the id's low hbits (ids are a
+// random permutation's worth of indices, so the low bits spread well); a slot
+// stores (id >> hbits) << 3 | probe offset, which reconstructs the id exactly,
+// so nothing is ever reported seen falsely.  A full window overwrites the home
+// slot (lossy): a lost id only costs a re-evaluation.  Needs
+// (n-1) >> hbits < 8191 (choose_hash enforces it).  16-bit slots halve the
+// table and double the warps per SM of the search kernels.
+constexpr unsigned short kSeenEmpty = 0xffffu;
+
+__device__ __forceinline__ bool seen_or_insert(unsigned short* hash, unsigned mask, int hbits, unsigned id) {
+    const unsigned home = id & mask;
+    const unsigned tag = (id >> hbits) << 3;
 #pragma unroll
     for (unsigned i = 0; i < 8; ++i) {
-        const unsigned s = (h + i) & mask;
+        const unsigned s = (home + i) & mask;
         const unsigned v = hash[s];
-        if (v == id) return true;
-        if (v == 0xffffffffu) {
-            hash[s] = id;
+        if (v == (tag | i)) return true;
+        if (v == kSeenEmpty) {
+            hash[s] = (unsigned short)(tag | i);
             return false;
         }
     }
-    hash[h] = id;
+    hash[home] = (unsigned short)tag;
     return false;
 }
 

@@ -412,11 +412,17 @@ int grid_for(long long work, int block) {
 }
 
 // ---- launch helpers --------------------------------------------------------------------------
-int choose_hash(int L, int hash_bits) {
-    if (hash_bits > 0) return 1 << hash_bits;
-    int h = next_pow2(16 * L);
-    if (h < 512) h = 512;
-    if (h > 8192) h = 8192;
+int choose_hash(int L, int hash_bits, long long n) {
+    int h;
+    if (hash_bits > 0) {
+        h = 1 << hash_bits;
+    } else {
+        h = next_pow2(16 * L);
+        if (h < 512) h = 512;
+        if (h > 8192) h = 8192;
+    }
+    // 16-bit slots hold (id >> log2 h) << 3: keep the quotient below 8191
+    while (((n - 1) >> (__builtin_ctz((unsigned)h))) >= 8191) h <<= 1;
     return h;
 }
 
@@ -561,7 +567,7 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
     // by the key-equality check when already in the beam): cheaper than a
     // dependent bitmap load on every neighbour.
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, nullptr, x8, (int)dw};
-    int H = choose_hash((int)L, hash_bits);
+    int H = choose_hash((int)L, hash_bits, n);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);
     long long* oc = reinterpret_cast<long long*>(out_counts);
@@ -613,7 +619,7 @@ extern "C" int pk_beam_search_single(const float* x, int64_t n, int64_t dp, cons
         return 2;
     }
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, nullptr};
-    int H = choose_hash((int)L, 0);
+    int H = choose_hash((int)L, 0, n);
     size_t bytes = align16(beam_smem_bytes((int)L, H));
     unsigned* vi = nullptr;
     double* vd = nullptr;
