@@ -247,6 +247,7 @@ def main_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     total_ms = 0.0
+    step_ms = []
     stage = {"index": 0.0, "density": 0.0, "dependent": 0.0, "unionfind": 0.0}
     rounds = []
     last = None
@@ -263,7 +264,8 @@ def main_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        total_ms += e0.elapsed_time(e1)
+        step_ms.append(e0.elapsed_time(e1))
+        total_ms += step_ms[-1]
         for kk_, v in last["timings"].items():
             stage[kk_] += v
         rounds = trace
@@ -360,6 +362,7 @@ def main_ours(args):
             "gpu_launches_per_step": launches / args.steps,
             "clocks": clk,
             "stage_ms": {k_: v / args.steps * 1e3 for k_, v in stage.items()},
+            "step_ms": [round(v, 3) for v in step_ms],
             "dependent_rounds": rounds,
             "kernels_ms_per_step": {k_: round(v[1] / args.steps, 4) for k_, v in sorted(prof.items(),
                                                                                       key=lambda kv: -kv[1][1])},

@@ -152,13 +152,34 @@ int pk_rank_order(const double* rho, int64_t n, int64_t* rank, int* nan_flag, vo
  * dependent.py:112). */
 int pk_resolve_lists(const int64_t* rank, const int64_t* qids, int64_t m, const int64_t* ids,
                      const double* dists, int64_t k, int64_t* lam, double* delta, int64_t* unresolved,
-                     int64_t* n_unresolved, int64_t skip, void* stream);
+                     int64_t* n_unresolved, int64_t skip, const int64_t* counts, int64_t* short_out,
+                     int64_t* n_short, void* stream);
+/* (counts, short_out, n_short may be null; with counts, rows whose beam
+ * search found fewer than k entries are not resolved from their partial
+ * list but appended to short_out for pk_resolve_short.) */
 
 /* Closest strictly denser point over all n for each query.  Replaces
  * _kernels.dp_scan_all (_kernels.py:442-462).  out_id (m,) int64,
  * out_sqd (m,) float64. */
-int pk_dp_scan(const float* x, int64_t n, int64_t dp, const int64_t* rank, const int64_t* qids, int64_t m,
-               int64_t* out_id, double* out_sqd, void* stream);
+int pk_dp_scan(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+               const int64_t* rank, const int64_t* qids, int64_t m, int64_t* out_id, double* out_sqd,
+               void* stream);
+
+/* out_count[t] = #{ j != qids[t] : (d(qids[t], j), j) < (key_d[t], key_i[t]) },
+ * i.e. the position the key would take in the query's exact kNN row. */
+int pk_count_below(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                   const int64_t* qids, int64_t m, const double* key_d, const int64_t* key_i,
+                   int64_t* out_count, void* stream);
+
+/* Doubling-round rows whose beam search came up short.  The reference
+ * replaces them with exact kNN rows of width kk (vamana.py:220-225) and takes
+ * the first strictly denser entry (dependent.py:80-93); that entry is the
+ * nearest denser point p* iff fewer than kk keys precede p*'s key.  So: one
+ * dp scan + one count scan, no row.  Resolved rows fill lam/delta, the others
+ * are appended (input order) to unresolved, count in *n_unresolved. */
+int pk_resolve_short(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                     const int64_t* rank, const int64_t* qids, int64_t m, int64_t kk, int64_t* lam,
+                     double* delta, int64_t* unresolved, int64_t* n_unresolved, void* stream);
 
 /* Scatter: lam[qids[i]] = src_id[i], delta[qids[i]] = sqrt(src_sqd[i])
  * (dependent.py:125-127). */

@@ -125,9 +125,18 @@ __global__ void rank_scatter_kernel(const long long* order, long long n, long lo
 // first denser entry per row; unresolved flagged (dependent.py:80-93)
 __global__ void resolve_kernel(const long long* rank, const long long* qids, long long m, const long long* ids,
                                const double* dists, int k, long long* lam, double* delta, unsigned char* unres,
-                               long long skip) {
+                               long long skip, const long long* counts, unsigned char* shortf) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < m; t += (long long)gridDim.x * blockDim.x) {
         long long q = qids[t];
+        if (counts) {
+            // a row the beam search could not fill: resolved by pk_resolve_short
+            const bool sh = counts[t] < k;
+            shortf[t] = sh;
+            if (sh) {
+                unres[t] = 0;
+                continue;
+            }
+        }
         long long rq = rank[q];
         int hit = -1;
         for (int j = 0; j < k; ++j) {
@@ -379,32 +388,43 @@ extern "C" int pk_rank_order(const double* rho, int64_t n, int64_t* rank, int* n
 
 extern "C" int pk_resolve_lists(const int64_t* rank, const int64_t* qids, int64_t m, const int64_t* ids,
                                 const double* dists, int64_t k, int64_t* lam, double* delta, int64_t* unresolved,
-                                int64_t* n_unresolved, int64_t skip, void* stream) {
+                                int64_t* n_unresolved, int64_t skip, const int64_t* counts, int64_t* short_out,
+                                int64_t* n_short, void* stream) {
     cudaStream_t st = as_stream(stream);
     if (m <= 0) {
         PK_CHECK(cudaMemsetAsync(n_unresolved, 0, sizeof(int64_t), st));
+        if (n_short) PK_CHECK(cudaMemsetAsync(n_short, 0, sizeof(int64_t), st));
         return 0;
     }
+    if (counts && (!short_out || !n_short)) {
+        set_error("pk_resolve_lists: counts given without a short-row output");
+        return 2;
+    }
     unsigned char* fl = nullptr;
-    long long* pos = nullptr;
+    unsigned char* sf = nullptr;
     PK_CHECK(scratch(&fl, (size_t)m, st));
-    PK_CHECK(scratch(&pos, (size_t)m, st));
+    if (counts) PK_CHECK(scratch(&sf, (size_t)m, st));
     if (k == 0) {
         PK_CHECK(cudaMemsetAsync(fl, 1, (size_t)m, st));
+        if (sf) PK_CHECK(cudaMemsetAsync(sf, 0, (size_t)m, st));
     } else {
         {
             ProfScope _ps("resolve_kernel", st);
             resolve_kernel<<<grid_for(m, 256), 256, 0, st>>>(
                 reinterpret_cast<const long long*>(rank), reinterpret_cast<const long long*>(qids), m,
-                reinterpret_cast<const long long*>(ids), dists, (int)k, reinterpret_cast<long long*>(lam), delta, fl, skip);
+                reinterpret_cast<const long long*>(ids), dists, (int)k, reinterpret_cast<long long*>(lam), delta, fl, skip,
+                reinterpret_cast<const long long*>(counts), sf);
         }
         PK_CHECK_LAUNCH("resolve_kernel");
     }
-    // unresolved qids, input order preserved
+    // unresolved (and short) qids, input order preserved
     int rc = compact_flagged(reinterpret_cast<const long long*>(qids), fl, m, reinterpret_cast<long long*>(unresolved),
                              reinterpret_cast<long long*>(n_unresolved), st);
+    if (!rc && sf)
+        rc = compact_flagged(reinterpret_cast<const long long*>(qids), sf, m, reinterpret_cast<long long*>(short_out),
+                             reinterpret_cast<long long*>(n_short), st);
     release(fl, st);
-    release(pos, st);
+    if (sf) release(sf, st);
     return rc;
 }
 

@@ -226,104 +226,6 @@ __global__ void __launch_bounds__(BT) brute_rows_kernel(const float* __restrict_
     }
 }
 
-// ---- dependent-point scan (_kernels.py:442-462) ------------------------------------------
-constexpr int DQ = 8;     // queries per block
-constexpr int DPT = 4;    // points per thread
-
-__global__ void __launch_bounds__(BT) dp_scan_kernel(const float* __restrict__ X, int n, int dp,
-                                                     const long long* __restrict__ rank,
-                                                     const long long* __restrict__ qids, int m,
-                                                     double* part_d, int* part_i) {
-    extern __shared__ __align__(16) float qs[];  // DQ * dp
-    __shared__ long long qr[DQ];
-    const int q0 = blockIdx.x * DQ;
-    const int nq = min(DQ, m - q0);
-    for (int x = threadIdx.x; x < DQ * dp; x += BT) {
-        int qq = x / dp, t = x % dp;
-        qs[x] = qq < nq ? X[(size_t)qids[q0 + qq] * dp + t] : 0.f;
-    }
-    if (threadIdx.x < DQ) qr[threadIdx.x] = threadIdx.x < nq ? rank[qids[q0 + threadIdx.x]] : 0x7fffffffffffffffLL;
-    __syncthreads();
-    long long rmin = qr[0];
-    for (int qq = 1; qq < DQ; ++qq) rmin = min(rmin, qr[qq]);
-    double best[DQ];
-    int bid[DQ];
-#pragma unroll
-    for (int qq = 0; qq < DQ; ++qq) {
-        best[qq] = __longlong_as_double(0x7ff0000000000000LL);
-        bid[qq] = -1;
-    }
-    const int chunk = BT * DPT;
-    const int j0 = blockIdx.y * chunk;
-    for (int jj = threadIdx.x; jj < chunk; jj += BT) {
-        int j = j0 + jj;
-        if (j >= n) break;
-        long long rj = __ldg(rank + j);
-        if (rj <= rmin) continue;
-        const float* r = X + (size_t)j * dp;
-        double acc[DQ];
-#pragma unroll
-        for (int qq = 0; qq < DQ; ++qq) acc[qq] = 0.0;
-        for (int t = 0; t < dp; t += 4) {
-            float4 x = ldg4(r + t);
-#pragma unroll
-            for (int qq = 0; qq < DQ; ++qq) {
-                const float* qv = qs + qq * dp + t;
-                double a = (double)qv[0] - (double)x.x; acc[qq] = __dadd_rn(acc[qq], __dmul_rn(a, a));
-                double b = (double)qv[1] - (double)x.y; acc[qq] = __dadd_rn(acc[qq], __dmul_rn(b, b));
-                double c = (double)qv[2] - (double)x.z; acc[qq] = __dadd_rn(acc[qq], __dmul_rn(c, c));
-                double e = (double)qv[3] - (double)x.w; acc[qq] = __dadd_rn(acc[qq], __dmul_rn(e, e));
-            }
-        }
-#pragma unroll
-        for (int qq = 0; qq < DQ; ++qq)
-            if (rj > qr[qq] && key_lt(acc[qq], (unsigned)j, best[qq], (unsigned)bid[qq])) {
-                best[qq] = acc[qq];
-                bid[qq] = j;
-            }
-    }
-    // block argmin per query
-    __shared__ double rd[BT / 32][DQ];
-    __shared__ int ri[BT / 32][DQ];
-    const int lane = lane_id(), w = threadIdx.x >> 5;
-#pragma unroll
-    for (int qq = 0; qq < DQ; ++qq) {
-        double d = best[qq];
-        unsigned i = (unsigned)bid[qq];
-        for (int s = 16; s; s >>= 1) {
-            double od = __shfl_xor_sync(PK_FULL, d, s);
-            unsigned oi = __shfl_xor_sync(PK_FULL, i, s);
-            if (key_lt(od, oi, d, i)) { d = od; i = oi; }
-        }
-        if (lane == 0) { rd[w][qq] = d; ri[w][qq] = (int)i; }
-    }
-    __syncthreads();
-    if (threadIdx.x < nq) {
-        int qq = threadIdx.x;
-        double d = rd[0][qq];
-        unsigned i = (unsigned)ri[0][qq];
-        for (int ww = 1; ww < BT / 32; ++ww)
-            if (key_lt(rd[ww][qq], (unsigned)ri[ww][qq], d, i)) { d = rd[ww][qq]; i = (unsigned)ri[ww][qq]; }
-        part_d[(size_t)(q0 + qq) * gridDim.y + blockIdx.y] = d;
-        part_i[(size_t)(q0 + qq) * gridDim.y + blockIdx.y] = (int)i;
-    }
-}
-
-__global__ void dp_scan_reduce_kernel(const double* part_d, const int* part_i, int m, int nchunk,
-                                      long long* out_id, double* out_d) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= m) return;
-    double d = __longlong_as_double(0x7ff0000000000000LL);
-    unsigned i = 0xffffffffu;
-    for (int c = 0; c < nchunk; ++c) {
-        double od = part_d[(size_t)t * nchunk + c];
-        unsigned oi = (unsigned)part_i[(size_t)t * nchunk + c];
-        if (key_lt(od, oi, d, i)) { d = od; i = oi; }
-    }
-    out_id[t] = i == 0xffffffffu ? -1 : (long long)i;
-    out_d[t] = d;
-}
-
 // ---- misc small kernels ----------------------------------------------------------------------
 __global__ void fill_ids_kernel(long long* ids, double* d, long long count) {
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < count; x += (long long)gridDim.x * blockDim.x) {
@@ -669,35 +571,6 @@ extern "C" int pk_brute_knn_vector(const float* x, int64_t n, int64_t dp, const 
     if (kk <= 0) return 0;
     return run_brute(x, (int)n, (int)dp, nullptr, qvec, nullptr, nullptr, 1, (int)kk,
                      reinterpret_cast<long long*>(out_ids), out_sqd, st);
-}
-
-extern "C" int pk_dp_scan(const float* x, int64_t n, int64_t dp, const int64_t* rank, const int64_t* qids, int64_t m,
-                          int64_t* out_id, double* out_sqd, void* stream) {
-    cudaStream_t st = as_stream(stream);
-    if (m <= 0) return 0;
-    int nchunk = (int)((n + BT * DPT - 1) / (BT * DPT));
-    dim3 grid((unsigned)((m + DQ - 1) / DQ), (unsigned)nchunk);
-    double* pd = nullptr;
-    int* pi = nullptr;
-    PK_CHECK(scratch(&pd, (size_t)m * nchunk, st));
-    PK_CHECK(scratch(&pi, (size_t)m * nchunk, st));
-    size_t sm = (size_t)DQ * dp * sizeof(float);
-    if (sm > 48 * 1024) PK_CHECK(cudaFuncSetAttribute(dp_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    {
-        ProfScope _ps("dp_scan_kernel", st);
-        dp_scan_kernel<<<grid, BT, sm, st>>>(x, (int)n, (int)dp, reinterpret_cast<const long long*>(rank),
-                                             reinterpret_cast<const long long*>(qids), (int)m, pd, pi);
-    }
-    PK_CHECK_LAUNCH("dp_scan_kernel");
-    {
-        ProfScope _ps("dp_scan_reduce_kernel", st);
-        dp_scan_reduce_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(pd, pi, (int)m, nchunk,
-                                                                         reinterpret_cast<long long*>(out_id), out_sqd);
-    }
-    PK_CHECK_LAUNCH("dp_scan_reduce_kernel");
-    release(pd, st);
-    release(pi, st);
-    return 0;
 }
 
 extern "C" int pk_sqrt(const double* sqd, int64_t count, double* out, void* stream) {

@@ -1,0 +1,336 @@
+// Exact full scans over all n points for a batch of member queries:
+//   * nearest strictly denser point (dp_scan_all, _kernels.py:442-462);
+//   * number of points whose (distance, id) key is below a given key -- used
+//     to decide whether a query's exact kNN row of width kk would contain its
+//     nearest denser point, without building the row (doubling rounds whose
+//     beam search came up short, vamana.py:220-225 + dependent.py:80-93).
+// Each block holds QT queries in shared memory and streams a chunk of points
+// once for all of them; distances are exact in the point set's policy (float64
+// in coordinate order, or integer dp4a on u8-packed rows).
+#include <algorithm>
+
+#include "../../include/peakann_b200.h"
+#include "api.cuh"
+#include "common.cuh"
+
+namespace pk {
+
+int grid_for(long long work, int block);
+
+constexpr int kScanThreads = 256;
+constexpr int kScanQ = 16;    // queries per block
+constexpr int kScanPPT = 4;   // points per thread per block
+
+struct ScanArgs {
+    DataRef D;
+    int n;
+    const long long* rank;     // (n,), SCAN_DENSER
+    const long long* qids;     // (m,)
+    int m;
+    const double* key_d;       // (m,) threshold distances, SCAN_COUNT
+    const long long* key_i;    // (m,) threshold ids, SCAN_COUNT
+    double* part_d;            // (m, nchunk) partial minima, SCAN_DENSER
+    int* part_i;
+    long long* count;          // (m,) SCAN_COUNT
+};
+
+enum { SCAN_DENSER = 0, SCAN_COUNT = 1 };
+
+// distances from one point row to the QT staged queries
+template <int MODE>
+struct QueryTile;
+
+template <>
+struct QueryTile<MODE_SEQ64> {
+    const float* q;  // smem, QT x dp floats
+    int dp;
+    __device__ __forceinline__ void dist(const DataRef& D, int j, double* acc) const {
+        const float* r = D.X + (size_t)j * dp;
+#pragma unroll
+        for (int a = 0; a < kScanQ; ++a) acc[a] = 0.0;
+        for (int t = 0; t < dp; t += 4) {
+            const float4 x = ldg4(r + t);
+#pragma unroll
+            for (int a = 0; a < kScanQ; ++a) {
+                const float* qa = q + a * dp + t;
+                double e0 = (double)qa[0] - (double)x.x; acc[a] = __dadd_rn(acc[a], __dmul_rn(e0, e0));
+                double e1 = (double)qa[1] - (double)x.y; acc[a] = __dadd_rn(acc[a], __dmul_rn(e1, e1));
+                double e2 = (double)qa[2] - (double)x.z; acc[a] = __dadd_rn(acc[a], __dmul_rn(e2, e2));
+                double e3 = (double)qa[3] - (double)x.w; acc[a] = __dadd_rn(acc[a], __dmul_rn(e3, e3));
+            }
+        }
+    }
+};
+
+template <>
+struct QueryTile<MODE_EXACT_U8> {
+    const unsigned* q;  // smem, QT x dw words
+    int dw;
+    __device__ __forceinline__ void dist(const DataRef& D, int j, double* acc) const {
+        const unsigned* r = D.X8 + (size_t)j * dw;
+        unsigned s[kScanQ];
+#pragma unroll
+        for (int a = 0; a < kScanQ; ++a) s[a] = 0u;
+        for (int w = 0; w < dw; ++w) {
+            const unsigned x = __ldg(r + w);
+#pragma unroll
+            for (int a = 0; a < kScanQ; ++a) {
+                const unsigned v = __vabsdiffu4(q[a * dw + w], x);
+                s[a] = __dp4a(v, v, s[a]);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < kScanQ; ++a) acc[a] = (double)s[a];
+    }
+};
+
+template <int MODE, int OP>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ long long qr[kScanQ];
+    __shared__ long long qid[kScanQ];
+    __shared__ double kdd[kScanQ];
+    __shared__ long long kdi[kScanQ];
+    const int q0 = blockIdx.x * kScanQ;
+    const int nq = min(kScanQ, A.m - q0);
+    const int width = MODE == MODE_EXACT_U8 ? A.D.dw : A.D.dp;
+    for (int x = threadIdx.x; x < kScanQ * width; x += kScanThreads) {
+        const int a = x / width, t = x % width;
+        const long long qi = a < nq ? A.qids[q0 + a] : 0;
+        if (MODE == MODE_EXACT_U8)
+            reinterpret_cast<unsigned*>(smem)[x] = a < nq ? A.D.X8[(size_t)qi * width + t] : 0u;
+        else
+            reinterpret_cast<float*>(smem)[x] = a < nq ? A.D.X[(size_t)qi * width + t] : 0.f;
+    }
+    if (threadIdx.x < kScanQ) {
+        const int a = threadIdx.x;
+        qid[a] = a < nq ? A.qids[q0 + a] : -1;
+        if (OP == SCAN_DENSER) qr[a] = a < nq ? A.rank[A.qids[q0 + a]] : 0x7fffffffffffffffLL;
+        if (OP == SCAN_COUNT) {
+            kdd[a] = a < nq ? A.key_d[q0 + a] : -1.0;
+            kdi[a] = a < nq ? A.key_i[q0 + a] : -1;
+        }
+    }
+    __syncthreads();
+    QueryTile<MODE> tile;
+    if constexpr (MODE == MODE_EXACT_U8) {
+        tile.q = reinterpret_cast<const unsigned*>(smem);
+        tile.dw = A.D.dw;
+    } else {
+        tile.q = reinterpret_cast<const float*>(smem);
+        tile.dp = A.D.dp;
+    }
+    long long rmin = 0x7fffffffffffffffLL;
+    if (OP == SCAN_DENSER)
+        for (int a = 0; a < kScanQ; ++a) rmin = min(rmin, qr[a]);
+    double best[kScanQ];
+    int bid[kScanQ];
+    int cnt[kScanQ];
+#pragma unroll
+    for (int a = 0; a < kScanQ; ++a) {
+        best[a] = __longlong_as_double(0x7ff0000000000000LL);
+        bid[a] = -1;
+        cnt[a] = 0;
+    }
+    const int chunk = kScanThreads * kScanPPT;
+    const int j0 = blockIdx.y * chunk;
+    for (int jj = threadIdx.x; jj < chunk; jj += kScanThreads) {
+        const int j = j0 + jj;
+        if (j >= A.n) break;
+        long long rj = 0;
+        if (OP == SCAN_DENSER) {
+            rj = __ldg(A.rank + j);
+            if (rj <= rmin) continue;
+        }
+        double acc[kScanQ];
+        tile.dist(A.D, j, acc);
+#pragma unroll
+        for (int a = 0; a < kScanQ; ++a) {
+            if (OP == SCAN_DENSER) {
+                if (rj > qr[a] && key_lt(acc[a], (unsigned)j, best[a], (unsigned)bid[a])) {
+                    best[a] = acc[a];
+                    bid[a] = j;
+                }
+            } else {
+                if ((long long)j != qid[a] && key_lt(acc[a], (unsigned)j, kdd[a], (unsigned)kdi[a])) ++cnt[a];
+            }
+        }
+    }
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    if (OP == SCAN_COUNT) {
+#pragma unroll
+        for (int a = 0; a < kScanQ; ++a) {
+            int c = cnt[a];
+            for (int s = 16; s; s >>= 1) c += __shfl_xor_sync(PK_FULL, c, s);
+            if (lane == 0 && c && a < nq) atomicAdd(reinterpret_cast<unsigned long long*>(A.count + q0 + a),
+                                                    (unsigned long long)c);
+        }
+        return;
+    }
+    __shared__ double rd[kScanThreads / 32][kScanQ];
+    __shared__ int ri[kScanThreads / 32][kScanQ];
+#pragma unroll
+    for (int a = 0; a < kScanQ; ++a) {
+        double d = best[a];
+        unsigned i = (unsigned)bid[a];
+        for (int s = 16; s; s >>= 1) {
+            double od = __shfl_xor_sync(PK_FULL, d, s);
+            unsigned oi = __shfl_xor_sync(PK_FULL, i, s);
+            if (key_lt(od, oi, d, i)) { d = od; i = oi; }
+        }
+        if (lane == 0) { rd[w][a] = d; ri[w][a] = (int)i; }
+    }
+    __syncthreads();
+    if (threadIdx.x < nq) {
+        const int a = threadIdx.x;
+        double d = rd[0][a];
+        unsigned i = (unsigned)ri[0][a];
+        for (int ww = 1; ww < kScanThreads / 32; ++ww)
+            if (key_lt(rd[ww][a], (unsigned)ri[ww][a], d, i)) { d = rd[ww][a]; i = (unsigned)ri[ww][a]; }
+        A.part_d[(size_t)(q0 + a) * gridDim.y + blockIdx.y] = d;
+        A.part_i[(size_t)(q0 + a) * gridDim.y + blockIdx.y] = (int)i;
+    }
+}
+
+__global__ void scan_reduce_kernel(const double* part_d, const int* part_i, int m, int nchunk, long long* out_id,
+                                   double* out_d) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    double d = __longlong_as_double(0x7ff0000000000000LL);
+    unsigned i = 0xffffffffu;
+    for (int c = 0; c < nchunk; ++c) {
+        const double od = part_d[(size_t)t * nchunk + c];
+        const unsigned oi = (unsigned)part_i[(size_t)t * nchunk + c];
+        if (key_lt(od, oi, d, i)) { d = od; i = oi; }
+    }
+    out_id[t] = i == 0xffffffffu ? -1 : (long long)i;
+    out_d[t] = d;
+}
+
+// rows resolved by the full scan: lam/delta scattered, the rest kept
+__global__ void short_resolve_kernel(const long long* qids, int m, const long long* sid, const double* ssq,
+                                     const long long* cnt, long long kk, long long* lam, double* delta,
+                                     unsigned char* unres) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const bool ok = sid[t] >= 0 && cnt[t] < kk;
+    if (ok) {
+        lam[qids[t]] = sid[t];
+        delta[qids[t]] = sqrt(ssq[t]);
+    }
+    unres[t] = !ok;
+}
+
+template <int MODE, int OP>
+int launch_scan(ScanArgs A, cudaStream_t st, int* nchunk_out) {
+    const int nchunk = (A.n + kScanThreads * kScanPPT - 1) / (kScanThreads * kScanPPT);
+    const int width = MODE == MODE_EXACT_U8 ? A.D.dw : A.D.dp;
+    const size_t sm = (size_t)kScanQ * width * 4;
+    auto kern = scan_kernel<MODE, OP>;
+    if (sm > 48 * 1024) PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dim3 grid((unsigned)((A.m + kScanQ - 1) / kScanQ), (unsigned)nchunk);
+    {
+        ProfScope _ps(OP == SCAN_DENSER ? "scan_denser_kernel" : "scan_count_kernel", st);
+        kern<<<grid, kScanThreads, sm, st>>>(A);
+    }
+    PK_CHECK_LAUNCH("scan_kernel");
+    *nchunk_out = nchunk;
+    return 0;
+}
+
+template <int OP>
+int dispatch_scan(int mode, ScanArgs A, cudaStream_t st, int* nchunk) {
+    // EXACT32 data is integer-valued: the float64 path computes the same values
+    if (mode == MODE_EXACT_U8) return launch_scan<MODE_EXACT_U8, OP>(A, st, nchunk);
+    return launch_scan<MODE_SEQ64, OP>(A, st, nchunk);
+}
+
+extern int compact_flagged(const long long* in, const unsigned char* flags, long long n, long long* out,
+                           long long* count, cudaStream_t st);
+
+}  // namespace pk
+
+using namespace pk;
+
+extern "C" int pk_dp_scan(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                          const int64_t* rank, const int64_t* qids, int64_t m, int64_t* out_id, double* out_sqd,
+                          void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (m <= 0) return 0;
+    if (mode == MODE_EXACT_U8 && !x8) {
+        set_error("u8 mode needs the packed rows");
+        return 2;
+    }
+    ScanArgs A{};
+    A.D = DataRef{x, (int)dp, x8, (int)dw};
+    A.n = (int)n;
+    A.rank = reinterpret_cast<const long long*>(rank);
+    A.qids = reinterpret_cast<const long long*>(qids);
+    A.m = (int)m;
+    const int nchunk = (int)((n + kScanThreads * kScanPPT - 1) / (kScanThreads * kScanPPT));
+    PK_CHECK(scratch(&A.part_d, (size_t)m * nchunk, st));
+    PK_CHECK(scratch(&A.part_i, (size_t)m * nchunk, st));
+    int nc = 0;
+    int rc = dispatch_scan<SCAN_DENSER>(mode, A, st, &nc);
+    if (rc) return rc;
+    {
+        ProfScope _ps("scan_reduce_kernel", st);
+        scan_reduce_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(A.part_d, A.part_i, (int)m, nc,
+                                                                      reinterpret_cast<long long*>(out_id), out_sqd);
+    }
+    PK_CHECK_LAUNCH("scan_reduce_kernel");
+    release(A.part_d, st);
+    release(A.part_i, st);
+    return 0;
+}
+
+extern "C" int pk_count_below(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                              const int64_t* qids, int64_t m, const double* key_d, const int64_t* key_i,
+                              int64_t* out_count, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (m <= 0) return 0;
+    ScanArgs A{};
+    A.D = DataRef{x, (int)dp, x8, (int)dw};
+    A.n = (int)n;
+    A.qids = reinterpret_cast<const long long*>(qids);
+    A.m = (int)m;
+    A.key_d = key_d;
+    A.key_i = reinterpret_cast<const long long*>(key_i);
+    A.count = reinterpret_cast<long long*>(out_count);
+    PK_CHECK(cudaMemsetAsync(out_count, 0, sizeof(int64_t) * (size_t)m, st));
+    int nc = 0;
+    return dispatch_scan<SCAN_COUNT>(mode, A, st, &nc);
+}
+
+extern "C" int pk_resolve_short(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                                const int64_t* rank, const int64_t* qids, int64_t m, int64_t kk, int64_t* lam,
+                                double* delta, int64_t* unresolved, int64_t* n_unresolved, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (m <= 0) {
+        PK_CHECK(cudaMemsetAsync(n_unresolved, 0, sizeof(int64_t), st));
+        return 0;
+    }
+    long long *sid = nullptr, *cnt = nullptr;
+    double* ssq = nullptr;
+    unsigned char* fl = nullptr;
+    PK_CHECK(scratch(&sid, (size_t)m, st));
+    PK_CHECK(scratch(&ssq, (size_t)m, st));
+    PK_CHECK(scratch(&cnt, (size_t)m, st));
+    PK_CHECK(scratch(&fl, (size_t)m, st));
+    int rc = pk_dp_scan(x, n, dp, x8, dw, mode, rank, qids, m, reinterpret_cast<int64_t*>(sid), ssq, stream);
+    if (rc) return rc;
+    rc = pk_count_below(x, n, dp, x8, dw, mode, qids, m, ssq, reinterpret_cast<int64_t*>(sid),
+                        reinterpret_cast<int64_t*>(cnt), stream);
+    if (rc) return rc;
+    {
+        ProfScope _ps("short_resolve_kernel", st);
+        short_resolve_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(
+            reinterpret_cast<const long long*>(qids), (int)m, sid, ssq, cnt, kk, reinterpret_cast<long long*>(lam),
+            delta, fl);
+    }
+    PK_CHECK_LAUNCH("short_resolve_kernel");
+    rc = compact_flagged(reinterpret_cast<const long long*>(qids), fl, m, reinterpret_cast<long long*>(unresolved),
+                         reinterpret_cast<long long*>(n_unresolved), st);
+    for (void* p : {(void*)sid, (void*)ssq, (void*)cnt, (void*)fl}) release(p, st);
+    return rc;
+}

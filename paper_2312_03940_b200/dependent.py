@@ -121,16 +121,33 @@ def dp_brute_force(i: int, candidates: Sequence[Neighbor], rho: np.ndarray) -> O
     return best
 
 
-def _resolve(rank_t, qids_t, ids_t, dists_t, lam_t, delta_t, skip: int):
-    """pk_resolve_lists -> (unresolved qids tensor, count)."""
+def _resolve(rank_t, qids_t, ids_t, dists_t, lam_t, delta_t, skip: int, counts_t=None):
+    """pk_resolve_lists -> (unresolved qids, count, short qids, short count).
+    With counts_t, rows the beam search could not fill are returned as
+    "short" instead of being resolved from their partial list."""
     import torch
 
     m = qids_t.shape[0]
-    out = torch.empty(max(m, 1), dtype=torch.int64, device=qids_t.device)
-    cnt = torch.zeros(1, dtype=torch.int64, device=qids_t.device)
+    dev = qids_t.device
+    out = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    short = torch.empty(max(m, 1), dtype=torch.int64, device=dev) if counts_t is not None else None
     k = ids_t.shape[1] if ids_t.dim() == 2 else 0
-    _lib.call("pk_resolve_lists", rank_t, qids_t, m, ids_t, dists_t, k, lam_t, delta_t, out, cnt, skip,
-              _lib.stream())
+    _lib.call("pk_resolve_lists", rank_t, qids_t, m, ids_t, dists_t, k, lam_t, delta_t, out, cnt[0:1], skip,
+              counts_t, short, cnt[1:2] if counts_t is not None else None, _lib.stream())
+    c, s = (int(v) for v in _lib.to_host(cnt))
+    return out[:c], c, (short[:s] if short is not None else None), s
+
+
+def _resolve_short(p: PointSet, rank_t, short_t, ms: int, kk: int, lam_t, delta_t):
+    """Rows whose beam search came up short: exact resolution by a dp scan +
+    count scan (pk_resolve_short) instead of full exact kNN rows."""
+    import torch
+
+    out = torch.empty(max(ms, 1), dtype=torch.int64, device=short_t.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=short_t.device)
+    _lib.call("pk_resolve_short", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, rank_t, short_t, ms, kk, lam_t,
+              delta_t, out, cnt, _lib.stream())
     c = int(cnt.item())
     return out[:c], c
 
@@ -148,16 +165,26 @@ def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: D
     _lib.call("pk_argmax_rank", rank_t, n, top_t, _lib.stream())
     top = int(top_t.item())
     all_t = torch.arange(n, dtype=torch.int64, device=dev)
-    todo, m = _resolve(rank_t, all_t, ids_t, dists_t, lam_t, delta_t, top)
+    todo, m, _, _ = _resolve(rank_t, all_t, ids_t, dists_t, lam_t, delta_t, top)
     if n > 1:
         kdep = params.validated_against(ids_t.shape[1]).initial_k
         if not isinstance(g, BruteForceIndex):
+            raw = getattr(g, "knn_rows_raw", None)
             while m > params.threshold:
                 kq = min(kdep, n - 1)
                 if trace is not None:
                     trace.append((m, kq))
-                r_ids, r_sqd = g.knn_batch_device(todo, kq)
-                todo, m = _resolve(rank_t, todo, r_ids, sqrt_device(r_sqd), lam_t, delta_t, -1)
+                if raw is not None:
+                    r_ids, r_sqd, r_cnt = raw(todo, kq)
+                    todo, m, short, ms = _resolve(rank_t, todo, r_ids, sqrt_device(r_sqd), lam_t, delta_t, -1, r_cnt)
+                    if ms:
+                        left, ml = _resolve_short(p, rank_t, short, ms, min(kq, n - 1), lam_t, delta_t)
+                        if ml:
+                            todo = torch.cat([todo, left])
+                            m += ml
+                else:
+                    r_ids, r_sqd = g.knn_batch_device(todo, kq)
+                    todo, m, _, _ = _resolve(rank_t, todo, r_ids, sqrt_device(r_sqd), lam_t, delta_t, -1)
                 if kq >= n - 1:
                     break
                 kdep *= 2
@@ -166,7 +193,8 @@ def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: D
             trace.append((m, "scan"))
         sid = torch.empty(m, dtype=torch.int64, device=dev)
         ssq = torch.empty(m, dtype=torch.float64, device=dev)
-        _lib.call("pk_dp_scan", p.device(), n, p.dp, rank_t, todo, m, sid, ssq, _lib.stream())
+        _lib.call("pk_dp_scan", p.device(), n, p.dp, p.packed(), p.dw, p.mode, rank_t, todo, m, sid, ssq,
+                  _lib.stream())
         _lib.call("pk_scatter_dependents", todo, m, sid, ssq, lam_t, delta_t, _lib.stream())
     return lam_t, delta_t, rank_t
 

@@ -342,6 +342,11 @@ class VamanaIndex(KnnIndex):
     def knn_batch_device(self, qids_t, k: int, evals=None):
         return beam_knn_device(self.graph, qids_t, k, max(self.query_beam, k), evals)
 
+    def knn_rows_raw(self, qids_t, k: int):
+        """Beam rows without the exact fallback: (ids_t, sqd_t, counts_t);
+        rows with counts < kk are left for the caller (dependent rounds)."""
+        return beam_knn_raw(self.graph, qids_t, max(self.query_beam, k), k, STATS["beam"])
+
     def knn_batch(self, qids: np.ndarray, k: int) -> Neighborhoods:
         if k < 1:
             raise ValueError(f"k must be >= 1, got {k}")
