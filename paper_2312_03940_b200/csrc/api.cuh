@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 
 namespace pk {
@@ -55,10 +56,18 @@ inline size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
 inline size_t cand_smem_bytes(int cap, int dw, int S, bool u8) {
     size_t keys = align16(((((size_t)cap * 15 + 3) & ~(size_t)3) + 128));
     if (!u8) return keys;
-    return align16(keys + (((size_t)dw + 3) & ~(size_t)3) * 4 + (size_t)S * (dw + 1) * 4);
+    return align16(keys + (((size_t)dw + 3) & ~(size_t)3) * 4 + (size_t)S * (dw + 4) * 4 + (size_t)S * 4);
 }
 
 int choose_hash(int L, int hash_bits, long long n);
+
+// integer tuning knob from the environment (default when unset / invalid)
+inline int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    int x = std::atoi(v);
+    return x > 0 ? x : dflt;
+}
 
 // ---- launch accounting -------------------------------------------------------
 // Every kernel launch site opens a ProfScope: launches are always counted per

@@ -246,11 +246,24 @@ struct WarpBeam {
             ++vl;
             cursor = pos + 1;
             __syncwarp();
-            const int nd = __ldg(P.deg + p);
             const int* row = P.adj + (size_t)p * P.R;
+            // the degree and the first 64 row slots are loaded together (slots
+            // past the degree are masked), so the two loads do not serialise
+            int w_a = lane < P.R ? __ldg(row + lane) : -1;
+            int w_b = lane + 32 < P.R ? __ldg(row + lane + 32) : -1;
+            const int nd = __ldg(P.deg + p);
+            {
+                // prefetch the adjacency row of the next unvisited entry: it is
+                // the next expansion unless this one inserts something closer
+                const int pn = next_unvisited();
+                if (pn >= 0 && lane < 2) {
+                    const int* nrow = P.adj + (size_t)(sm.bi[pn] & PK_IDMASK) * P.R + 32 * lane;
+                    if (32 * lane < P.R) asm volatile("prefetch.global.L1 [%0];" ::"l"(nrow));
+                }
+            }
             int c = 0;
             for (int e0 = 0; e0 < nd; e0 += 32) {
-                int w = e0 + lane < nd ? __ldg(row + e0 + lane) : -1;
+                int w = e0 + lane < nd ? (e0 == 0 ? w_a : e0 == 32 ? w_b : __ldg(row + e0 + lane)) : -1;
                 bool cand = w >= 0;
                 if (cand && P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u)) cand = false;
                 if (cand && seen_or_insert(sm.hash, sm.hmask, sm.hbits, (unsigned)w)) cand = false;
@@ -497,6 +510,120 @@ __device__ __forceinline__ void stage_u8_rows(const unsigned* __restrict__ X8, i
     for (; x < S; ++x)
         for (int w = lane; w < dw; w += 32) rows[x * rs + w] = __ldg(X8 + (size_t)ki[x] * dw + w);
     __syncwarp();
+}
+
+// ---- d = 128 fast path (dw == 32 words per u8 row) ------------------------------
+// Squared distances as |a|^2 + |b|^2 - 2 a.b: one __dp4a per word instead of
+// absdiff + dp4a, the query row held in registers, rows read as 128-bit LDS.
+// Staged rows use a 36-word stride (16-byte aligned, conflict-free per
+// quarter warp); nrm[slot] holds each staged row's |x|^2.  All exact integers.
+constexpr int kRs32 = 36;
+
+__device__ __forceinline__ void load_row32(const unsigned* r, uint4 (&q)[8]) {
+    const uint4* v = reinterpret_cast<const uint4*>(r);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = v[i];
+}
+
+__device__ __forceinline__ unsigned dot32(const uint4 (&q)[8], const unsigned* r) {
+    const uint4* v = reinterpret_cast<const uint4*>(r);
+    unsigned a0 = 0u, a1 = 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint4 x = v[i];
+        a0 = __dp4a(q[i].x, x.x, a0);
+        a1 = __dp4a(q[i].y, x.y, a1);
+        a0 = __dp4a(q[i].z, x.z, a0);
+        a1 = __dp4a(q[i].w, x.w, a1);
+    }
+    return a0 + a1;
+}
+
+__device__ __forceinline__ unsigned norm32(const unsigned* r) {
+    uint4 q[8];
+    load_row32(r, q);
+    return dot32(q, r);
+}
+
+// stage rows ki[0..S) (stride kRs32) and their norms
+__device__ __forceinline__ void stage_u8_rows32(const unsigned* __restrict__ X8, const unsigned* ki, int S,
+                                                unsigned* rows, unsigned* nrm) {
+    const int lane = lane_id();
+    // cp.async (LDGSTS): every row of the batch in flight at once, no registers;
+    // lane l copies 16-byte chunk l % 8 of row x + l / 8
+    const int chunk = lane & 7;
+    for (int x = lane >> 3; x < S; x += 4) {
+        const unsigned* src = X8 + (size_t)ki[x] * 32 + chunk * 4;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(rows + (size_t)x * kRs32 + chunk * 4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    for (int r = lane; r < S; r += 32) nrm[r] = norm32(rows + (size_t)r * kRs32);
+    __syncwarp();
+}
+
+// RobustPrune, d = 128 u8 rows: as warp_prune_u8, dot-product form
+static __device__ int warp_prune_u8_32(const unsigned* __restrict__ X8, const double* kd, const unsigned* ki,
+                                       const unsigned short* kp, int c, double alpha2, int R, unsigned char* alive,
+                                       unsigned* cbuf, int* out, const unsigned* rows, const unsigned* nrm, int S,
+                                       long long* evals) {
+    const int lane = lane_id();
+    for (int i = lane; i < c; i += 32) alive[i] = 1;
+    __syncwarp();
+    int sel = 0;
+    int t = 0;
+    while (sel < R) {
+        int nt = -1;
+        for (int base = t; base < c; base += 32) {
+            int i = base + lane;
+            unsigned b = __ballot_sync(PK_FULL, i < c && alive[i]);
+            if (b) { nt = base + __ffs(b) - 1; break; }
+        }
+        if (nt < 0) break;
+        t = nt;
+        if (lane == 0) out[sel] = (int)ki[t];
+        ++sel;
+        if (sel >= R) break;
+        const bool tin = kp[t] < S;
+        const unsigned* rt = tin ? rows + (size_t)kp[t] * kRs32 : X8 + (size_t)ki[t] * 32;
+        uint4 q[8];
+        load_row32(rt, q);
+        const unsigned nt_ = tin ? nrm[kp[t]] : dot32(q, rt);
+        int nq = 0;
+        auto run = [&](int cnt) {
+            __syncwarp();
+            if (lane < cnt) {
+                const int u = (int)cbuf[lane];
+                unsigned du;
+                if (kp[u] < S) {
+                    du = nt_ + nrm[kp[u]] - 2u * dot32(q, rows + (size_t)kp[u] * kRs32);
+                } else {
+                    const unsigned* ru = X8 + (size_t)ki[u] * 32;
+                    du = nt_ + norm32(ru) - 2u * dot32(q, ru);
+                }
+                if (alpha2 * (double)du <= kd[u]) alive[u] = 0;
+            }
+            if (lane == 0) *evals += cnt;
+            __syncwarp();
+        };
+        for (int base = t + 1; base < c; base += 32) {
+            const int u = base + lane;
+            const bool a = u < c && alive[u];
+            const unsigned b = __ballot_sync(PK_FULL, a);
+            const int k = __popc(b);
+            if (nq + k > 32) {
+                run(nq);
+                nq = 0;
+            }
+            if (a) cbuf[nq + warp_excl_prefix(b)] = (unsigned)u;
+            nq += k;
+        }
+        if (nq) run(nq);
+        ++t;
+    }
+    __syncwarp();
+    return sel;
 }
 
 // RobustPrune on u8 rows staged in shared memory (rows >= S come from

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(128) build_search_kernel(BuildArgs A) {
 // Shared-memory view of the candidate buffers of one warp (host size:
 // cand_smem_bytes in api.cuh):
 //   kd[cap] f64 | ki[cap] u32 | kp[cap] u16 | alive[cap] u8 | cbuf[32] u32 |
-//   qrow[dw] u32 | rows[S][dw + 1] u32   (the last two in the u8 mode only)
+//   qrow[dw] u32 | rows[S][dw + 4] u32 | nrm[S] u32   (the last three: u8 mode)
 struct CandSmem {
     double* kd;
     unsigned* ki;
@@ -89,9 +89,10 @@ struct CandSmem {
     unsigned* cbuf;
     unsigned* qrow;
     unsigned* rows;
+    unsigned* nrm;
 };
 
-__device__ __forceinline__ CandSmem carve_cand(unsigned char* base, int cap, int dw) {
+__device__ __forceinline__ CandSmem carve_cand(unsigned char* base, int cap, int dw, int S) {
     CandSmem c;
     c.kd = reinterpret_cast<double*>(base);
     c.ki = reinterpret_cast<unsigned*>(base + (size_t)cap * 8);
@@ -101,22 +102,40 @@ __device__ __forceinline__ CandSmem carve_cand(unsigned char* base, int cap, int
     const size_t q = (((size_t)cap * 15 + 3) & ~(size_t)3) + 128;
     c.qrow = reinterpret_cast<unsigned*>(base + ((q + 15) & ~(size_t)15));
     c.rows = c.qrow + (((size_t)dw + 3) & ~(size_t)3);
+    c.nrm = c.rows + (size_t)S * (dw + 4);
     return c;
 }
 
 // Stage candidate rows ki[0..c) in input order (slot = position) plus the
-// query row, then compute kd[x] = d(query, ki[x]) one lane per candidate from
-// shared memory (u8 mode).  Returns the number of staged rows.
+// query row, then compute kd[x] = d(query, ki[x]) for x >= from, one lane per
+// candidate from shared memory (u8 mode).  Returns the number of staged rows.
 __device__ __forceinline__ int stage_and_measure_u8(const DataRef& D, const CandSmem& C, unsigned q, int c, int S,
                                                     int from, long long* ev) {
     const int lane = lane_id();
-    const int rs = D.dw + 1;
     const int st = min(c, S);
     for (int w = lane; w < D.dw; w += 32) C.qrow[w] = __ldg(D.X8 + (size_t)q * D.dw + w);
-    stage_u8_rows(D.X8, D.dw, C.ki, st, C.rows, rs);
-    for (int x = from + lane; x < c; x += 32) {
-        const unsigned* rx = x < st ? C.rows + (size_t)x * rs : D.X8 + (size_t)C.ki[x] * D.dw;
-        C.kd[x] = (double)u8_row_dist(C.qrow, rx, D.dw);
+    if (D.dw == 32) {
+        stage_u8_rows32(D.X8, C.ki, st, C.rows, C.nrm);
+        uint4 qr[8];
+        load_row32(C.qrow, qr);
+        const unsigned nq = dot32(qr, C.qrow);
+        for (int x = from + lane; x < c; x += 32) {
+            unsigned dx;
+            if (x < st) {
+                dx = nq + C.nrm[x] - 2u * dot32(qr, C.rows + (size_t)x * kRs32);
+            } else {
+                const unsigned* rx = D.X8 + (size_t)C.ki[x] * 32;
+                dx = nq + norm32(rx) - 2u * dot32(qr, rx);
+            }
+            C.kd[x] = (double)dx;
+        }
+    } else {
+        const int rs = D.dw + 1;
+        stage_u8_rows(D.X8, D.dw, C.ki, st, C.rows, rs);
+        for (int x = from + lane; x < c; x += 32) {
+            const unsigned* rx = x < st ? C.rows + (size_t)x * rs : D.X8 + (size_t)C.ki[x] * D.dw;
+            C.kd[x] = (double)u8_row_dist(C.qrow, rx, D.dw);
+        }
     }
     if (lane == 0) *ev += c - from;
     __syncwarp();
@@ -127,6 +146,9 @@ __device__ __forceinline__ int stage_and_measure_u8(const DataRef& D, const Cand
 template <int MODE, int QV>
 __device__ __forceinline__ int prune_candidates(const DataRef& D, const CandSmem& C, int c, double alpha2, int R,
                                                 int staged, int* out, long long* ev) {
+    if (MODE == MODE_EXACT_U8 && D.dw == 32)
+        return warp_prune_u8_32(D.X8, C.kd, C.ki, C.kp, c, alpha2, R, C.alive, C.cbuf, out, C.rows, C.nrm, staged,
+                                ev);
     if (MODE == MODE_EXACT_U8)
         return warp_prune_u8(D.X8, D.dw, C.kd, C.ki, C.kp, c, alpha2, R, C.alive, C.cbuf, out, C.rows, D.dw + 1,
                              staged, ev);
@@ -142,7 +164,7 @@ __global__ void __launch_bounds__(128) build_prune_kernel(BuildArgs A) {
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int lane = lane_id();
-    const CandSmem C = carve_cand(smem + (size_t)wib * A.prune_bytes, A.cap, A.D.dw);
+    const CandSmem C = carve_cand(smem + (size_t)wib * A.prune_bytes, A.cap, A.D.dw, A.S);
     const MakeAt<MODE, QV> make{A.D};
     long long ev_prune = 0;
     const int R = A.P.R;
@@ -357,7 +379,7 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int lane = lane_id();
-    const CandSmem C = carve_cand(smem + (size_t)wib * A.warp_bytes, A.cap, A.D.dw);
+    const CandSmem C = carve_cand(smem + (size_t)wib * A.warp_bytes, A.cap, A.D.dw, A.S);
     double* kd = C.kd;
     unsigned* ki = C.ki;
     unsigned* pcbuf = C.cbuf;
@@ -656,8 +678,10 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     // reverse groups: row (<= R) + incoming sources; larger groups take the
     // selection path (prune_by_selection)
     const int capR = next_pow2(std::max(4 * R, 256));
-    const int S = std::min(cap, 192);
-    const int SR = std::min(capR, 128);
+    // staged u8 rows per warp (prune / reverse): more rows = fewer L2 reads in
+    // the kill loop, fewer rows = more warps per SM (PK_PRUNE_S / PK_REV_S tune)
+    const int S = std::min(cap, env_int("PK_PRUNE_S", 128));
+    const int SR = std::min(capR, env_int("PK_REV_S", 128));
 
     BuildArgs A;
     A.search_bytes = align16(beam_smem_bytes(L, H));

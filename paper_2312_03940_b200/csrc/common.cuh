@@ -218,63 +218,68 @@ struct Exact32 {
 // (x - min), four per 32-bit word, rows of `dw` words.  |a - b| per byte
 // (__vabsdiffu4) and its square summed by __dp4a are exact integer
 // arithmetic, identical to the reference's float64 value (every term and sum
-// is an integer far below 2^53).  QW words per lane: dims [4*(lane + 32*v)].
+// is an integer far below 2^53).  Four lanes per candidate: lane quarter
+// sub = lane & 3 owns words 32*v + 8*sub .. +8 of every row (v < QW), so one
+// pass evaluates 8 candidates with two 128-bit loads per lane and a 2-step
+// reduction (rows with dw % 8 != 0 use guarded scalar loads).
 template <int QW>
 struct ExactU8 {
     const unsigned* X8;
-    unsigned q[QW];
+    unsigned q[8 * QW];
     int dw;
+
+    __device__ __forceinline__ void fetch(const unsigned* r, unsigned (&o)[8 * QW]) const {
+        const int sub = lane_id() & 3;
+#pragma unroll
+        for (int v = 0; v < QW; ++v) {
+            const int w0 = 32 * v + 8 * sub;
+            if ((dw & 7) == 0) {
+                if (w0 < dw) {
+                    const uint4 a = __ldg(reinterpret_cast<const uint4*>(r + w0));
+                    const uint4 b = __ldg(reinterpret_cast<const uint4*>(r + w0 + 4));
+                    o[8 * v + 0] = a.x; o[8 * v + 1] = a.y; o[8 * v + 2] = a.z; o[8 * v + 3] = a.w;
+                    o[8 * v + 4] = b.x; o[8 * v + 5] = b.y; o[8 * v + 6] = b.z; o[8 * v + 7] = b.w;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) o[8 * v + i] = 0u;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[8 * v + i] = w0 + i < dw ? __ldg(r + w0 + i) : 0u;
+            }
+        }
+    }
 
     __device__ __forceinline__ void load(const unsigned* X8_, int dw_, unsigned id) {
         X8 = X8_;
         dw = dw_;
-        const int lane = lane_id();
-#pragma unroll
-        for (int v = 0; v < QW; ++v) {
-            int col = lane + 32 * v;
-            q[v] = col < dw ? __ldg(X8 + (size_t)id * dw + col) : 0u;
-        }
+        fetch(X8 + (size_t)id * dw, q);
     }
 
     __device__ __forceinline__ unsigned partial(int id) const {
-        const unsigned* r = X8 + (size_t)id * dw;
-        const int lane = lane_id();
-        unsigned acc = 0u;
+        unsigned x[8 * QW];
+        fetch(X8 + (size_t)id * dw, x);
+        unsigned a0 = 0u, a1 = 0u;
 #pragma unroll
-        for (int v = 0; v < QW; ++v) {
-            int col = lane + 32 * v;
-            if (col < dw) {
-                unsigned x = __vabsdiffu4(q[v], __ldg(r + col));
-                acc = __dp4a(x, x, acc);
-            }
+        for (int i = 0; i < 8 * QW; i += 2) {
+            const unsigned e = __vabsdiffu4(q[i], x[i]);
+            const unsigned f = __vabsdiffu4(q[i + 1], x[i + 1]);
+            a0 = __dp4a(e, e, a0);
+            a1 = __dp4a(f, f, a1);
         }
-        return acc;
+        return a0 + a1;
     }
 
-    // same transposed butterfly as Exact32, on exact unsigned integers
     __device__ __forceinline__ double eval(const float* __restrict__, int cid, int c) const {
         const int lane = lane_id();
         double mine = 0.0;
         for (int g = 0; g < c; g += 8) {
-            unsigned v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int id = __shfl_sync(PK_FULL, cid, (g + j) & 31);
-                v[j] = (g + j < c) ? partial(id) : 0u;
-            }
-#pragma unroll
-            for (int s = 16, h = 4; s >= 4; s >>= 1, h >>= 1) {
-                const bool up = lane & s;
-#pragma unroll
-                for (int j = 0; j < h; ++j) {
-                    unsigned send = up ? v[j] : v[j + h];
-                    unsigned keep = up ? v[j + h] : v[j];
-                    v[j] = keep + __shfl_xor_sync(PK_FULL, send, s);
-                }
-            }
-            v[0] += __shfl_xor_sync(PK_FULL, v[0], 2);
-            v[0] += __shfl_xor_sync(PK_FULL, v[0], 1);
-            unsigned got = __shfl_sync(PK_FULL, v[0], ((lane - g) & 7) << 2);
+            const int gi = g + (lane >> 2);
+            const int id = __shfl_sync(PK_FULL, cid, gi & 31);
+            unsigned s = gi < c ? partial(id) : 0u;
+            s += __shfl_xor_sync(PK_FULL, s, 1);
+            s += __shfl_xor_sync(PK_FULL, s, 2);
+            const unsigned got = __shfl_sync(PK_FULL, s, ((lane - g) & 7) << 2);
             if (lane >= g && lane < g + 8 && lane < c) mine = (double)got;
         }
         return mine;
