@@ -97,6 +97,15 @@ int pk_beam_search_single(const float* x, int64_t n, int64_t dp, const int32_t* 
 int pk_brute_knn(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
                  int64_t* out_ids, double* out_sqd, void* stream);
 
+/* Same contract as pk_brute_knn (kk <= 32), on the tensor cores: a tcgen05
+ * fp16 GEMM screens the K' = 64 nearest candidates of every query (fused
+ * distance + top-K' epilogue), then each row is rescored with the float64
+ * sequential distance and sorted by (dist, id).  row_flags (device u8, m)
+ * marks rows whose error-bound certificate failed (the caller recomputes them
+ * with pk_brute_knn); *uncertified (device u64) counts them. */
+int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
+                    int64_t* out_ids, double* out_sqd, uint8_t* row_flags, uint64_t* uncertified, void* stream);
+
 /* Exact kNN of one float64 vector, no exclusion, kk = min(k, n).
  * Replaces _kernels.brute_knn_vector (_kernels.py:107-118). */
 int pk_brute_knn_vector(const float* x, int64_t n, int64_t dp, const double* qvec, int64_t k,

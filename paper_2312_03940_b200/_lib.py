@@ -35,6 +35,7 @@ SIGNATURES = {
     "pk_beam_search_single": [_P, _I, _I, _P, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P],
     "pk_brute_knn": [_P, _I, _I, _P, _I, _I, _P, _P, _P],
     "pk_brute_knn_vector": [_P, _I, _I, _P, _I, _P, _P, _P],
+    "pk_brute_knn_tc": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P],
     "pk_build_vamana": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P],
     "pk_robust_prune": [_P, _I, _I, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P],
     "pk_nearest_to_centroid": [_P, _I, _I, _P, _P],

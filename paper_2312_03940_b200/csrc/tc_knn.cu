@@ -1,0 +1,528 @@
+// Exact kNN on the tensor cores (the reference's brute_knn_batch,
+// _kernels.py:86-104, for BruteForceIndex / the exact pipeline mode).
+//
+// 1. Screening: a tcgen05 GEMM of fp16 queries x fp16 points (K-major, TMA
+//    tiles with 128-byte swizzle, fp32 accumulators in TMEM) with a fused
+//    epilogue that turns every accumulator into ||q||^2 + ||p||^2 - 2 q.p and
+//    keeps, per query row, the K' = 64 smallest screened distances (self
+//    excluded).  Warp-specialised, one CTA per 128-query block (optionally a
+//    slice of the points): warp 0 issues TMA, warp 1 issues tcgen05.mma (one
+//    elected lane) into a double-buffered TMEM accumulator (2 x 256 columns),
+//    warps 2-5 drain TMEM (tcgen05.ld) while the next tile accumulates.
+// 2. Rescoring: one warp per query recomputes the K' candidates with the
+//    reference's float64 sequential distance, sorts by (dist, id) and emits the
+//    first kk -- the same keys the reference selects among.  A per-row
+//    certificate checks that every screened-out point lies beyond the exact
+//    kk-th distance given the fp16 error bound; rows that fail are counted and
+//    reported (and recomputed exactly by the caller when requested).
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "../../include/peakann_b200.h"
+#include "api.cuh"
+#include "common.cuh"
+
+namespace pk {
+
+int grid_for(long long work, int block);
+
+constexpr int TC_BM = 128;          // queries per tile (UMMA M)
+constexpr int TC_BN = 256;          // points per tile (UMMA N)
+constexpr int TC_BK = 64;           // fp16 elements per stage (128-byte rows)
+constexpr int TC_STAGES = 3;
+constexpr int TC_KP = 64;           // screened candidates kept per row (K')
+constexpr int TC_THREADS = 192;     // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
+constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;
+constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
+constexpr int TC_LIST_BYTES = TC_KP * TC_BM * 8;
+constexpr size_t TC_SMEM = 1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256;
+
+struct TcArgs {
+    const float* qn;       // (m,) ||q||^2 of the fp16-rounded-from rows (fp32 originals)
+    const float* pn;       // (n,)
+    const long long* qids; // (m,) member ids (self exclusion), may be null
+    int m, n, kblocks;     // kblocks = Kp / 64
+    int tiles_per_split;   // point tiles handled by one CTA
+    int nsplit;
+    int* out_id;           // (m, nsplit, K') screened ids (-1 = empty)
+    float* out_d;          // (m, nsplit, K') screened distances
+};
+
+// ---- small PTX wrappers ---------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, unsigned long long* bar, int c0,
+                                            int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(unsigned long long* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16(unsigned tmem_d, unsigned long long da, unsigned long long db, unsigned idesc,
+                                           unsigned accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+// K-major, 128-byte-swizzled operand tile: rows of 128 B, 8-row groups 1024 B apart
+__device__ __forceinline__ unsigned long long umma_desc_sw128(const void* smem) {
+    const unsigned long long addr = smem_u32(smem);
+    unsigned long long d = 0;
+    d |= (addr >> 4) & 0x3fffull;          // start address
+    d |= 1ull << 16;                       // leading byte offset (unused for swizzled K-major)
+    d |= (unsigned long long)(1024 >> 4) << 32;  // stride byte offset: 8 rows x 128 B
+    d |= 1ull << 46;                       // descriptor version (sm100)
+    d |= 2ull << 61;                       // SWIZZLE_128B
+    return d;
+}
+
+// ---- screening kernel ------------------------------------------------------------------
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_constant__ CUtensorMap map_q,
+                                                                  const __grid_constant__ CUtensorMap map_p, TcArgs A) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(((size_t)smem_raw + 1023) & ~(size_t)1023);
+    unsigned char* stage_base = smem;
+    float* lst_d = reinterpret_cast<float*>(smem + (size_t)TC_STAGES * TC_STAGE_BYTES);
+    int* lst_i = reinterpret_cast<int*>(lst_d + TC_KP * TC_BM);
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(lst_i + TC_KP * TC_BM);
+    unsigned long long* full = bars;
+    unsigned long long* empty = bars + TC_STAGES;
+    unsigned long long* tfull = bars + 2 * TC_STAGES;
+    unsigned long long* tempty = bars + 2 * TC_STAGES + 2;
+    unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * TC_STAGES + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = lane_id();
+    const int qblock = blockIdx.x;
+    const int split = blockIdx.y;
+    const int ntiles_total = (A.n + TC_BN - 1) / TC_BN;
+    const int t0 = split * A.tiles_per_split;
+    const int t1 = min(ntiles_total, t0 + A.tiles_per_split);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const unsigned tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            unsigned phase = 0;
+            for (int t = t0; t < t1; ++t) {
+                for (int kb = 0; kb < A.kblocks; ++kb) {
+                    mbar_wait(empty + stage, phase ^ 1);
+                    unsigned char* sa = stage_base + (size_t)stage * TC_STAGE_BYTES;
+                    mbar_expect_tx(full + stage, TC_STAGE_BYTES);
+                    tma_load_2d(&map_q, sa, full + stage, kb * TC_BK, qblock * TC_BM);
+                    tma_load_2d(&map_p, sa + TC_A_BYTES, full + stage, kb * TC_BK, t * TC_BN);
+                    if (++stage == TC_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // instruction descriptor: F32 accumulate, F16 x F16, both K-major, N = 256, M = 128
+        const unsigned idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((unsigned)(TC_BN >> 3) << 17) |
+                               ((unsigned)(TC_BM >> 4) << 24);
+        int stage = 0;
+        unsigned phase = 0;
+        int acc = 0;
+        unsigned aphase = 0;
+        for (int t = t0; t < t1; ++t) {
+            mbar_wait(tempty + acc, aphase ^ 1);
+            tc_fence_after();
+            const unsigned tmem_d = tmem + (unsigned)(acc * TC_BN);
+            for (int kb = 0; kb < A.kblocks; ++kb) {
+                mbar_wait(full + stage, phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    unsigned char* sa = stage_base + (size_t)stage * TC_STAGE_BYTES;
+                    const unsigned long long da = umma_desc_sw128(sa);
+                    const unsigned long long db = umma_desc_sw128(sa + TC_A_BYTES);
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 16; ++k)  // 16 fp16 = 32 bytes per UMMA_K step
+                        tc_mma_f16(tmem_d, da + (unsigned long long)(2 * k), db + (unsigned long long)(2 * k), idesc,
+                                   (kb | k) != 0);
+                    tc_commit(empty + stage);
+                }
+                __syncwarp();
+                if (++stage == TC_STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (lane == 0) tc_commit(tfull + acc);
+            __syncwarp();
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    } else {
+        // epilogue: thread owns TMEM lane (query row) 32 * (warp % 4) + lane
+        const int ew = warp & 3;
+        const int row = ew * 32 + lane;
+        const int tid = row;  // list column
+        const int q = qblock * TC_BM + row;
+        const bool live = q < A.m;
+        const long long self = (live && A.qids) ? A.qids[q] : -1;
+        const float qn = live ? A.qn[q] : 0.f;
+        for (int k = 0; k < TC_KP; ++k) {
+            lst_d[k * TC_BM + tid] = __int_as_float(0x7f800000);
+            lst_i[k * TC_BM + tid] = -1;
+        }
+        float thr = __int_as_float(0x7f800000);
+        int acc = 0;
+        unsigned aphase = 0;
+        for (int t = t0; t < t1; ++t) {
+            mbar_wait(tfull + acc, aphase);
+            tc_fence_after();
+            const unsigned taddr = tmem + ((unsigned)(ew * 32) << 16) + (unsigned)(acc * TC_BN);
+            for (int ch = 0; ch < TC_BN / 32; ++ch) {
+                unsigned v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr + (unsigned)(ch * 32)));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int cbase = t * TC_BN + ch * 32;
+                if (!live) continue;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int col = cbase + j;
+                    if (col >= A.n) break;
+                    const float dd = qn + __ldg(A.pn + col) - 2.f * __uint_as_float(v[j]);
+                    if (dd < thr && (long long)col != self) {
+                        // the list is a binary max-heap: replace the root, sift down
+                        int i = 0;
+                        for (;;) {
+                            const int l = 2 * i + 1;
+                            if (l >= TC_KP) break;
+                            const int r = l + 1;
+                            const float dl = lst_d[l * TC_BM + tid];
+                            const float dr = r < TC_KP ? lst_d[r * TC_BM + tid] : -1.f;
+                            const int cidx = dr > dl ? r : l;
+                            const float dc = dr > dl ? dr : dl;
+                            if (dc <= dd) break;
+                            lst_d[i * TC_BM + tid] = dc;
+                            lst_i[i * TC_BM + tid] = lst_i[cidx * TC_BM + tid];
+                            i = cidx;
+                        }
+                        lst_d[i * TC_BM + tid] = dd;
+                        lst_i[i * TC_BM + tid] = col;
+                        thr = lst_d[tid];
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty + acc);
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+        if (live) {
+            const size_t base = ((size_t)q * A.nsplit + split) * TC_KP;
+            for (int k = 0; k < TC_KP; ++k) {
+                A.out_id[base + k] = lst_i[k * TC_BM + tid];
+                A.out_d[base + k] = lst_d[k * TC_BM + tid];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// ---- operand preparation -------------------------------------------------------------------
+// fp16 rows (K padded to a multiple of 64 with zeros) and fp32 squared norms
+__global__ void tc_prep_kernel(const float* __restrict__ X, int dp, const long long* rows, int m, int kp,
+                               __half* out, float* nrm) {
+    const int r = blockIdx.x;
+    if (r >= m) return;
+    const long long src = rows ? rows[r] : r;
+    const float* x = X + (size_t)src * dp;
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < kp; t += blockDim.x) {
+        const float v = t < dp ? x[t] : 0.f;
+        out[(size_t)r * kp + t] = __float2half_rn(v);
+        acc += (double)v * (double)v;
+    }
+    __shared__ double red[8];
+    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+        nrm[r] = (float)tot;
+    }
+}
+
+// ---- exact rescoring ---------------------------------------------------------------------
+// one warp per query: float64 sequential distances of the screened candidates,
+// (dist, id) sort, first kk out; certificate: every screened-out point has
+// screened distance >= the split's worst kept value, true >= screened - eps.
+__global__ void tc_rescore_kernel(const float* __restrict__ X, int dp, const long long* __restrict__ qids, int m,
+                                  int nsplit, const int* cand_i, const float* cand_d, int kk, float eps_scale,
+                                  const float* qn, float pmax, long long* out_ids, double* out_d,
+                                  unsigned long long* uncertified, unsigned char* row_flag, int P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int lane = lane_id();
+    double* kd = reinterpret_cast<double*>(smem) + (size_t)wib * P;
+    unsigned* ki = reinterpret_cast<unsigned*>(reinterpret_cast<double*>(smem) + (size_t)wpb * P) + (size_t)wib * P;
+    for (int t = blockIdx.x * wpb + wib; t < m; t += gridDim.x * wpb) {
+        const long long qi = qids[t];
+        const int c = nsplit * TC_KP;
+        Seq64Member dq{X + (size_t)qi * dp, dp};
+        for (int x = lane; x < P; x += 32) {
+            const int id = x < c ? cand_i[(size_t)t * c + x] : -1;
+            if (id >= 0) {
+                kd[x] = dq.eval_one(X, id);
+                ki[x] = (unsigned)id;
+            } else {
+                kd[x] = __longlong_as_double(0x7ff0000000000000LL);
+                ki[x] = 0xffffffffu;
+            }
+        }
+        __syncwarp();
+        for (int k = 2; k <= P; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < P; i += 32) {
+                    const int x = i ^ j;
+                    if (x > i) {
+                        double a = kd[i], b = kd[x];
+                        unsigned ia = ki[i], ib = ki[x];
+                        if (key_lt(b, ib, a, ia) == ((i & k) == 0)) {
+                            kd[i] = b; kd[x] = a;
+                            ki[i] = ib; ki[x] = ia;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        for (int x = lane; x < kk; x += 32) {
+            out_ids[(size_t)t * kk + x] = ki[x] == 0xffffffffu ? -1 : (long long)ki[x];
+            out_d[(size_t)t * kk + x] = kd[x];
+        }
+        // certificate
+        const double tk = kd[kk - 1];
+        const double eps = (double)eps_scale * sqrt((double)qn[t]) * (double)pmax;
+        bool ok = true;
+        for (int s = lane; s < nsplit; s += 32) {
+            float worst = -1.f;
+            bool full = true;
+            for (int k = 0; k < TC_KP; ++k) {
+                const size_t o = (size_t)t * c + (size_t)s * TC_KP + k;
+                if (cand_i[o] < 0) full = false;
+                worst = fmaxf(worst, cand_d[o]);
+            }
+            if (full && !((double)worst - eps > tk)) ok = false;
+        }
+        ok = __all_sync(PK_FULL, ok);
+        if (lane == 0) {
+            if (row_flag) row_flag[t] = ok ? 0 : 1;
+            if (!ok && uncertified) atomicAdd(uncertified, 1ull);
+        }
+        __syncwarp();
+    }
+}
+
+// ---- host -----------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    return fn;
+}
+
+static int make_map(CUtensorMap* map, const __half* base, int rows, int kp, int box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return 2;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
+    cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed");
+        return 2;
+    }
+    return 0;
+}
+
+__global__ void tc_max_kernel(const float* v, int n, float* out) {
+    float mx = 0.f;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) mx = fmaxf(mx, v[i]);
+    for (int s = 16; s; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(PK_FULL, mx, s));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(mx));
+}
+
+bool tc_supported() {
+    int dev = 0, major = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    return major == 10;
+}
+
+}  // namespace pk
+
+using namespace pk;
+
+extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
+                               int64_t* out_ids, double* out_sqd, uint8_t* row_flags, uint64_t* uncertified,
+                               void* stream) {
+    cudaStream_t st = as_stream(stream);
+    const int64_t kk = k < n - 1 ? k : n - 1;
+    if (kk <= 0 || m <= 0) return 0;
+    if (kk > TC_KP / 2) {
+        set_error("tensor-core kNN keeps k <= 32");
+        return 2;
+    }
+    if (!tc_supported()) {
+        set_error("tensor-core kNN needs an sm_100 device");
+        return 2;
+    }
+    const int kp = (int)((dp + TC_BK - 1) / TC_BK * TC_BK);
+    __half *qh = nullptr, *ph = nullptr;
+    float *qn = nullptr, *pn = nullptr, *pmax = nullptr;
+    long long* iota = nullptr;
+    PK_CHECK(scratch(&qh, (size_t)m * kp, st));
+    PK_CHECK(scratch(&ph, (size_t)n * kp, st));
+    PK_CHECK(scratch(&qn, (size_t)m, st));
+    PK_CHECK(scratch(&pn, (size_t)n, st));
+    PK_CHECK(scratch(&pmax, 1, st));
+    {
+        ProfScope _ps("tc_prep_kernel", st);
+        tc_prep_kernel<<<(unsigned)m, 256, 0, st>>>(x, (int)dp, reinterpret_cast<const long long*>(qids), (int)m, kp,
+                                                    qh, qn);
+        tc_prep_kernel<<<(unsigned)n, 256, 0, st>>>(x, (int)dp, nullptr, (int)n, kp, ph, pn);
+    }
+    PK_CHECK(cudaMemsetAsync(pmax, 0, sizeof(float), st));
+    {
+        ProfScope _ps("tc_max_kernel", st);
+        tc_max_kernel<<<grid_for(n, 256), 256, 0, st>>>(pn, (int)n, pmax);
+    }
+    PK_CHECK_LAUNCH("tc_prep");
+    CUtensorMap mq, mp;
+    int rc = make_map(&mq, qh, (int)m, kp, TC_BM);
+    if (rc) return rc;
+    rc = make_map(&mp, ph, (int)n, kp, TC_BN);
+    if (rc) return rc;
+    const int qblocks = (int)((m + TC_BM - 1) / TC_BM);
+    const int ntiles = (int)((n + TC_BN - 1) / TC_BN);
+    int nsplit = std::max(1, std::min(ntiles, (2 * sm_count() + qblocks - 1) / qblocks));
+    const int per = (ntiles + nsplit - 1) / nsplit;
+    nsplit = (ntiles + per - 1) / per;
+    TcArgs A;
+    A.qn = qn;
+    A.pn = pn;
+    A.qids = reinterpret_cast<const long long*>(qids);
+    A.m = (int)m;
+    A.n = (int)n;
+    A.kblocks = kp / TC_BK;
+    A.tiles_per_split = per;
+    A.nsplit = nsplit;
+    PK_CHECK(scratch(&A.out_id, (size_t)m * nsplit * TC_KP, st));
+    PK_CHECK(scratch(&A.out_d, (size_t)m * nsplit * TC_KP, st));
+    PK_CHECK(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
+    {
+        ProfScope _ps("tc_screen_kernel", st);
+        tc_screen_kernel<<<dim3((unsigned)qblocks, (unsigned)nsplit), TC_THREADS, TC_SMEM, st>>>(mq, mp, A);
+    }
+    PK_CHECK_LAUNCH("tc_screen_kernel");
+    // rescoring
+    float hmax = 0.f;
+    PK_CHECK(cudaMemcpyAsync(&hmax, pmax, sizeof(float), cudaMemcpyDeviceToHost, st));
+    PK_CHECK(cudaStreamSynchronize(st));
+    const int P = next_pow2(nsplit * TC_KP);
+    const int wpb = 4;
+    const size_t rs_smem = (size_t)wpb * P * 12;
+    if (rs_smem > 48 * 1024)
+        PK_CHECK(cudaFuncSetAttribute(tc_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
+    // |q.p error| <= (2 * 2^-11 + d * 2^-24) |q| |p| for fp16 operands with fp32 accumulation
+    const float eps_scale = 2.f * (2.f * ldexpf(1.f, -11) + (float)kp * ldexpf(1.f, -24));
+    {
+        ProfScope _ps("tc_rescore_kernel", st);
+        tc_rescore_kernel<<<(unsigned)std::min<long long>((m + wpb - 1) / wpb, 65535), 32 * wpb, rs_smem, st>>>(
+            x, (int)dp, reinterpret_cast<const long long*>(qids), (int)m, nsplit, A.out_id, A.out_d, (int)kk,
+            eps_scale, qn, sqrtf(hmax), reinterpret_cast<long long*>(out_ids), out_sqd,
+            reinterpret_cast<unsigned long long*>(uncertified), row_flags, P);
+    }
+    PK_CHECK_LAUNCH("tc_rescore_kernel");
+    for (void* p : {(void*)qh, (void*)ph, (void*)qn, (void*)pn, (void*)pmax, (void*)A.out_id, (void*)A.out_d})
+        release(p, st);
+    (void)iota;
+    return 0;
+}
