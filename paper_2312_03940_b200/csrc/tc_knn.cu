@@ -39,7 +39,7 @@ constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_LIST_BYTES = TC_KP * TC_BM * 8;
-constexpr size_t TC_SMEM = 1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256;
+constexpr size_t TC_SMEM = 1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256 + 2 * TC_BN * 4;
 
 struct TcArgs {
     const float* qn;       // (m,) ||q||^2 of the fp16-rounded-from rows (fp32 originals)
@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
     unsigned long long* tfull = bars + 2 * TC_STAGES;
     unsigned long long* tempty = bars + 2 * TC_STAGES + 2;
     unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * TC_STAGES + 4);
+    float* pn_s = reinterpret_cast<float*>(bars + 2 * TC_STAGES + 8);  // [2][TC_BN]
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
@@ -225,6 +226,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
         int acc = 0;
         unsigned aphase = 0;
         for (int t = t0; t < t1; ++t) {
+            // this tile's point norms, staged once for the 128 epilogue threads
+            for (int x = tid; x < TC_BN; x += TC_BM) {
+                const int col = t * TC_BN + x;
+                pn_s[acc * TC_BN + x] = col < A.n ? __ldg(A.pn + col) : 0.f;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
             const unsigned taddr = tmem + ((unsigned)(ew * 32) << 16) + (unsigned)(acc * TC_BN);
@@ -242,11 +249,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 const int cbase = t * TC_BN + ch * 32;
                 if (!live) continue;
+                const float* pnt = pn_s + acc * TC_BN + ch * 32;
+                float dmin = __int_as_float(0x7f800000);
 #pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float dd = qn + pnt[j] - 2.f * __uint_as_float(v[j]);
+                    v[j] = __float_as_uint(dd);
+                    dmin = fminf(dmin, dd);
+                }
+                if (!(dmin < thr)) continue;  // nothing in this chunk beats the current K'-th
                 for (int j = 0; j < 32; ++j) {
                     const int col = cbase + j;
                     if (col >= A.n) break;
-                    const float dd = qn + __ldg(A.pn + col) - 2.f * __uint_as_float(v[j]);
+                    const float dd = __uint_as_float(v[j]);
                     if (dd < thr && (long long)col != self) {
                         // the list is a binary max-heap: replace the root, sift down
                         int i = 0;
