@@ -39,7 +39,9 @@ constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_LIST_BYTES = TC_KP * TC_BM * 8;
-constexpr size_t TC_SMEM = 1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256 + 2 * TC_BN * 4;
+constexpr int TC_CH = 16;           // accumulator columns per tcgen05.ld in the epilogue
+constexpr size_t TC_SMEM =
+    1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256 + 2 * TC_BN * 4 + TC_CH * TC_BM * 4;
 
 struct TcArgs {
     const float* qn;       // (m,) ||q||^2 of the fp16-rounded-from rows (fp32 originals)
@@ -124,6 +126,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
     unsigned long long* tempty = bars + 2 * TC_STAGES + 2;
     unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * TC_STAGES + 4);
     float* pn_s = reinterpret_cast<float*>(bars + 2 * TC_STAGES + 8);  // [2][TC_BN]
+    float* stg = pn_s + 2 * TC_BN;                                     // [TC_CH][TC_BM]
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
@@ -235,53 +238,54 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
             const unsigned taddr = tmem + ((unsigned)(ew * 32) << 16) + (unsigned)(acc * TC_BN);
-            for (int ch = 0; ch < TC_BN / 32; ++ch) {
-                unsigned v[32];
+            for (int ch = 0; ch < TC_BN / TC_CH; ++ch) {
+                unsigned v[TC_CH];
                 asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                    "[%16];"
                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                       "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr + (unsigned)(ch * 32)));
+                      "=r"(v[15])
+                    : "r"(taddr + (unsigned)(ch * TC_CH)));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int cbase = t * TC_BN + ch * 32;
                 if (!live) continue;
-                const float* pnt = pn_s + acc * TC_BN + ch * 32;
-                float dmin = __int_as_float(0x7f800000);
+                const int cbase = t * TC_BN + ch * TC_CH;
+                const float* pnt = pn_s + acc * TC_BN + ch * TC_CH;
+                // distances of the chunk to smem, bit mask of the ones below the K'-th
+                unsigned mask = 0;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
+                for (int j = 0; j < TC_CH; ++j) {
                     const float dd = qn + pnt[j] - 2.f * __uint_as_float(v[j]);
-                    v[j] = __float_as_uint(dd);
-                    dmin = fminf(dmin, dd);
+                    stg[j * TC_BM + tid] = dd;
+                    mask |= (dd < thr ? 1u : 0u) << j;
                 }
-                if (!(dmin < thr)) continue;  // nothing in this chunk beats the current K'-th
-                for (int j = 0; j < 32; ++j) {
-                    const int col = cbase + j;
-                    if (col >= A.n) break;
-                    const float dd = __uint_as_float(v[j]);
-                    if (dd < thr && (long long)col != self) {
-                        // the list is a binary max-heap: replace the root, sift down
-                        int i = 0;
-                        for (;;) {
-                            const int l = 2 * i + 1;
-                            if (l >= TC_KP) break;
-                            const int r = l + 1;
-                            const float dl = lst_d[l * TC_BM + tid];
-                            const float dr = r < TC_KP ? lst_d[r * TC_BM + tid] : -1.f;
-                            const int cidx = dr > dl ? r : l;
-                            const float dc = dr > dl ? dr : dl;
-                            if (dc <= dd) break;
-                            lst_d[i * TC_BM + tid] = dc;
-                            lst_i[i * TC_BM + tid] = lst_i[cidx * TC_BM + tid];
-                            i = cidx;
-                        }
-                        lst_d[i * TC_BM + tid] = dd;
-                        lst_i[i * TC_BM + tid] = col;
-                        thr = lst_d[tid];
+                if (cbase + TC_CH > A.n) mask &= A.n > cbase ? (1u << (A.n - cbase)) - 1u : 0u;
+                if (self >= cbase && self < cbase + TC_CH) mask &= ~(1u << (int)(self - cbase));
+                // every lane walks its own pending candidates: the warp runs max-popcount
+                // iterations instead of one per column
+                while (mask) {
+                    const int j = __ffs(mask) - 1;
+                    mask &= mask - 1u;
+                    const float dd = stg[j * TC_BM + tid];
+                    if (!(dd < thr)) continue;
+                    // the list is a binary max-heap: replace the root, sift down
+                    int i = 0;
+                    for (;;) {
+                        const int l = 2 * i + 1;
+                        if (l >= TC_KP) break;
+                        const int r = l + 1;
+                        const float dl = lst_d[l * TC_BM + tid];
+                        const float dr = r < TC_KP ? lst_d[r * TC_BM + tid] : -1.f;
+                        const int cidx = dr > dl ? r : l;
+                        const float dc = dr > dl ? dr : dl;
+                        if (dc <= dd) break;
+                        lst_d[i * TC_BM + tid] = dc;
+                        lst_i[i * TC_BM + tid] = lst_i[cidx * TC_BM + tid];
+                        i = cidx;
                     }
+                    lst_d[i * TC_BM + tid] = dd;
+                    lst_i[i * TC_BM + tid] = cbase + j;
+                    thr = lst_d[tid];
                 }
             }
             tc_fence_before();
@@ -330,6 +334,27 @@ __global__ void tc_prep_kernel(const float* __restrict__ X, int dp, const long l
     }
 }
 
+// (dist, id) bitonic sort of P (power of two) entries in shared memory by one warp
+__device__ __forceinline__ void warp_bitonic(double* kd, unsigned* ki, int P, int lane) {
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                const int x = i ^ j;
+                if (x > i) {
+                    const double a = kd[i], b = kd[x];
+                    const unsigned ia = ki[i], ib = ki[x];
+                    if (key_lt(b, ib, a, ia) == ((i & k) == 0)) {
+                        kd[i] = b;
+                        kd[x] = a;
+                        ki[i] = ib;
+                        ki[x] = ia;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+}
+
 // ---- exact rescoring ---------------------------------------------------------------------
 // one warp per query: float64 sequential distances of the screened candidates,
 // (dist, id) sort, first kk out; certificate: every screened-out point has
@@ -347,39 +372,35 @@ __global__ void tc_rescore_kernel(const float* __restrict__ X, int dp, const lon
         const long long qi = qids[t];
         const int c = nsplit * TC_KP;
         Seq64Member dq{X + (size_t)qi * dp, dp};
+        const double eps = (double)eps_scale * sqrt((double)qn[t]) * (double)pmax;
+        // 1. order the candidates by screened distance
         for (int x = lane; x < P; x += 32) {
             const int id = x < c ? cand_i[(size_t)t * c + x] : -1;
-            if (id >= 0) {
-                kd[x] = dq.eval_one(X, id);
-                ki[x] = (unsigned)id;
+            kd[x] = id >= 0 ? (double)cand_d[(size_t)t * c + x] : __longlong_as_double(0x7ff0000000000000LL);
+            ki[x] = id >= 0 ? (unsigned)id : 0xffffffffu;
+        }
+        __syncwarp();
+        warp_bitonic(kd, ki, P, lane);
+        // 2. exact distances only where the screened value allows a place in the top kk:
+        //    true kk-th <= s_kk + eps and true >= screened - eps
+        const double bound = kd[kk - 1] + 2.0 * eps;
+        __syncwarp();
+        for (int x = lane; x < P; x += 32) {
+            if (ki[x] != 0xffffffffu && kd[x] <= bound) {
+                kd[x] = dq.eval_one(X, (int)ki[x]);
             } else {
                 kd[x] = __longlong_as_double(0x7ff0000000000000LL);
                 ki[x] = 0xffffffffu;
             }
         }
         __syncwarp();
-        for (int k = 2; k <= P; k <<= 1)
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = lane; i < P; i += 32) {
-                    const int x = i ^ j;
-                    if (x > i) {
-                        double a = kd[i], b = kd[x];
-                        unsigned ia = ki[i], ib = ki[x];
-                        if (key_lt(b, ib, a, ia) == ((i & k) == 0)) {
-                            kd[i] = b; kd[x] = a;
-                            ki[i] = ib; ki[x] = ia;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
+        warp_bitonic(kd, ki, P, lane);
         for (int x = lane; x < kk; x += 32) {
             out_ids[(size_t)t * kk + x] = ki[x] == 0xffffffffu ? -1 : (long long)ki[x];
             out_d[(size_t)t * kk + x] = kd[x];
         }
         // certificate
         const double tk = kd[kk - 1];
-        const double eps = (double)eps_scale * sqrt((double)qn[t]) * (double)pmax;
         bool ok = true;
         for (int s = lane; s < nsplit; s += 32) {
             float worst = -1.f;
