@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "../../include/peakann_b200.h"
 #include "api.cuh"
@@ -32,11 +33,11 @@ int grid_for(long long work, int block);
 constexpr int TC_BM = 128;          // queries per tile (UMMA M)
 constexpr int TC_BN = 256;          // points per tile (UMMA N)
 constexpr int TC_BK = 64;           // fp16 elements per stage (128-byte rows)
-constexpr int TC_STAGES = 3;
+constexpr int TC_STAGES = 4;
 constexpr int TC_KP = 64;           // screened candidates kept per row (K')
 constexpr int TC_THREADS = 192;     // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
-constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;
+constexpr int TC_B_BYTES = (TC_BN / 2) * TC_BK * 2;  // each CTA of the pair holds half the point tile
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_LIST_BYTES = TC_KP * TC_BM * 8;
 constexpr int TC_CH = 16;           // accumulator columns per tcgen05.ld in the epilogue
@@ -49,6 +50,7 @@ struct TcArgs {
     const long long* qids; // (m,) member ids (self exclusion), may be null
     int m, n, kblocks;     // kblocks = Kp / 64
     int tiles_per_split;   // point tiles handled by one CTA
+    int dbg;
     int nsplit;
     int* out_id;           // (m, nsplit, K') screened ids (-1 = empty)
     float* out_d;          // (m, nsplit, K') screened distances
@@ -84,6 +86,47 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, u
         "l"(reinterpret_cast<unsigned long long>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ unsigned mapa_shared(unsigned addr, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(unsigned cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// pair TMA: the bytes land in this CTA's smem, completion is counted on the leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, void* dst, unsigned bar_cluster, int c0,
+                                                 int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(unsigned long long* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16_pair(unsigned tmem_d, unsigned long long da, unsigned long long db,
+                                                unsigned idesc, unsigned accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(unsigned long long* bar) {
@@ -112,10 +155,15 @@ __device__ __forceinline__ unsigned long long umma_desc_sw128(const void* smem) 
 }
 
 // ---- screening kernel ------------------------------------------------------------------
-__global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_constant__ CUtensorMap map_q,
+// CTA pair (cluster of 2 along x): CTA r owns query rows (2*pair + r)*128.. and loads
+// point rows t*256 + r*128.. of every tile; the leader issues M=256 x N=256 MMAs that
+// read both CTAs' smem and write each CTA's 128 rows into its own TMEM.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_constant__ CUtensorMap map_q,
                                                                   const __grid_constant__ CUtensorMap map_p, TcArgs A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(((size_t)smem_raw + 1023) & ~(size_t)1023);
+    // offset from the shared array itself (not an integer round trip) so every
+    // access below compiles to LDS/STS instead of generic loads/stores
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* stage_base = smem;
     float* lst_d = reinterpret_cast<float*>(smem + (size_t)TC_STAGES * TC_STAGE_BYTES);
     int* lst_i = reinterpret_cast<int*>(lst_d + TC_KP * TC_BM);
@@ -136,6 +184,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
     const int t0 = split * A.tiles_per_split;
     const int t1 = min(ntiles_total, t0 + A.tiles_per_split);
 
+    const unsigned rank = cluster_rank();
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
             mbar_init(full + s, 1);
@@ -143,20 +192,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 128);
+            mbar_init(tempty + a, 8);  // one arrival per epilogue warp of both CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();
     tc_fence_after();
     const unsigned tmem = *tmem_slot;
+    const unsigned full_lead = mapa_shared(smem_u32(full), 0);
+    const unsigned tempty_lead = mapa_shared(smem_u32(tempty), 0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -166,9 +218,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
                 for (int kb = 0; kb < A.kblocks; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1);
                     unsigned char* sa = stage_base + (size_t)stage * TC_STAGE_BYTES;
-                    mbar_expect_tx(full + stage, TC_STAGE_BYTES);
-                    tma_load_2d(&map_q, sa, full + stage, kb * TC_BK, qblock * TC_BM);
-                    tma_load_2d(&map_p, sa + TC_A_BYTES, full + stage, kb * TC_BK, t * TC_BN);
+                    if (rank == 0) mbar_expect_tx(full + stage, 2 * TC_STAGE_BYTES);
+                    const unsigned fb = full_lead + 8u * (unsigned)stage;
+                    tma_load_2d_pair(&map_q, sa, fb, kb * TC_BK, qblock * TC_BM);
+                    tma_load_2d_pair(&map_p, sa + TC_A_BYTES, fb, kb * TC_BK, t * TC_BN + (int)rank * (TC_BN / 2));
                     if (++stage == TC_STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -176,10 +229,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
                 }
             }
         }
-    } else if (warp == 1) {
-        // instruction descriptor: F32 accumulate, F16 x F16, both K-major, N = 256, M = 128
+    } else if (warp == 1 && rank == 0) {
+        // instruction descriptor: F32 accumulate, F16 x F16, both K-major, N = 256, M = 256 (pair)
         const unsigned idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((unsigned)(TC_BN >> 3) << 17) |
-                               ((unsigned)(TC_BM >> 4) << 24);
+                               ((unsigned)((2 * TC_BM) >> 4) << 24);
         int stage = 0;
         unsigned phase = 0;
         int acc = 0;
@@ -197,9 +250,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
                     const unsigned long long db = umma_desc_sw128(sa + TC_A_BYTES);
 #pragma unroll
                     for (int k = 0; k < TC_BK / 16; ++k)  // 16 fp16 = 32 bytes per UMMA_K step
-                        tc_mma_f16(tmem_d, da + (unsigned long long)(2 * k), db + (unsigned long long)(2 * k), idesc,
-                                   (kb | k) != 0);
-                    tc_commit(empty + stage);
+                        if (!(A.dbg & 2)) tc_mma_f16_pair(tmem_d, da + (unsigned long long)(2 * k), db + (unsigned long long)(2 * k),
+                                        idesc, (kb | k) != 0);
+                    tc_commit_pair(empty + stage);
                 }
                 __syncwarp();
                 if (++stage == TC_STAGES) {
@@ -207,12 +260,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
                     phase ^= 1;
                 }
             }
-            if (lane == 0) tc_commit(tfull + acc);
+            if (lane == 0) tc_commit_pair(tfull + acc);
             __syncwarp();
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
-    } else {
+    } else if (warp >= 2) {
         // epilogue: thread owns TMEM lane (query row) 32 * (warp % 4) + lane
         const int ew = warp & 3;
         const int row = ew * 32 + lane;
@@ -240,6 +293,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
             const unsigned taddr = tmem + ((unsigned)(ew * 32) << 16) + (unsigned)(acc * TC_BN);
             for (int ch = 0; ch < TC_BN / TC_CH; ++ch) {
                 unsigned v[TC_CH];
+                __syncwarp();
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
                     "[%16];"
@@ -248,16 +302,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
                       "=r"(v[15])
                     : "r"(taddr + (unsigned)(ch * TC_CH)));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (!live) continue;
+                if (A.dbg & 1) continue;  // warp-uniform (profiling aid)
                 const int cbase = t * TC_BN + ch * TC_CH;
                 const float* pnt = pn_s + acc * TC_BN + ch * TC_CH;
                 // distances of the chunk to smem, bit mask of the ones below the K'-th
+                float pv[TC_CH];
+#pragma unroll
+                for (int j = 0; j < TC_CH; j += 4) {
+                    const float4 t4 = *reinterpret_cast<const float4*>(pnt + j);
+                    pv[j] = t4.x;
+                    pv[j + 1] = t4.y;
+                    pv[j + 2] = t4.z;
+                    pv[j + 3] = t4.w;
+                }
                 unsigned mask = 0;
 #pragma unroll
                 for (int j = 0; j < TC_CH; ++j) {
-                    const float dd = qn + pnt[j] - 2.f * __uint_as_float(v[j]);
-                    stg[j * TC_BM + tid] = dd;
+                    const float dd = qn + pv[j] - 2.f * __uint_as_float(v[j]);
+                    v[j] = __float_as_uint(dd);
                     mask |= (dd < thr ? 1u : 0u) << j;
+                }
+                if (!live) mask = 0;
+                if (__any_sync(PK_FULL, mask != 0)) {
+#pragma unroll
+                    for (int j = 0; j < TC_CH; ++j) stg[j * TC_BM + tid] = __uint_as_float(v[j]);
                 }
                 if (cbase + TC_CH > A.n) mask &= A.n > cbase ? (1u << (A.n - cbase)) - 1u : 0u;
                 if (self >= cbase && self < cbase + TC_CH) mask &= ~(1u << (int)(self - cbase));
@@ -289,7 +357,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
                 }
             }
             tc_fence_before();
-            mbar_arrive(tempty + acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_lead + 8u * (unsigned)acc);
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
@@ -303,9 +372,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_screen_kernel(const __grid_c
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 
@@ -514,9 +584,9 @@ extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int6
     CUtensorMap mq, mp;
     int rc = make_map(&mq, qh, (int)m, kp, TC_BM);
     if (rc) return rc;
-    rc = make_map(&mp, ph, (int)n, kp, TC_BN);
+    rc = make_map(&mp, ph, (int)n, kp, TC_BN / 2);
     if (rc) return rc;
-    const int qblocks = (int)((m + TC_BM - 1) / TC_BM);
+    const int qblocks = (int)((m + 2 * TC_BM - 1) / (2 * TC_BM)) * 2;  // whole CTA pairs
     const int ntiles = (int)((n + TC_BN - 1) / TC_BN);
     int nsplit = std::max(1, std::min(ntiles, (2 * sm_count() + qblocks - 1) / qblocks));
     const int per = (ntiles + nsplit - 1) / nsplit;
@@ -530,6 +600,7 @@ extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int6
     A.kblocks = kp / TC_BK;
     A.tiles_per_split = per;
     A.nsplit = nsplit;
+    A.dbg = getenv("PK_TC_DEBUG") ? atoi(getenv("PK_TC_DEBUG")) : 0;
     PK_CHECK(scratch(&A.out_id, (size_t)m * nsplit * TC_KP, st));
     PK_CHECK(scratch(&A.out_d, (size_t)m * nsplit * TC_KP, st));
     PK_CHECK(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
