@@ -15,9 +15,11 @@ through the public API (`run_pipeline(PointSet(host array))`) with the
 host->device upload of the points and the device->host read of every result
 array inside the timed region.
 
-Multi-GPU (torchrun, one rank per GPU): each rank runs its own replica of the
-workload (replicas only in this round -- see DESIGN.md, multi-GPU), so per-GPU
-work is fixed ("scaling": "weak"); times are the max over ranks.
+Multi-GPU (torchrun, one rank per GPU, NCCL): the same n points are split
+across the ranks (shard.py: build batches, kNN queries, dependent-point
+queries; out-lists / rows / kNN rows all-gathered, lam / delta all-reduced),
+so the total work is fixed ("scaling": "strong"); value = n / (max over ranks
+of the step time).
 
 --impl reference times the reference algorithm's CPU implementation on the
 host cores: the oracle/ C restatement of the reference's numba kernels
@@ -178,7 +180,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(args.config, args.n, 1),
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -188,6 +190,7 @@ def run_reference(args):
 
 
 def workload_config(name, n_override, n_gpus):
+    par = "single GPU" if n_gpus == 1 else f"sharded x{n_gpus} (queries + build batches split, NCCL all-gather)"
     from paper_2312_03940_b200 import workloads
 
     w = workloads.WORKLOADS[name]
@@ -195,7 +198,7 @@ def workload_config(name, n_override, n_gpus):
     return {"workload": f"{name}: n={n} d={w.d} Vamana R={w.R} L={w.L} alpha={w.alpha} {w.density} k={w.k} "
                         f"ProductCenter({w.n_centers}) doubling from {2 * w.k}, threshold 300",
             "n": n, "d": w.d, "R": w.R, "L": w.L, "k": w.k, "density": w.density,
-            "parallelism": f"replicas x{n_gpus}", "l2": "flushed (256 MiB write) before every timed step"}
+            "parallelism": par, "l2": "flushed (256 MiB write) before every timed step"}
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -209,13 +212,16 @@ def main_ours(args):
     from paper_2312_03940_b200 import _lib, vamana, workloads
     from paper_2312_03940_b200.cluster import run_pipeline_device
     from paper_2312_03940_b200.core import upload_points
+    from paper_2312_03940_b200.shard import Comm
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = Comm()
 
     name = args.config
     w = workloads.WORKLOADS[name]
@@ -235,7 +241,7 @@ def main_ours(args):
 
     # warm-up (untimed)
     for _ in range(args.warmup):
-        run_pipeline_device(p, **kw)
+        run_pipeline_device(p, **kw, comm=comm)
     torch.cuda.synchronize()
 
     build_stats = torch.zeros(4, dtype=torch.int64, device="cuda")
@@ -260,7 +266,7 @@ def main_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         trace = []
-        last = run_pipeline_device(p, **kw, trace=trace)
+        last = run_pipeline_device(p, **kw, trace=trace, comm=comm)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -279,7 +285,7 @@ def main_ours(args):
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_step = float(t_local.item()) / args.steps
-    value = world * n / (ms_step / 1e3)
+    value = n / (ms_step / 1e3)  # the n points are split across the ranks
 
     # quality of the last timed run (ARI vs generator labels)
     labels = _lib.to_host(last["labels"])
@@ -297,7 +303,7 @@ def main_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        res = pk.run_pipeline(pk.PointSet(host_view), **kw)
+        res = pk.run_pipeline(pk.PointSet(host_view), **kw, comm=comm)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -309,7 +315,7 @@ def main_ours(args):
     t_e2e = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = world * n / (float(t_e2e.item()) / args.e2e_steps / 1e3)
+    e2e_value = n / (float(t_e2e.item()) / args.e2e_steps / 1e3)
 
     # roofline of the dominant kernel
     hbm, tflops, peak_kind = peaks()
@@ -347,7 +353,7 @@ def main_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": {0: "f64", 1: "f32 (exact: integer data)", 2: "u8/int32 (exact: integer data)"}[p.mode],
             "data": f"synthetic ({name} generator, seed 0)",
             "config": workload_config(name, args.n, world),

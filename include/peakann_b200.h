@@ -125,6 +125,33 @@ int pk_build_vamana(const float* x, int64_t n, int64_t dp, const uint32_t* x8, i
                     const int32_t* starts, int64_t s, const int32_t* order, int32_t* adj_out,
                     int32_t* deg_out, int64_t* stats, int hash_bits, void* stream);
 
+/* Sharded build: one process per GPU, every rank holds the full point set
+ * and ends with the full graph (identical on every rank and to
+ * pk_build_vamana).  A batch of m >= min_shard points is split into world
+ * contiguous chunks of c = ceil(m / world); rank r searches and prunes chunk r
+ * into xids[(r*c + t) * R ...] / xlen[r*c + t], then calls
+ *     exchange(ctx, PK_XCHG_OUTLISTS, c, 0)
+ * which must all-gather xids[0, world*c*R) and xlen[0, world*c) in place.
+ * Reverse-edge re-prunes run on the targets u with u % world == rank; their
+ * rows are packed as [u, deg, row[R]] (R + 2 int32) into xsend and
+ *     maxc = exchange(ctx, PK_XCHG_ROWS, own_count, 0)
+ * must all-gather the counts into xcnt[world] (device int32) and
+ * xsend[0, maxc*(R+2)) into xrecv[0, world*maxc*(R+2)), returning maxc (< 0 =
+ * error).  Buffers: xids >= (B + world) * R, xlen >= B + world with B the
+ * largest batch (<= n), xsend >= U * (R+2), xrecv >= world * U * (R+2) with
+ * U = min(n, B * R).  Smaller batches run replicated (no exchange).
+ * Replaces the batch loop of vamana.py:146-169 with the multi-GPU split
+ * SURVEY.md section 8(e) step 6 describes. */
+typedef int64_t (*pk_exchange_fn)(void* ctx, int kind, int64_t a, int64_t b);
+#define PK_XCHG_OUTLISTS 0
+#define PK_XCHG_ROWS 1
+int pk_build_vamana_sharded(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                            int64_t R, int64_t L, double alpha,
+                            const int32_t* starts, int64_t s, const int32_t* order, int32_t* adj_out,
+                            int32_t* deg_out, int64_t* stats, int hash_bits, int rank, int world,
+                            int64_t min_shard, pk_exchange_fn exchange, void* ctx, int32_t* xids,
+                            int32_t* xlen, int32_t* xsend, int32_t* xrecv, int32_t* xcnt, void* stream);
+
 /* RobustPrune of vertex p over explicit candidates (ids, squared distances)
  * merged with its current out-list cur_ids (distances recomputed).  Replaces
  * _kernels.robust_prune_standalone (_kernels.py:318-335).  out (R,) int64,

@@ -27,6 +27,9 @@ _I = ctypes.c_int64
 _i = ctypes.c_int
 _D = ctypes.c_double
 
+# host callback of the sharded build (pk_exchange_fn): (ctx, kind, a, b) -> int64
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64)
+
 # name -> argtypes (every entry returns int status)
 SIGNATURES = {
     "pk_check_exact32": [_P, _I, _I, _I, _P, _P],
@@ -37,6 +40,8 @@ SIGNATURES = {
     "pk_brute_knn_vector": [_P, _I, _I, _P, _I, _P, _P, _P],
     "pk_brute_knn_tc": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P],
     "pk_build_vamana": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P],
+    "pk_build_vamana_sharded": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _i, _i, _I,
+                                EXCHANGE_FN, _P, _P, _P, _P, _P, _P, _P],
     "pk_robust_prune": [_P, _I, _I, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P],
     "pk_nearest_to_centroid": [_P, _I, _I, _P, _P],
     "pk_sqrt": [_P, _I, _P, _P],

@@ -322,7 +322,7 @@ def reapply_policies(state: DpcState, center_policy: CenterPolicy, noise_policy:
     return _apply_policies(state, center_policy, noise_policy)
 
 
-def _build_index(p: PointSet, config: IndexConfig) -> KnnIndex:
+def _build_index(p: PointSet, config: IndexConfig, comm=None) -> KnnIndex:
     if isinstance(config, BruteForceConfig):
         return build_bruteforce(p)
     if isinstance(config, VamanaConfig):
@@ -335,6 +335,7 @@ def _build_index(p: PointSet, config: IndexConfig) -> KnnIndex:
             seed=config.seed,
             medoid_start=config.medoid_start,
             query_beam=config.L,
+            comm=comm,
         )
     raise TypeError(f"unknown index config {config!r}")
 
@@ -345,11 +346,36 @@ def _sync():
     torch.cuda.synchronize()
 
 
+def _knn_all_device(index: KnnIndex, n: int, k: int, comm=None):
+    """knn_all on device; with `comm` each rank answers a contiguous chunk of
+    the queries and the (n, k) rows are all-gathered."""
+    import torch
+
+    dev = _lib.device()
+    if comm is None or comm.world == 1:
+        return index.knn_batch_device(torch.arange(n, dtype=torch.int64, device=dev), k)
+    lo, hi = comm.my_range(n)
+    c = comm.chunk(n)
+    kk = max(0, min(k, n - 1))
+    ids = torch.full((comm.world * c, kk), -1, dtype=torch.int64, device=dev)
+    sqd = torch.full((comm.world * c, kk), float("inf"), dtype=torch.float64, device=dev)
+    if hi > lo:
+        li, ls = index.knn_batch_device(torch.arange(lo, hi, dtype=torch.int64, device=dev), k)
+        ids[lo:hi] = li
+        sqd[lo:hi] = ls
+    comm.all_gather_chunks(ids, c)
+    comm.all_gather_chunks(sqd, c)
+    return ids[:n], sqd[:n]
+
+
 def run_pipeline_device(p: PointSet, index_config: IndexConfig, k: int, density_kind: str,
                         center_policy: CenterPolicy, noise_policy: NoisePolicy = NoisePolicy(),
-                        doubling_params: Optional[DoublingParams] = None, trace=None):
+                        doubling_params: Optional[DoublingParams] = None, trace=None, comm=None):
     """The pipeline with every intermediate left in HBM.  Returns a dict of
-    device tensors plus the stage timings (cluster.py:279-311)."""
+    device tensors plus the stage timings (cluster.py:279-311).  With `comm`
+    (shard.Comm, one process per GPU) the build, the kNN queries and the
+    dependent-point queries are split across the ranks (shard.py); every rank
+    returns the full result."""
     import torch
 
     if doubling_params is None:
@@ -358,19 +384,18 @@ def run_pipeline_device(p: PointSet, index_config: IndexConfig, k: int, density_
     timings: dict = {}
     _sync()
     t0 = time.perf_counter()
-    index = _build_index(p, index_config)
+    index = _build_index(p, index_config, comm)
     _sync()
     t1 = time.perf_counter()
     if k < 1:
         raise ValueError(f"k must be >= 1, got {k}")
-    all_t = torch.arange(n, dtype=torch.int64, device=_lib.device())
-    ids_t, sqd_t = index.knn_batch_device(all_t, k)
+    ids_t, sqd_t = _knn_all_device(index, n, k, comm)
     dists_t = sqrt_device(sqd_t)
     check_neighborhoods(density_kind, p, Neighborhoods.on_device(ids_t, dists_t))
     rho_t = densities_device(density_kind, ids_t, dists_t)
     _sync()
     t2 = time.perf_counter()
-    lam_t, delta_t, rank_t = dependents_device(index, p, rho_t, ids_t, dists_t, doubling_params, trace)
+    lam_t, delta_t, rank_t = dependents_device(index, p, rho_t, ids_t, dists_t, doubling_params, trace, comm)
     _sync()
     t3 = time.perf_counter()
     labels_t, c_t, n_t = _apply_policies_device(rho_t, lam_t, delta_t, ids_t, center_policy, noise_policy, rank_t)
@@ -392,9 +417,13 @@ def run_pipeline(
     center_policy: CenterPolicy,
     noise_policy: NoisePolicy = NoisePolicy(),
     doubling_params: Optional[DoublingParams] = None,
+    comm=None,
 ) -> PipelineResult:
-    """Index build, kNN, densities, dependent points, policies, union-find."""
-    out = run_pipeline_device(p, index_config, k, density_kind, center_policy, noise_policy, doubling_params)
+    """Index build, kNN, densities, dependent points, policies, union-find.
+    `comm` (shard.Comm) splits the work across one process per GPU; every
+    rank returns the full result."""
+    out = run_pipeline_device(p, index_config, k, density_kind, center_policy, noise_policy, doubling_params,
+                              comm=comm)
     state = DpcState(rho=_lib.to_host(out["rho"]),
                      dependents=Dependents(_lib.to_host(out["lam"]), _lib.to_host(out["delta"])),
                      neighbors=Neighborhoods(_lib.to_host(out["ids"]), _lib.to_host(out["dists"])))

@@ -284,7 +284,54 @@ struct RevArgs {
     int capB;       // largest group handled by reverse_big_kernel
     int* biglist;   // groups with cap < candidates <= capB
     int* nbig;
+    int rank, world;  // sharded build: this rank re-prunes the targets u % world == rank
 };
+
+// multi-GPU build context (pk_build_vamana_sharded)
+struct Shard {
+    int rank = 0, world = 1;
+    long long min_shard = 0;
+    pk_exchange_fn fn = nullptr;
+    void* ctx = nullptr;
+    int *xids = nullptr, *xlen = nullptr, *xsend = nullptr, *xrecv = nullptr, *xcnt = nullptr;
+};
+
+// rows of the targets this rank re-pruned -> [u, deg, row[R]] records
+__global__ void pack_rows_kernel(const int* targets, const int* ntargets, int rank, int world, const int* adj,
+                                 const int* deg, int R, int* out, int* npack) {
+    const int lane = lane_id();
+    const int nt = *ntargets;
+    const int wpb = blockDim.x >> 5;
+    for (int s = blockIdx.x * wpb + (threadIdx.x >> 5); s < nt; s += gridDim.x * wpb) {
+        const int u = targets[s];
+        if (u % world != rank) continue;
+        int pos = 0;
+        if (lane == 0) pos = atomicAdd(npack, 1);
+        pos = __shfl_sync(PK_FULL, pos, 0);
+        int* rec = out + (size_t)pos * (R + 2);
+        if (lane == 0) {
+            rec[0] = u;
+            rec[1] = deg[u];
+        }
+        for (int x = lane; x < R; x += 32) rec[2 + x] = adj[(size_t)u * R + x];
+    }
+}
+
+// apply the other ranks' records (every rank ends with the same graph)
+__global__ void unpack_rows_kernel(const int* recv, const int* cnt, int maxc, int world, int rank, int R, int* adj,
+                                   int* deg) {
+    const int lane = lane_id();
+    const int wpb = blockDim.x >> 5;
+    const long long tot = (long long)world * maxc;
+    for (long long e = blockIdx.x * (long long)wpb + (threadIdx.x >> 5); e < tot; e += (long long)gridDim.x * wpb) {
+        const int r = (int)(e / maxc), i = (int)(e % maxc);
+        if (r == rank || i >= cnt[r]) continue;
+        const int* rec = recv + (size_t)e * (R + 2);
+        const int u = rec[0];
+        if (lane == 0) deg[u] = rec[1];
+        for (int x = lane; x < R; x += 32) adj[(size_t)u * R + x] = rec[2 + x];
+    }
+}
 
 // Oversized group (more candidates than the shared buffer): RobustPrune by
 // repeated selection of the smallest alive key (equal keys = same id, i.e. a
@@ -389,6 +436,11 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
     long long ev = 0;
     for (int s = blockIdx.x * wpb + wib; s < nt; s += gridDim.x * wpb) {
         const unsigned u = (unsigned)A.targets[s];
+        if (A.world > 1 && (int)(u % (unsigned)A.world) != A.rank) {
+            // another rank re-prunes this row; only the per-batch counter is reset here
+            if (lane == 0) A.cnt[u] = 0;
+            continue;
+        }
         const int nd = A.deg[u];
         const int off = A.offs[s];
         const int size = A.sizes[s];
@@ -670,7 +722,7 @@ int config_kernel(K kern, size_t warp_bytes, int want_wpb, int* wpb_out, int* gr
 
 template <int MODE, int QV>
 int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
-              int* adj, int* deg, long long* stats, int hash_bits, cudaStream_t st) {
+              int* adj, int* deg, long long* stats, int hash_bits, const Shard& SH, cudaStream_t st) {
     const bool u8 = MODE == MODE_EXACT_U8;
     const int H = choose_hash(L, hash_bits, n);
     const int cap = next_pow2(2 * L + 64 + R);
@@ -716,8 +768,16 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     PK_CHECK(scratch(&vlog_i, (size_t)mb * vcap, st));
     PK_CHECK(scratch(&vlog_d, (size_t)mb * vcap, st));
     PK_CHECK(scratch(&vlen, (size_t)mb, st));
-    PK_CHECK(scratch(&new_ids, (size_t)E, st));
-    PK_CHECK(scratch(&new_len, (size_t)mb, st));
+    const bool multi = SH.world > 1;
+    if (multi) {
+        new_ids = SH.xids;
+        new_len = SH.xlen;
+    } else {
+        PK_CHECK(scratch(&new_ids, (size_t)E, st));
+        PK_CHECK(scratch(&new_len, (size_t)mb, st));
+    }
+    int* npack = nullptr;
+    PK_CHECK(scratch(&npack, 1, st));
     PK_CHECK(scratch(&cnt, (size_t)n, st));
     PK_CHECK(scratch(&tslot, (size_t)n, st));
     PK_CHECK(scratch(&targets, (size_t)ub, st));
@@ -780,21 +840,38 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     B.capB = capB;
     B.biglist = biglist;
     B.nbig = nbig;
+    B.rank = 0;
+    B.world = 1;
 
     for (int lo = 0, batch = 1; lo < n; lo += batch, batch *= 2) {
         const int m = std::min(batch, n - lo);
-        A.bids = order + lo;
-        A.m = m;
-        {
-            ProfScope _ps("build_search_kernel", st);
-            sk<<<std::min(grid_s, (m + wpb_s - 1) / wpb_s), 32 * wpb_s, A.search_bytes * wpb_s, st>>>(A);
+        // sharded batch: rank r searches + prunes chunk r, then the out-lists are all-gathered
+        const bool sharded = multi && m >= SH.min_shard;
+        const int chunk = sharded ? (m + SH.world - 1) / SH.world : m;
+        const int my_lo = sharded ? std::min(m, SH.rank * chunk) : 0;
+        const int my_m = sharded ? std::min(m, my_lo + chunk) - my_lo : m;
+        A.bids = order + lo + my_lo;
+        A.m = my_m;
+        A.new_ids = new_ids + (size_t)my_lo * R;
+        A.new_len = new_len + my_lo;
+        if (my_m > 0) {
+            {
+                ProfScope _ps("build_search_kernel", st);
+                sk<<<std::min(grid_s, (my_m + wpb_s - 1) / wpb_s), 32 * wpb_s, A.search_bytes * wpb_s, st>>>(A);
+            }
+            PK_CHECK_LAUNCH("build_search_kernel");
+            {
+                ProfScope _ps("build_prune_kernel", st);
+                pkk<<<std::min(grid_p, (my_m + wpb_p - 1) / wpb_p), 32 * wpb_p, A.prune_bytes * wpb_p, st>>>(A);
+            }
+            PK_CHECK_LAUNCH("build_prune_kernel");
         }
-        PK_CHECK_LAUNCH("build_search_kernel");
-        {
-            ProfScope _ps("build_prune_kernel", st);
-            pkk<<<std::min(grid_p, (m + wpb_p - 1) / wpb_p), 32 * wpb_p, A.prune_bytes * wpb_p, st>>>(A);
+        if (sharded && SH.fn(SH.ctx, PK_XCHG_OUTLISTS, chunk, 0) < 0) {
+            set_error("out-list exchange failed");
+            return 4;
         }
-        PK_CHECK_LAUNCH("build_prune_kernel");
+        B.rank = sharded ? SH.rank : 0;
+        B.world = sharded ? SH.world : 1;
         const int ubb = (int)std::min<long long>(n, (long long)m * R);
         PK_CHECK(cudaMemsetAsync(ntargets, 0, sizeof(int), st));
         PK_CHECK(cudaMemsetAsync(nbig, 0, sizeof(int), st));
@@ -831,12 +908,39 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             bigk<<<grid_big, kBigThreads, big_bytes, st>>>(B);
         }
         PK_CHECK_LAUNCH("reverse_big_kernel");
+        if (sharded) {
+            PK_CHECK(cudaMemsetAsync(npack, 0, sizeof(int), st));
+            {
+                ProfScope _ps("pack_rows_kernel", st);
+                pack_rows_kernel<<<grid_for((long long)ubb * 32, 256), 256, 0, st>>>(targets, ntargets, SH.rank, SH.world,
+                                                                                    adj, deg, R, SH.xsend, npack);
+            }
+            PK_CHECK_LAUNCH("pack_rows_kernel");
+            int own = 0;
+            PK_CHECK(cudaMemcpyAsync(&own, npack, sizeof(int), cudaMemcpyDeviceToHost, st));
+            PK_CHECK(cudaStreamSynchronize(st));
+            const long long maxc = SH.fn(SH.ctx, PK_XCHG_ROWS, own, 0);
+            if (maxc < 0) {
+                set_error("row exchange failed");
+                return 4;
+            }
+            if (maxc > 0) {
+                ProfScope _ps("unpack_rows_kernel", st);
+                unpack_rows_kernel<<<grid_for((long long)SH.world * maxc * 32, 256), 256, 0, st>>>(
+                    SH.xrecv, SH.xcnt, (int)maxc, SH.world, SH.rank, R, adj, deg);
+            }
+            PK_CHECK_LAUNCH("unpack_rows_kernel");
+        }
     }
     unsigned herr = 0;
     PK_CHECK(cudaMemcpyAsync(&herr, err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)new_ids, (void*)new_len, (void*)cnt, (void*)tslot,
-                    (void*)targets, (void*)sizes, (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive,
-                    (void*)ntargets, (void*)err, (void*)biglist, (void*)nbig, cub_tmp})
+    if (!multi) {
+        release(new_ids, st);
+        release(new_len, st);
+    }
+    for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
+                    (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
+                    (void*)biglist, (void*)nbig, (void*)npack, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {
@@ -848,13 +952,14 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
 
 template <int MODE>
 int dispatch_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
-                   int* adj, int* deg, long long* stats, int hash_bits, cudaStream_t st) {
-    if (MODE == MODE_SEQ64) return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
+                   int* adj, int* deg, long long* stats, int hash_bits, const Shard& SH, cudaStream_t st) {
+    if (MODE == MODE_SEQ64)
+        return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
     const int qv = MODE == MODE_EXACT_U8 ? (D.dw + 31) / 32 : (D.dp + 127) / 128;
-    if (qv <= 1) return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
-    if (qv <= 2) return run_build<MODE, 2>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
-    if (qv <= 4) return run_build<MODE, 4>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
-    if (qv <= 8) return run_build<MODE, 8>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, st);
+    if (qv <= 1) return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
+    if (qv <= 2) return run_build<MODE, 2>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
+    if (qv <= 4) return run_build<MODE, 4>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
+    if (qv <= 8) return run_build<MODE, 8>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
     set_error("exact integer modes support d <= 1024");
     return 2;
 }
@@ -863,10 +968,10 @@ int dispatch_build(const DataRef& D, int n, int R, int L, double alpha, const in
 
 using namespace pk;
 
-extern "C" int pk_build_vamana(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
-                               int64_t R, int64_t L, double alpha, const int32_t* starts, int64_t s,
-                               const int32_t* order, int32_t* adj_out, int32_t* deg_out, int64_t* stats,
-                               int hash_bits, void* stream) {
+static int build_entry(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode, int64_t R,
+                       int64_t L, double alpha, const int32_t* starts, int64_t s, const int32_t* order,
+                       int32_t* adj_out, int32_t* deg_out, int64_t* stats, int hash_bits, const Shard& SH,
+                       void* stream) {
     cudaStream_t st = as_stream(stream);
     long long* ls = reinterpret_cast<long long*>(stats);
     const DataRef D{x, (int)dp, x8, (int)dw};
@@ -876,12 +981,49 @@ extern "C" int pk_build_vamana(const float* x, int64_t n, int64_t dp, const uint
     }
     if (mode == MODE_EXACT_U8)
         return dispatch_build<MODE_EXACT_U8>(D, (int)n, (int)R, (int)L, alpha, starts, (int)s, order, adj_out, deg_out,
-                                             ls, hash_bits, st);
+                                             ls, hash_bits, SH, st);
     if (mode == MODE_EXACT32)
         return dispatch_build<MODE_EXACT32>(D, (int)n, (int)R, (int)L, alpha, starts, (int)s, order, adj_out, deg_out,
-                                            ls, hash_bits, st);
+                                            ls, hash_bits, SH, st);
     return dispatch_build<MODE_SEQ64>(D, (int)n, (int)R, (int)L, alpha, starts, (int)s, order, adj_out, deg_out, ls,
-                                      hash_bits, st);
+                                      hash_bits, SH, st);
+}
+
+extern "C" int pk_build_vamana(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                               int64_t R, int64_t L, double alpha, const int32_t* starts, int64_t s,
+                               const int32_t* order, int32_t* adj_out, int32_t* deg_out, int64_t* stats,
+                               int hash_bits, void* stream) {
+    return build_entry(x, n, dp, x8, dw, mode, R, L, alpha, starts, s, order, adj_out, deg_out, stats, hash_bits,
+                       Shard{}, stream);
+}
+
+extern "C" int pk_build_vamana_sharded(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw,
+                                       int mode, int64_t R, int64_t L, double alpha, const int32_t* starts, int64_t s,
+                                       const int32_t* order, int32_t* adj_out, int32_t* deg_out, int64_t* stats,
+                                       int hash_bits, int rank, int world, int64_t min_shard,
+                                       pk_exchange_fn exchange, void* ctx, int32_t* xids, int32_t* xlen,
+                                       int32_t* xsend, int32_t* xrecv, int32_t* xcnt, void* stream) {
+    if (world < 1 || rank < 0 || rank >= world) {
+        set_error("invalid rank / world");
+        return 2;
+    }
+    Shard SH;
+    SH.rank = rank;
+    SH.world = world;
+    SH.min_shard = min_shard < 1 ? 1 : min_shard;
+    SH.fn = exchange;
+    SH.ctx = ctx;
+    SH.xids = xids;
+    SH.xlen = xlen;
+    SH.xsend = xsend;
+    SH.xrecv = xrecv;
+    SH.xcnt = xcnt;
+    if (world > 1 && (!exchange || !xids || !xlen || !xsend || !xrecv || !xcnt)) {
+        set_error("sharded build needs the exchange callback and buffers");
+        return 2;
+    }
+    return build_entry(x, n, dp, x8, dw, mode, R, L, alpha, starts, s, order, adj_out, deg_out, stats, hash_bits, SH,
+                       stream);
 }
 
 extern "C" int pk_robust_prune(const float* x, int64_t n, int64_t dp, int64_t p, const int64_t* cand_ids,

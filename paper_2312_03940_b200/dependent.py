@@ -152,9 +152,24 @@ def _resolve_short(p: PointSet, rank_t, short_t, ms: int, kk: int, lam_t, delta_
     return out[:c], c
 
 
-def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: DoublingParams, trace=None):
-    """(lam_t, delta_t) on device; `trace` collects (unresolved, kq) per round."""
+def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: DoublingParams, trace=None,
+                      comm=None):
+    """(lam_t, delta_t) on device; `trace` collects (unresolved, kq) per round.
+    With `comm` every doubling round and the final scan split the sorted
+    unresolved ids across the ranks (shard.py)."""
     import torch
+
+    def mine(t):
+        if comm is None:
+            return t
+        lo, hi = comm.my_range(t.shape[0])
+        return t[lo:hi]
+
+    def regroup(t):
+        if comm is None:
+            return t, t.shape[0]
+        t = torch.sort(comm.all_gather_varlen(t)).values
+        return t, t.shape[0]
 
     n = p.n
     dev = rho_t.device
@@ -166,6 +181,8 @@ def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: D
     top = int(top_t.item())
     all_t = torch.arange(n, dtype=torch.int64, device=dev)
     todo, m, _, _ = _resolve(rank_t, all_t, ids_t, dists_t, lam_t, delta_t, top)
+    if comm is not None:
+        todo = torch.sort(todo).values  # same order on every rank
     if n > 1:
         kdep = params.validated_against(ids_t.shape[1]).initial_k
         if not isinstance(g, BruteForceIndex):
@@ -174,28 +191,38 @@ def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: D
                 kq = min(kdep, n - 1)
                 if trace is not None:
                     trace.append((m, kq))
+                q = mine(todo)
                 if raw is not None:
-                    r_ids, r_sqd, r_cnt = raw(todo, kq)
-                    todo, m, short, ms = _resolve(rank_t, todo, r_ids, sqrt_device(r_sqd), lam_t, delta_t, -1, r_cnt)
+                    r_ids, r_sqd, r_cnt = raw(q, kq)
+                    todo, m, short, ms = _resolve(rank_t, q, r_ids, sqrt_device(r_sqd), lam_t, delta_t, -1, r_cnt)
                     if ms:
                         left, ml = _resolve_short(p, rank_t, short, ms, min(kq, n - 1), lam_t, delta_t)
                         if ml:
                             todo = torch.cat([todo, left])
                             m += ml
                 else:
-                    r_ids, r_sqd = g.knn_batch_device(todo, kq)
-                    todo, m, _, _ = _resolve(rank_t, todo, r_ids, sqrt_device(r_sqd), lam_t, delta_t, -1)
+                    r_ids, r_sqd = g.knn_batch_device(q, kq)
+                    todo, m, _, _ = _resolve(rank_t, q, r_ids, sqrt_device(r_sqd), lam_t, delta_t, -1)
+                if comm is not None:
+                    todo, m = regroup(todo)
                 if kq >= n - 1:
                     break
                 kdep *= 2
     if m > 0:
         if trace is not None:
             trace.append((m, "scan"))
-        sid = torch.empty(m, dtype=torch.int64, device=dev)
-        ssq = torch.empty(m, dtype=torch.float64, device=dev)
-        _lib.call("pk_dp_scan", p.device(), n, p.dp, p.packed(), p.dw, p.mode, rank_t, todo, m, sid, ssq,
-                  _lib.stream())
-        _lib.call("pk_scatter_dependents", todo, m, sid, ssq, lam_t, delta_t, _lib.stream())
+        q = mine(todo)
+        mq = q.shape[0]
+        if mq:
+            sid = torch.empty(mq, dtype=torch.int64, device=dev)
+            ssq = torch.empty(mq, dtype=torch.float64, device=dev)
+            _lib.call("pk_dp_scan", p.device(), n, p.dp, p.packed(), p.dw, p.mode, rank_t, q, mq, sid, ssq,
+                      _lib.stream())
+            _lib.call("pk_scatter_dependents", q, mq, sid, ssq, lam_t, delta_t, _lib.stream())
+    if comm is not None:
+        # each point was resolved by exactly one rank; the others hold -1 / +inf
+        comm.all_reduce(lam_t, "max")
+        comm.all_reduce(delta_t, "min")
     return lam_t, delta_t, rank_t
 
 

@@ -226,9 +226,13 @@ def sample_starts(n: int, num_starts, seed: int, medoid_start: bool, p: PointSet
     return starts, order
 
 
+# batches smaller than this run replicated on every rank of a sharded build
+MIN_SHARD_BATCH = 2048
+
+
 def build_graph_device(p: PointSet, R: int, L_build: int, alpha: float, starts: np.ndarray, order: np.ndarray,
-                       stats=None, order_t=None, starts_t=None):
-    """Run pk_build_vamana; returns (adj_t, deg_t)."""
+                       stats=None, order_t=None, starts_t=None, comm=None):
+    """Run pk_build_vamana (or pk_build_vamana_sharded over `comm`); returns (adj_t, deg_t)."""
     import torch
 
     dev = _lib.device()
@@ -238,8 +242,21 @@ def build_graph_device(p: PointSet, R: int, L_build: int, alpha: float, starts: 
     od = order_t if order_t is not None else _lib.to_dev(order.astype(np.int32))
     if stats is None:
         stats = STATS["build"]
-    _lib.call("pk_build_vamana", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, R, L_build, float(alpha), st, st.shape[0], od, adj,
-              deg, stats, 0, _lib.stream())
+    if comm is None or comm.world == 1:
+        _lib.call("pk_build_vamana", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, R, L_build, float(alpha), st,
+                  st.shape[0], od, adj, deg, stats, 0, _lib.stream())
+        return adj, deg
+    from .shard import BuildExchange
+
+    ex = BuildExchange(comm, p.n, R, dev)
+    try:
+        _lib.call("pk_build_vamana_sharded", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, R, L_build,
+                  float(alpha), st, st.shape[0], od, adj, deg, stats, 0, comm.rank, comm.world, MIN_SHARD_BATCH,
+                  *ex.pointers(), _lib.stream())
+    except RuntimeError:
+        if ex.error is not None:
+            raise ex.error from None
+        raise
     return adj, deg
 
 
@@ -252,6 +269,7 @@ def build_vamana(
     seed: int = 42,
     medoid_start: bool = False,
     query_beam: int | None = None,
+    comm=None,
 ) -> "VamanaIndex":
     """Construct the search graph by batched insertion of doubling size
     (vamana.py:106-172), entirely on the GPU."""
@@ -262,7 +280,7 @@ def build_vamana(
     if alpha < 1.0:
         raise ValueError(f"alpha must be >= 1, got {alpha}")
     starts, order = sample_starts(p.n, num_starts, seed, medoid_start, p)
-    adj, deg = build_graph_device(p, R, L_build, alpha, starts, order)
+    adj, deg = build_graph_device(p, R, L_build, alpha, starts, order, comm=comm)
     graph = GraphIndex.on_device(p, adj, deg, R, starts, float(alpha))
     return VamanaIndex(graph, query_beam if query_beam is not None else L_build)
 
