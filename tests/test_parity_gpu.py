@@ -197,3 +197,36 @@ def test_config_pipelines_golden(tag, name, n, comps, brute):
         w = workloads.WORKLOADS[name]
         idx = pk.build_vamana(pk.PointSet(data), R=w.R, L_build=w.L, alpha=w.alpha, seed=0, query_beam=w.L)
         assert digest(idx.graph.adjacency) == str(z["digest__adj"])
+
+
+def _tc_cases():
+    rng = np.random.default_rng(11)
+    grid = rng.integers(0, 3, size=(2_000, 8)).astype(np.float32)  # heavy exact ties + duplicates
+    gauss = rng.normal(size=(3_000, 40)).astype(np.float32)
+    c5, _ = workloads.generate("C5", n=4_096, components=4)
+    return {"grid": grid, "gauss": gauss, "c5": c5}
+
+
+@pytest.mark.parametrize("case", ["grid", "gauss", "c5"])
+def test_tensor_core_knn_equals_float64_path(case, monkeypatch):
+    """pk_brute_knn_tc (fp16 tcgen05 screening + float64 rescoring + certificate,
+    uncertified rows recomputed) returns exactly the float64 path's rows."""
+    from paper_2312_03940_b200 import index
+
+    data = _tc_cases()[case]
+    p = pk.PointSet(data)
+    q = torch.arange(p.n, dtype=torch.int64, device="cuda")
+    for k in (1, 16, 32):
+        monkeypatch.setenv("PEAKANN_B200_TC", "0")
+        i0, s0 = index.brute_device(p, q, k)
+        monkeypatch.setenv("PEAKANN_B200_TC", "1")
+        before = index.TC_STATS["rows"]
+        i1, s1 = index.brute_device(p, q, k)
+        assert index.TC_STATS["rows"] == before + p.n, "tensor-core path not taken"
+        assert torch.equal(i0, i1), (case, k, int((i0 != i1).any(dim=1).sum()))
+        assert torch.equal(s0, s1), (case, k)
+
+
+def test_c1brute_golden_without_tensor_cores(monkeypatch):
+    monkeypatch.setenv("PEAKANN_B200_TC", "0")
+    test_config_pipelines_golden("c1brute", "C1", 4_000, 10, True)
