@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tc-sample", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     return ap.parse_args()
 
@@ -122,6 +123,49 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- tensor-core sample
+
+
+def brute_tc_sample(n=131_072, k=16, reps=3):
+    """Brute-force exact-mode distance tiles (tensor-core bound):
+    pk_brute_knn_tc over a C5-generator sample (d=1024), all n queries.  Flops
+    = 2 m n d of the screening GEMM; time = tc_screen_kernel's CUDA-event time."""
+    import torch
+
+    import paper_2312_03940_b200 as pk
+    from paper_2312_03940_b200 import _lib, index, workloads
+
+    data, _ = workloads.generate("C5", n=n, components=max(1, n // 1281))
+    p = pk.PointSet(data)
+    q = torch.arange(n, dtype=torch.int64, device="cuda")
+    index.brute_device(p, q[:4096], k)
+    torch.cuda.synchronize()
+    _lib.prof_collect(reset=True)
+    _lib.prof_enable(True)
+    index.TC_STATS.update(rows=0, uncertified=0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        index.brute_device(p, q, k)
+    e1.record()
+    torch.cuda.synchronize()
+    _lib.prof_enable(False)
+    prof = _lib.prof_collect(reset=True)
+    scr_ms = prof["tc_screen_kernel"][1] / reps
+    flops = 2.0 * n * n * 1024
+    _, tflops, kind = peaks()
+    ach = flops / (scr_ms / 1e3) / 1e12
+    del p, data
+    torch.cuda.empty_cache()
+    return {"bound": "tensor", "kernel": "tc_screen_kernel", "achieved": ach, "peak": tflops, "unit": "TFLOP/s",
+            "frac": ach / tflops, "traffic": None, "peak_source": kind,
+            "sample": f"exact kNN (BruteForceIndex path) of all {n} points, C5 generator d=1024, k={k}, fp16 "
+                      f"tcgen05 screening + float64 rescoring",
+            "screen_ms": scr_ms, "call_ms": e0.elapsed_time(e1) / reps,
+            "rescore_ms": prof.get("tc_rescore_kernel", (0, 0.0))[1] / reps,
+            "uncertified_rows": index.TC_STATS["uncertified"] // reps}
 
 
 # ---------------------------------------------------------------------------- CPU baseline
@@ -317,10 +361,12 @@ def main_ours(args):
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_value = n / (float(t_e2e.item()) / args.e2e_steps / 1e3)
 
-    # roofline of the dominant kernel
+    # roofline: the dominant HBM-gather kernel (beam searches)
     hbm, tflops, peak_kind = peaks()
     launches = sum(c for c, _ in prof.values())
-    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    overall = max(prof.items(), key=lambda kv: kv[1][1])
+    gather = {k_: v for k_, v in prof.items() if k_.startswith(("build_search", "beam_knn"))}
+    dom = max(gather.items(), key=lambda kv: kv[1][1])
     dom_name, (dom_cnt, dom_ms) = dom
     bs = _lib.to_host(build_stats) / args.steps
     be = _lib.to_host(beam_stats) / args.steps
@@ -344,6 +390,18 @@ def main_ours(args):
     if alg_bytes is not None:
         achieved = (alg_bytes / 1e9) / (dom_ms / args.steps / 1e3)  # GB/s averaged over the step's launches
 
+    tc = None
+    if rank == 0 and not args.no_tc_sample:
+        try:
+            tc = brute_tc_sample()
+        except Exception as e:  # noqa: BLE001 -- reported, never silently replaced
+            tc = {"error": repr(e)}
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom_name, {}).get("dram_bytes_per_launch")
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, secs, timings = cpu_pipeline(name, args.n)
@@ -359,10 +417,13 @@ def main_ours(args):
             "config": workload_config(name, args.n, world),
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                         "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
                          "peak_source": peak_kind, "algorithmic_bytes_per_step": alg_bytes,
                          "launches_per_step": per_step_launches, "avg_launch_ms": per_launch_ms,
-                         "kernel_share_of_step": dom_ms / args.steps / ms_step, "definition": unit_desc},
+                         "kernel_share_of_step": dom_ms / args.steps / ms_step, "definition": unit_desc,
+                         "largest_kernel_overall": overall[0],
+                         "largest_kernel_share": overall[1][1] / args.steps / ms_step},
+            "roofline_tensor": tc,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches / args.steps) * args.steps,
             "gpu_launches_per_step": launches / args.steps,
