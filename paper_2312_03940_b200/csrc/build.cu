@@ -46,6 +46,8 @@ struct BuildArgs {
     int* new_len;      // [m]
     unsigned* err;
     long long* stats;  // [4]
+    const int* items;  // optional: batch indices to process (overflow of the block prune), count *nitems
+    const int* nitems;
 };
 
 // phase 1: one warp per inserted point searches the adjacency snapshot and
@@ -168,7 +170,9 @@ __global__ void __launch_bounds__(128) build_prune_kernel(BuildArgs A) {
     const MakeAt<MODE, QV> make{A.D};
     long long ev_prune = 0;
     const int R = A.P.R;
-    for (int t = blockIdx.x * wpb + wib; t < A.m; t += gridDim.x * wpb) {
+    const int total = A.items ? *A.nitems : A.m;
+    for (int it = blockIdx.x * wpb + wib; it < total; it += gridDim.x * wpb) {
+        const int t = A.items ? A.items[it] : it;
         const unsigned p = (unsigned)A.bids[t];
         const int vl = A.vlen[t];
         const unsigned* vi = A.vlog_i + (size_t)t * A.vcap;
@@ -500,6 +504,385 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
     if (lane == 0 && A.stats && ev) atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 2), (unsigned long long)ev);
 }
 
+// ---- block-per-item RobustPrune on the integer tensor cores (u8, d = 128) -------------------
+// The sequential RobustPrune (_kernels.py:283-315) only ever asks "does pick t
+// occlude candidate u": alpha^2 * d(t, u) <= d(p, u).  For the sorted,
+// de-duplicated candidates of one item every such bit is computed up front:
+// d(t, u) = |t|^2 + |u|^2 - 2 t.u with the dot products of all pairs t < u from
+// exact u8 x u8 -> s32 mma.sync tiles (16 x 8 x 32), the occlusion bits packed
+// per row; the greedy pass is then bit arithmetic (alive &= ~kill[t]).  The
+// picks are identical to the sequential algorithm: the kill decision for (t, u)
+// depends only on the pair and on t being picked.
+constexpr int BP_CAP = 256;      // candidates per item (more -> warp path / big-group path)
+constexpr int BP_THREADS = 128;
+
+struct BPSmem {
+    unsigned* rows;   // [BP_CAP][32] u8 rows in sorted order, 16-byte chunks XOR-swizzled by (row & 7)
+    unsigned* nrm;    // [BP_CAP] |row|^2
+    double* kd;       // [BP_CAP] candidate keys (input order, then bitonic-sorted)
+    unsigned* ki;
+    double* kd2;      // [BP_CAP] de-duplicated, sorted
+    unsigned* ki2;
+    unsigned* kill;   // [BP_CAP][8] occlusion bits: bit u of row t = t occludes u
+    int* scal;        // [16] block scalars
+};
+
+__host__ __device__ constexpr size_t bp_smem_bytes() {
+    return (size_t)BP_CAP * 32 * 4 + BP_CAP * 4 + BP_CAP * 8 * 2 + BP_CAP * 4 * 2 + BP_CAP * 32 + 16 * 4 + 16;
+}
+
+__device__ __forceinline__ BPSmem carve_bp(unsigned char* base) {
+    BPSmem S;
+    S.rows = reinterpret_cast<unsigned*>(base);
+    S.kd = reinterpret_cast<double*>(base + (size_t)BP_CAP * 128);
+    S.kd2 = S.kd + BP_CAP;
+    S.nrm = reinterpret_cast<unsigned*>(S.kd2 + BP_CAP);
+    S.ki = S.nrm + BP_CAP;
+    S.ki2 = S.ki + BP_CAP;
+    S.kill = S.ki2 + BP_CAP;
+    S.scal = reinterpret_cast<int*>(S.kill + BP_CAP * 8);
+    return S;
+}
+
+__device__ __forceinline__ int bp_swz(int r, int w) { return r * 32 + (w ^ ((r & 7) << 2)); }
+
+// exact |a - b|^2 of a global u8 row against a register row (dot-product form)
+__device__ __forceinline__ unsigned bp_dist_global(const uint4 (&q)[8], unsigned nq, const unsigned* row) {
+    uint4 r[8];
+    const uint4* v = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = __ldg(v + i);
+    unsigned n0 = 0u, n1 = 0u, d0 = 0u, d1 = 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        n0 = __dp4a(r[i].x, r[i].x, n0);
+        n1 = __dp4a(r[i].y, r[i].y, n1);
+        n0 = __dp4a(r[i].z, r[i].z, n0);
+        n1 = __dp4a(r[i].w, r[i].w, n1);
+        d0 = __dp4a(q[i].x, r[i].x, d0);
+        d1 = __dp4a(q[i].y, r[i].y, d1);
+        d0 = __dp4a(q[i].z, r[i].z, d0);
+        d1 = __dp4a(q[i].w, r[i].w, d1);
+    }
+    return nq + (n0 + n1) - 2u * (d0 + d1);
+}
+
+// block bitonic sort of (kd, ki)[0, P) by (dist, id); P a power of two
+__device__ __forceinline__ void bp_sort(double* kd, unsigned* ki, int P) {
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += BP_THREADS) {
+                const int x = i ^ j;
+                if (x > i) {
+                    const double a = kd[i], b = kd[x];
+                    const unsigned ia = ki[i], ib = ki[x];
+                    if (key_lt(b, ib, a, ia) == ((i & k) == 0)) {
+                        kd[i] = b;
+                        kd[x] = a;
+                        ki[i] = ib;
+                        ki[x] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// drop `self` and repeated (dist, id) entries, keep order -> kd2/ki2; returns the count
+__device__ __forceinline__ int bp_unique(const BPSmem& S, int c, unsigned self) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // thread tid owns positions 2 tid and 2 tid + 1 (c <= 256)
+    bool keep[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int i = 2 * tid + e;
+        keep[e] = false;
+        if (i < c) {
+            const unsigned id = S.ki[i];
+            keep[e] = id != self && !(i > 0 && S.ki[i - 1] == id && S.kd[i - 1] == S.kd[i]);
+        }
+    }
+    const int mine = (int)keep[0] + (int)keep[1];
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(PK_FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) S.scal[wid] = incl;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < wid; ++w) base += S.scal[w];
+    const int total = S.scal[0] + S.scal[1] + S.scal[2] + S.scal[3];
+    int o = base + incl - mine;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+        if (keep[e]) {
+            S.kd2[o] = S.kd[2 * tid + e];
+            S.ki2[o] = S.ki[2 * tid + e];
+            ++o;
+        }
+    __syncthreads();
+    return total;
+}
+
+__device__ __forceinline__ void bp_mma(const unsigned (&a)[4], const unsigned (&b)[2], int (&d)[4]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+__device__ __forceinline__ unsigned bp_spread4(unsigned x) {
+    return (x & 1u) | ((x & 2u) << 1) | ((x & 4u) << 2) | ((x & 8u) << 3);
+}
+
+// RobustPrune of the c sorted unique candidates kd2/ki2 (c > R) -> out[0, sel); returns sel
+__device__ int bp_prune(const unsigned* __restrict__ X8, const BPSmem& S, int c, double alpha2, int R, int* out,
+                        long long* pairs) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // stage the rows in sorted order (cp.async, 16-byte chunks, swizzled), clear the bits
+    for (int e = tid; e < c * 8; e += BP_THREADS) {
+        const int x = e >> 3, ch = e & 7;
+        const unsigned* src = X8 + (size_t)S.ki2[x] * 32 + ch * 4;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(S.rows + x * 32 + ((ch ^ (x & 7)) << 2));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    for (int e = tid; e < c * 8; e += BP_THREADS) S.kill[e] = 0u;
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    for (int x = tid; x < c; x += BP_THREADS) {
+        unsigned n0 = 0u, n1 = 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(S.rows + x * 32 + ((q ^ (x & 7)) << 2));
+            n0 = __dp4a(v.x, v.x, n0);
+            n1 = __dp4a(v.y, v.y, n1);
+            n0 = __dp4a(v.z, v.z, n0);
+            n1 = __dp4a(v.w, v.w, n1);
+        }
+        S.nrm[x] = n0 + n1;
+    }
+    __syncthreads();
+    // occlusion bits of all pairs t < u: 16-row tiles (snake-assigned to warps) x 8-column tiles
+    const int T = (c + 15) >> 4, U = (c + 7) >> 3;
+    const int g = lane >> 2, tig = lane & 3;
+    for (int i0 = 0; i0 < T; i0 += 4) {
+        const int i = ((i0 >> 2) & 1) ? i0 + 3 - wid : i0 + wid;
+        if (i >= T) continue;
+        const int t0 = 16 * i + g, t1 = t0 + 8;
+        const int r0 = min(t0, c - 1), r1 = min(t1, c - 1);
+        unsigned a[4][4];
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            a[ks][0] = S.rows[bp_swz(r0, ks * 8 + tig)];
+            a[ks][1] = S.rows[bp_swz(r1, ks * 8 + tig)];
+            a[ks][2] = S.rows[bp_swz(r0, ks * 8 + 4 + tig)];
+            a[ks][3] = S.rows[bp_swz(r1, ks * 8 + 4 + tig)];
+        }
+        const int n0 = (int)S.nrm[r0], n1 = (int)S.nrm[r1];
+        for (int j = 2 * i; j < U; ++j) {
+            const int rb = min(8 * j + g, c - 1);
+            int d[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const unsigned b[2] = {S.rows[bp_swz(rb, ks * 8 + tig)], S.rows[bp_swz(rb, ks * 8 + 4 + tig)]};
+                bp_mma(a[ks], b, d);
+            }
+            const int u0 = 8 * j + 2 * tig, u1 = u0 + 1;
+            const int m0 = (int)S.nrm[min(u0, c - 1)], m1 = (int)S.nrm[min(u1, c - 1)];
+            const double k0 = S.kd2[min(u0, c - 1)], k1 = S.kd2[min(u1, c - 1)];
+            const bool v0 = u0 < c, v1 = u1 < c;
+            const bool k00 = v0 && u0 > t0 && alpha2 * (double)(n0 + m0 - 2 * d[0]) <= k0;
+            const bool k01 = v1 && u1 > t0 && alpha2 * (double)(n0 + m1 - 2 * d[1]) <= k1;
+            const bool k10 = v0 && u0 > t1 && alpha2 * (double)(n1 + m0 - 2 * d[2]) <= k0;
+            const bool k11 = v1 && u1 > t1 && alpha2 * (double)(n1 + m1 - 2 * d[3]) <= k1;
+            const unsigned b00 = __ballot_sync(PK_FULL, k00), b01 = __ballot_sync(PK_FULL, k01);
+            const unsigned b10 = __ballot_sync(PK_FULL, k10), b11 = __ballot_sync(PK_FULL, k11);
+            if (lane < 16) {
+                const int r = lane & 7;
+                const unsigned e0 = lane < 8 ? b00 : b10, e1 = lane < 8 ? b01 : b11;
+                const unsigned byte = bp_spread4((e0 >> (4 * r)) & 15u) | (bp_spread4((e1 >> (4 * r)) & 15u) << 1);
+                const int t = 16 * i + lane;
+                if (t < c) reinterpret_cast<unsigned char*>(S.kill)[t * 32 + j] = (unsigned char)byte;
+            }
+        }
+    }
+    __syncthreads();
+    // greedy picks (warp 0): first alive, then alive &= ~kill[pick]
+    if (wid == 0) {
+        unsigned alive = 0u;
+        if (lane < 8) {
+            const int lo = 32 * lane;
+            alive = c >= lo + 32 ? 0xffffffffu : (c > lo ? (1u << (c - lo)) - 1u : 0u);
+        }
+        int sel = 0;
+        while (sel < R) {
+            const unsigned nz = __ballot_sync(PK_FULL, alive != 0u);
+            if (!nz) break;
+            const int w = __ffs(nz) - 1;
+            const unsigned word = __shfl_sync(PK_FULL, alive, w);
+            const int t = 32 * w + __ffs(word) - 1;
+            if (lane == 0) out[sel] = (int)S.ki2[t];
+            ++sel;
+            if (lane < 8) alive &= ~S.kill[t * 8 + lane];
+            if (lane == w) alive &= ~(1u << (t & 31));
+        }
+        if (lane == 0) {
+            S.scal[8] = sel;
+            if (pairs) *pairs += (long long)c * (c - 1) / 2;
+        }
+    }
+    __syncthreads();
+    return S.scal[8];
+}
+
+// build phase 2 for u8 rows (d = 128): one block per inserted point; items with
+// more than BP_CAP candidates are queued for build_prune_kernel
+__global__ void __launch_bounds__(BP_THREADS) build_prune_block_kernel(BuildArgs A, int* over, int* nover) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const BPSmem S = carve_bp(smem);
+    const int tid = threadIdx.x;
+    const int R = A.P.R;
+    long long pairs = 0;
+    for (int t = blockIdx.x; t < A.m; t += gridDim.x) {
+        const unsigned p = (unsigned)A.bids[t];
+        const int vl = A.vlen[t];
+        const int nd = __ldg(A.P.deg + p);
+        const int c0 = vl + nd;
+        if (c0 > BP_CAP) {
+            if (tid == 0) over[atomicAdd(nover, 1)] = t;
+            continue;
+        }
+        const unsigned* vi = A.vlog_i + (size_t)t * A.vcap;
+        const double* vd = A.vlog_d + (size_t)t * A.vcap;
+        const int* row = A.P.adj + (size_t)p * R;
+        uint4 q[8];
+        const uint4* qv = reinterpret_cast<const uint4*>(A.D.X8 + (size_t)p * 32);
+        unsigned nq0 = 0u, nq1 = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            q[i] = __ldg(qv + i);
+            nq0 = __dp4a(q[i].x, q[i].x, nq0);
+            nq1 = __dp4a(q[i].y, q[i].y, nq1);
+            nq0 = __dp4a(q[i].z, q[i].z, nq0);
+            nq1 = __dp4a(q[i].w, q[i].w, nq1);
+        }
+        const unsigned nq = nq0 + nq1;
+        // candidates in input order: visit log (distances known), then the current out-row
+        for (int x = tid; x < c0; x += BP_THREADS) {
+            if (x < vl) {
+                S.kd[x] = vd[x];
+                S.ki[x] = vi[x];
+            } else {
+                const unsigned id = (unsigned)__ldg(row + x - vl);
+                S.ki[x] = id;
+                S.kd[x] = (double)bp_dist_global(q, nq, A.D.X8 + (size_t)id * 32);
+            }
+        }
+        const int P = next_pow2_dev(c0 < 2 ? 2 : c0);
+        for (int x = c0 + tid; x < P; x += BP_THREADS) {
+            S.kd[x] = __longlong_as_double(0x7ff0000000000000LL);
+            S.ki[x] = 0xffffffffu;
+        }
+        __syncthreads();
+        bp_sort(S.kd, S.ki, P);
+        const int c = bp_unique(S, c0, p);
+        int* out = A.new_ids + (size_t)t * R;
+        int sel = c;
+        if (c <= R) {
+            for (int x = tid; x < c; x += BP_THREADS) out[x] = (int)S.ki2[x];
+        } else {
+            sel = bp_prune(A.D.X8, S, c, A.alpha2, R, out, &pairs);
+        }
+        for (int x = sel + tid; x < R; x += BP_THREADS) out[x] = -1;
+        if (tid == 0) A.new_len[t] = sel;
+        __syncthreads();
+    }
+    if (tid == 0 && A.stats && pairs)
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 1), (unsigned long long)pairs);
+}
+
+// reverse-edge re-prune for u8 rows (d = 128): one block per target vertex
+// (groups above BP_CAP go to reverse_big_kernel / the selection path as in
+// reverse_kernel)
+template <int MODE, int QV>
+__global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const BPSmem S = carve_bp(smem);
+    const int tid = threadIdx.x, wid = tid >> 5;
+    const MakeAt<MODE, QV> make{A.D};
+    const int nt = *A.ntargets;
+    long long ev = 0;
+    for (int s = blockIdx.x; s < nt; s += gridDim.x) {
+        const unsigned u = (unsigned)A.targets[s];
+        if (A.world > 1 && (int)(u % (unsigned)A.world) != A.rank) {
+            if (tid == 0) A.cnt[u] = 0;
+            continue;
+        }
+        const int nd = A.deg[u];
+        const int off = A.offs[s];
+        const int size = A.sizes[s];
+        int* row = A.adj + (size_t)u * A.R;
+        const int c0 = nd + size;
+        int sel;
+        if (c0 > BP_CAP) {
+            if (c0 <= A.capB) {
+                if (tid == 0) A.biglist[atomicAdd(A.nbig, 1)] = s;
+                continue;
+            }
+            if (wid == 0) {
+                sel = prune_by_selection(A, u, make, S.kd, S.ki, reinterpret_cast<unsigned char*>(S.rows), S.nrm, nd,
+                                         off, size, row, &ev);
+                if (lane_id() == 0) S.scal[9] = sel;
+            }
+            __syncthreads();
+            sel = S.scal[9];
+        } else {
+            uint4 q[8];
+            const uint4* qv = reinterpret_cast<const uint4*>(A.D.X8 + (size_t)u * 32);
+            unsigned nq0 = 0u, nq1 = 0u;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                q[i] = __ldg(qv + i);
+                nq0 = __dp4a(q[i].x, q[i].x, nq0);
+                nq1 = __dp4a(q[i].y, q[i].y, nq1);
+                nq0 = __dp4a(q[i].z, q[i].z, nq0);
+                nq1 = __dp4a(q[i].w, q[i].w, nq1);
+            }
+            const unsigned nq = nq0 + nq1;
+            for (int x = tid; x < c0; x += BP_THREADS) {
+                const unsigned id = x < nd ? (unsigned)row[x] : (unsigned)A.adds[off + x - nd];
+                S.ki[x] = id;
+                S.kd[x] = (double)bp_dist_global(q, nq, A.D.X8 + (size_t)id * 32);
+            }
+            const int P = next_pow2_dev(c0 < 2 ? 2 : c0);
+            for (int x = c0 + tid; x < P; x += BP_THREADS) {
+                S.kd[x] = __longlong_as_double(0x7ff0000000000000LL);
+                S.ki[x] = 0xffffffffu;
+            }
+            __syncthreads();
+            bp_sort(S.kd, S.ki, P);
+            const int c = bp_unique(S, c0, u);
+            if (tid == 0) ev += c0;
+            if (c <= A.R) {
+                for (int x = tid; x < c; x += BP_THREADS) row[x] = (int)S.ki2[x];
+                sel = c;
+            } else {
+                sel = bp_prune(A.D.X8, S, c, A.alpha2, A.R, row, &ev);
+            }
+        }
+        for (int x = sel + tid; x < A.R; x += BP_THREADS) row[x] = -1;
+        if (tid == 0) {
+            A.deg[u] = sel;
+            A.cnt[u] = 0;
+        }
+        __syncthreads();
+    }
+    if (tid == 0 && A.stats && ev) atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 2), (unsigned long long)ev);
+}
+
 // one thread, one full distance between two point ids (exact in every mode)
 template <int MODE>
 __device__ __forceinline__ double thread_dist(const DataRef& D, unsigned a, unsigned b) {
@@ -746,6 +1129,19 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     if ((rc = config_kernel(pkk, A.prune_bytes, 2, &wpb_p, &grid_p))) return rc;
     const size_t wbr = cand_smem_bytes(capR, D.dw, SR, u8);
     if ((rc = config_kernel(rk, wbr, 2, &wpb_r, &grid_r))) return rc;
+    // u8 rows of d = 128: block-per-item RobustPrune on the integer tensor cores
+    const bool blockp = MODE == MODE_EXACT_U8 && D.dw == 32 && env_int("PK_BLOCK_PRUNE", 1) == 1;
+    auto bpk = build_prune_block_kernel;
+    auto rbk = reverse_block_kernel<MODE, QV>;
+    int grid_bp = 0;
+    if (blockp) {
+        const int bytes = (int)bp_smem_bytes();
+        PK_CHECK(cudaFuncSetAttribute(bpk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        PK_CHECK(cudaFuncSetAttribute(rbk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        int per_sm = 0;
+        PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bpk, BP_THREADS, bytes));
+        grid_bp = sm_count() * std::max(1, per_sm);
+    }
     const int capB = 8192;
     const size_t big_bytes = (size_t)capB * 13 + 16;
     auto bigk = reverse_big_kernel<MODE>;
@@ -778,6 +1174,9 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     }
     int* npack = nullptr;
     PK_CHECK(scratch(&npack, 1, st));
+    int *over = nullptr, *nover = nullptr;
+    PK_CHECK(scratch(&over, (size_t)mb, st));
+    PK_CHECK(scratch(&nover, 1, st));
     PK_CHECK(scratch(&cnt, (size_t)n, st));
     PK_CHECK(scratch(&tslot, (size_t)n, st));
     PK_CHECK(scratch(&targets, (size_t)ub, st));
@@ -816,6 +1215,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.new_len = new_len;
     A.err = err;
     A.stats = stats;
+    A.items = nullptr;
+    A.nitems = nullptr;
 
     RevArgs B;
     B.X = D.X;
@@ -860,7 +1261,22 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                 sk<<<std::min(grid_s, (my_m + wpb_s - 1) / wpb_s), 32 * wpb_s, A.search_bytes * wpb_s, st>>>(A);
             }
             PK_CHECK_LAUNCH("build_search_kernel");
-            {
+            if (blockp) {
+                PK_CHECK(cudaMemsetAsync(nover, 0, sizeof(int), st));
+                {
+                    ProfScope _ps("build_prune_block_kernel", st);
+                    bpk<<<std::min(grid_bp, my_m), BP_THREADS, bp_smem_bytes(), st>>>(A, over, nover);
+                }
+                PK_CHECK_LAUNCH("build_prune_block_kernel");
+                A.items = over;  // the few items with more than BP_CAP candidates
+                A.nitems = nover;
+                {
+                    ProfScope _ps("build_prune_kernel", st);
+                    pkk<<<std::min(grid_p, sm_count()), 32 * wpb_p, A.prune_bytes * wpb_p, st>>>(A);
+                }
+                A.items = nullptr;
+                A.nitems = nullptr;
+            } else {
                 ProfScope _ps("build_prune_kernel", st);
                 pkk<<<std::min(grid_p, (my_m + wpb_p - 1) / wpb_p), 32 * wpb_p, A.prune_bytes * wpb_p, st>>>(A);
             }
@@ -898,7 +1314,10 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                                                                              offs, fill, adds);
         }
         PK_CHECK_LAUNCH("scatter_kernel");
-        {
+        if (blockp) {
+            ProfScope _ps("reverse_block_kernel", st);
+            rbk<<<std::min(grid_bp, ubb), BP_THREADS, bp_smem_bytes(), st>>>(B);
+        } else {
             ProfScope _ps("reverse_kernel", st);
             rk<<<std::min(grid_r, (ubb + wpb_r - 1) / wpb_r), 32 * wpb_r, wbr * wpb_r, st>>>(B);
         }
@@ -940,7 +1359,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     }
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
-                    (void*)biglist, (void*)nbig, (void*)npack, cub_tmp})
+                    (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

@@ -1,39 +1,24 @@
-"""One C2 pipeline pass for profilers (ncu): no warm-up, no CPU baseline.
+"""One C2 pipeline step (after one untimed warm-up) for ncu captures.
 
-    python tools/profile_step.py [--config C2] [--n N] [--runs R]
+    ncu --metrics gpu__time_duration.sum --clock-control none --csv python tools/profile_step.py
+    ncu --set full -k regex:build_search -s 33 -c 1 python tools/profile_step.py   # largest batch, 2nd run
 """
-import argparse
 import os
 import sys
 
+import torch
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import paper_2312_03940_b200 as pk  # noqa: E402
+from paper_2312_03940_b200 import workloads  # noqa: E402
+from paper_2312_03940_b200.cluster import run_pipeline_device  # noqa: E402
 
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--n", type=int, default=None)
-    ap.add_argument("--runs", type=int, default=1)
-    a = ap.parse_args()
-    import torch
-
-    import paper_2312_03940_b200 as pk
-    from paper_2312_03940_b200 import workloads
-    from paper_2312_03940_b200.cluster import run_pipeline_device
-    from paper_2312_03940_b200.core import upload_points
-
-    w = workloads.WORKLOADS[a.config]
-    n = a.n or w.n
-    comps = w.components if a.n is None else max(1, int(round(w.components * n / w.n)))
-    data, _ = workloads.generate(a.config, n=n, components=comps)
-    p = pk.PointSet(data).attach_device(upload_points(data))
-    kw = workloads.pipeline_args(a.config, pk, n_centers=min(w.n_centers, comps))
-    for _ in range(a.runs):
-        out = run_pipeline_device(p, **kw)
-    torch.cuda.synchronize()
-    print({k: round(v * 1e3, 2) for k, v in out["timings"].items()})
-
-
-if __name__ == "__main__":
-    main()
+name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+data, _ = workloads.generate(name)
+kw = workloads.pipeline_args(name, pk)
+p = pk.PointSet(data)
+for _ in range(2):
+    out = run_pipeline_device(p, **kw)
+torch.cuda.synchronize()
+print({k: round(v * 1e3, 2) for k, v in out["timings"].items()})
