@@ -11,6 +11,7 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+    by = 1 if len(sys.argv) > 3 and sys.argv[3] == "inst" else 0
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -35,7 +36,7 @@ def main():
     ts = sum(v[0] for v in agg.values()) or 1
     ti = sum(v[1] for v in agg.values()) or 1
     print(f"total stall samples {ts:.0f}, instructions {ti:.3e}")
-    for (f, ln), (st, ins, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    for (f, ln), (st, ins, src) in sorted(agg.items(), key=lambda kv: -kv[1][by])[:top]:
         print(f"{st / ts * 100:5.1f}% {ins / ti * 100:5.1f}%  {f}:{ln:<4d} {src}")
 
 
