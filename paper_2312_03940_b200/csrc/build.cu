@@ -527,20 +527,21 @@ struct BPSmem {
     int* scal;        // [16] block scalars
 };
 
-__host__ __device__ constexpr size_t bp_smem_bytes() {
-    return (size_t)BP_CAP * 32 * 4 + BP_CAP * 4 + BP_CAP * 8 * 2 + BP_CAP * 4 * 2 + BP_CAP * 32 + 16 * 4 + 16;
+// shared memory of one item with room for `cap` (<= BP_CAP) candidates
+__host__ __device__ constexpr size_t bp_smem_bytes(int cap) {
+    return (size_t)cap * 32 * 4 + cap * 4 + cap * 8 * 2 + cap * 4 * 2 + cap * 32 + 16 * 4 + 16;
 }
 
-__device__ __forceinline__ BPSmem carve_bp(unsigned char* base) {
+__device__ __forceinline__ BPSmem carve_bp(unsigned char* base, int cap) {
     BPSmem S;
     S.rows = reinterpret_cast<unsigned*>(base);
-    S.kd = reinterpret_cast<double*>(base + (size_t)BP_CAP * 128);
-    S.kd2 = S.kd + BP_CAP;
-    S.nrm = reinterpret_cast<unsigned*>(S.kd2 + BP_CAP);
-    S.ki = S.nrm + BP_CAP;
-    S.ki2 = S.ki + BP_CAP;
-    S.kill = S.ki2 + BP_CAP;
-    S.scal = reinterpret_cast<int*>(S.kill + BP_CAP * 8);
+    S.kd = reinterpret_cast<double*>(base + (size_t)cap * 128);
+    S.kd2 = S.kd + cap;
+    S.nrm = reinterpret_cast<unsigned*>(S.kd2 + cap);
+    S.ki = S.nrm + cap;
+    S.ki2 = S.ki + cap;
+    S.kill = S.ki2 + cap;
+    S.scal = reinterpret_cast<int*>(S.kill + cap * 8);
     return S;
 }
 
@@ -742,7 +743,7 @@ __device__ int bp_prune(const unsigned* __restrict__ X8, const BPSmem& S, int c,
 // more than BP_CAP candidates are queued for build_prune_kernel
 __global__ void __launch_bounds__(BP_THREADS) build_prune_block_kernel(BuildArgs A, int* over, int* nover) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const BPSmem S = carve_bp(smem);
+    const BPSmem S = carve_bp(smem, BP_CAP);
     const int tid = threadIdx.x;
     const int R = A.P.R;
     long long pairs = 0;
@@ -807,15 +808,19 @@ __global__ void __launch_bounds__(BP_THREADS) build_prune_block_kernel(BuildArgs
 // reverse-edge re-prune for u8 rows (d = 128): one block per target vertex
 // (groups above BP_CAP go to reverse_big_kernel / the selection path as in
 // reverse_kernel)
+// cap = candidate room of this launch: groups with cap < c0 <= BP_CAP are queued
+// on (mid, nmid) for a second launch with cap = BP_CAP over items = mid.
 template <int MODE, int QV>
-__global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A) {
+__global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A, int cap, const int* items,
+                                                                   const int* nitems, int* mid, int* nmid) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const BPSmem S = carve_bp(smem);
+    const BPSmem S = carve_bp(smem, cap);
     const int tid = threadIdx.x, wid = tid >> 5;
     const MakeAt<MODE, QV> make{A.D};
-    const int nt = *A.ntargets;
+    const int nt = items ? *nitems : *A.ntargets;
     long long ev = 0;
-    for (int s = blockIdx.x; s < nt; s += gridDim.x) {
+    for (int it = blockIdx.x; it < nt; it += gridDim.x) {
+        const int s = items ? items[it] : it;
         const unsigned u = (unsigned)A.targets[s];
         if (A.world > 1 && (int)(u % (unsigned)A.world) != A.rank) {
             if (tid == 0) A.cnt[u] = 0;
@@ -827,6 +832,10 @@ __global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A) {
         int* row = A.adj + (size_t)u * A.R;
         const int c0 = nd + size;
         int sel;
+        if (c0 > cap && c0 <= BP_CAP) {
+            if (tid == 0) mid[atomicAdd(nmid, 1)] = s;
+            continue;
+        }
         if (c0 > BP_CAP) {
             if (c0 <= A.capB) {
                 if (tid == 0) A.biglist[atomicAdd(A.nbig, 1)] = s;
@@ -1133,14 +1142,17 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     const bool blockp = MODE == MODE_EXACT_U8 && D.dw == 32 && env_int("PK_BLOCK_PRUNE", 1) == 1;
     auto bpk = build_prune_block_kernel;
     auto rbk = reverse_block_kernel<MODE, QV>;
-    int grid_bp = 0;
+    int grid_bp = 0, grid_rb = 0;
+    constexpr int kRevCap = 128;  // most reverse groups (row + this batch's sources) fit 128
     if (blockp) {
-        const int bytes = (int)bp_smem_bytes();
+        const int bytes = (int)bp_smem_bytes(BP_CAP);
         PK_CHECK(cudaFuncSetAttribute(bpk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         PK_CHECK(cudaFuncSetAttribute(rbk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         int per_sm = 0;
         PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bpk, BP_THREADS, bytes));
         grid_bp = sm_count() * std::max(1, per_sm);
+        PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbk, BP_THREADS, bp_smem_bytes(kRevCap)));
+        grid_rb = sm_count() * std::max(1, per_sm);
     }
     const int capB = 8192;
     const size_t big_bytes = (size_t)capB * 13 + 16;
@@ -1177,6 +1189,9 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     int *over = nullptr, *nover = nullptr;
     PK_CHECK(scratch(&over, (size_t)mb, st));
     PK_CHECK(scratch(&nover, 1, st));
+    int *midl = nullptr, *nmid = nullptr;
+    PK_CHECK(scratch(&midl, (size_t)ub, st));
+    PK_CHECK(scratch(&nmid, 1, st));
     PK_CHECK(scratch(&cnt, (size_t)n, st));
     PK_CHECK(scratch(&tslot, (size_t)n, st));
     PK_CHECK(scratch(&targets, (size_t)ub, st));
@@ -1265,7 +1280,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                 PK_CHECK(cudaMemsetAsync(nover, 0, sizeof(int), st));
                 {
                     ProfScope _ps("build_prune_block_kernel", st);
-                    bpk<<<std::min(grid_bp, my_m), BP_THREADS, bp_smem_bytes(), st>>>(A, over, nover);
+                    bpk<<<std::min(grid_bp, my_m), BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(A, over, nover);
                 }
                 PK_CHECK_LAUNCH("build_prune_block_kernel");
                 A.items = over;  // the few items with more than BP_CAP candidates
@@ -1315,8 +1330,17 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         }
         PK_CHECK_LAUNCH("scatter_kernel");
         if (blockp) {
-            ProfScope _ps("reverse_block_kernel", st);
-            rbk<<<std::min(grid_bp, ubb), BP_THREADS, bp_smem_bytes(), st>>>(B);
+            PK_CHECK(cudaMemsetAsync(nmid, 0, sizeof(int), st));
+            {
+                ProfScope _ps("reverse_block_kernel", st);
+                rbk<<<std::min(grid_rb, ubb), BP_THREADS, bp_smem_bytes(kRevCap), st>>>(B, kRevCap, nullptr, nullptr,
+                                                                                       midl, nmid);
+            }
+            PK_CHECK_LAUNCH("reverse_block_kernel");
+            {
+                ProfScope _ps("reverse_block_kernel", st);
+                rbk<<<grid_bp, BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(B, BP_CAP, midl, nmid, nullptr, nullptr);
+            }
         } else {
             ProfScope _ps("reverse_kernel", st);
             rk<<<std::min(grid_r, (ubb + wpb_r - 1) / wpb_r), 32 * wpb_r, wbr * wpb_r, st>>>(B);
@@ -1359,7 +1383,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     }
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
-                    (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, cub_tmp})
+                    (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
+                    (void*)nmid, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {
