@@ -711,24 +711,36 @@ __device__ int bp_prune(const unsigned* __restrict__ X8, const BPSmem& S, int c,
         }
     }
     __syncthreads();
-    // greedy picks (warp 0): first alive, then alive &= ~kill[pick]
+    // greedy picks (warp 0), 32 candidates (one bit word) at a time: lane j holds
+    // candidate 32w + j's occlusion word w, so a pick inside the word is an ffs + a
+    // shuffle; the word's picks then clear their bits in later words (OR-reduce)
     if (wid == 0) {
-        unsigned alive = 0u;
-        if (lane < 8) {
-            const int lo = 32 * lane;
-            alive = c >= lo + 32 ? 0xffffffffu : (c > lo ? (1u << (c - lo)) - 1u : 0u);
-        }
+        const int nw = (c + 31) >> 5;
+        unsigned acc = 0u;  // lane v: bits of word v occluded by the picks so far
         int sel = 0;
-        while (sel < R) {
-            const unsigned nz = __ballot_sync(PK_FULL, alive != 0u);
-            if (!nz) break;
-            const int w = __ffs(nz) - 1;
-            const unsigned word = __shfl_sync(PK_FULL, alive, w);
-            const int t = 32 * w + __ffs(word) - 1;
-            if (lane == 0) out[sel] = (int)S.ki2[t];
-            ++sel;
-            if (lane < 8) alive &= ~S.kill[t * 8 + lane];
-            if (lane == w) alive &= ~(1u << (t & 31));
+        for (int w = 0; w < nw && sel < R; ++w) {
+            const int x = 32 * w + lane;
+            const int left = c - 32 * w;
+            const unsigned valid = left >= 32 ? 0xffffffffu : (1u << left) - 1u;
+            unsigned alive = valid & ~__shfl_sync(PK_FULL, acc, w);
+            const unsigned kw = x < c ? S.kill[x * 8 + w] : 0u;
+            const int sel0 = sel;
+            unsigned picked = 0u;
+            while (alive && sel < R) {
+                const int j = __ffs(alive) - 1;
+                picked |= 1u << j;
+                ++sel;
+                alive &= ~(1u << j);
+                alive &= ~__shfl_sync(PK_FULL, kw, j);
+            }
+            const bool mine = (picked >> lane) & 1u;
+            if (mine) out[sel0 + __popc(picked & ((1u << lane) - 1u))] = (int)S.ki2[x];
+            if (sel < R) {
+                for (int v = w + 1; v < nw; ++v) {
+                    const unsigned r = __reduce_or_sync(PK_FULL, mine ? S.kill[x * 8 + v] : 0u);
+                    if (lane == v) acc |= r;
+                }
+            }
         }
         if (lane == 0) {
             S.scal[8] = sel;

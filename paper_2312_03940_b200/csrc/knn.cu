@@ -316,6 +316,7 @@ int grid_for(long long work, int block) {
 // ---- launch helpers --------------------------------------------------------------------------
 int choose_hash(int L, int hash_bits, long long n) {
     int h;
+    if (hash_bits <= 0) hash_bits = env_int("PK_HASH_BITS", 0);  // tuning override
     if (hash_bits > 0) {
         h = 1 << hash_bits;
     } else {
