@@ -152,6 +152,14 @@ int pk_build_vamana_sharded(const float* x, int64_t n, int64_t dp, const uint32_
                             int64_t min_shard, pk_exchange_fn exchange, void* ctx, int32_t* xids,
                             int32_t* xlen, int32_t* xsend, int32_t* xrecv, int32_t* xcnt, void* stream);
 
+/* Host helper (no device work): numpy's Generator.permutation(n) on a PCG64
+ * stream given as state = {state_hi, state_lo, inc_hi, inc_lo} plus the
+ * buffered 32-bit half (has_uint32, uinteger), written as int32 into `out`
+ * (the build's insertion order, vamana.py:141-143).  state_out (optional):
+ * {state_hi, state_lo, has_uint32, uinteger} after the draws. */
+int pk_pcg64_permutation(const uint64_t* state, int has_uint32, uint32_t uinteger, int64_t n, int32_t* out,
+                         uint64_t* state_out);
+
 /* RobustPrune of vertex p over explicit candidates (ids, squared distances)
  * merged with its current out-list cur_ids (distances recomputed).  Replaces
  * _kernels.robust_prune_standalone (_kernels.py:318-335).  out (R,) int64,

@@ -42,6 +42,7 @@ SIGNATURES = {
     "pk_build_vamana": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P],
     "pk_build_vamana_sharded": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _i, _i, _I,
                                 EXCHANGE_FN, _P, _P, _P, _P, _P, _P, _P],
+    "pk_pcg64_permutation": [_P, _i, ctypes.c_uint32, _I, _P, _P],
     "pk_robust_prune": [_P, _I, _I, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P],
     "pk_nearest_to_centroid": [_P, _I, _I, _P, _P],
     "pk_sqrt": [_P, _I, _P, _P],
@@ -117,6 +118,13 @@ def call(name: str, *args) -> None:
     if rc != 0:
         msg = lib().pk_last_error().decode(errors="replace")
         raise RuntimeError(f"{name} failed ({rc}): {msg}")
+
+
+def call_host(name: str, *args) -> None:
+    """Invoke a host-only C-ABI helper (no device work, usable without a GPU)."""
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        raise RuntimeError(f"{name} failed ({rc})")
 
 
 def stream() -> int:

@@ -222,8 +222,30 @@ def sample_starts(n: int, num_starts, seed: int, medoid_start: bool, p: PointSet
         if not 1 <= s <= n:
             raise ValueError(f"num_starts must be in [1, {n}], got {s}")
         starts = np.sort(rng.choice(n, size=s, replace=False).astype(np.int64))
-    order = rng.permutation(n).astype(np.int64)
+    order = permutation_int32(rng, n)
     return starts, order
+
+
+def permutation_int32(rng: np.random.Generator, n: int) -> np.ndarray:
+    """rng.permutation(n) as int32 (the build's insertion order), drawn by the
+    library's restatement of numpy's shuffle on the same PCG64 stream; the
+    generator's state is advanced exactly as numpy would."""
+    bg = rng.bit_generator
+    st = bg.state
+    if st.get("bit_generator") != "PCG64":
+        return rng.permutation(n).astype(np.int32)
+    mask = (1 << 64) - 1
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    words = np.array([s >> 64, s & mask, inc >> 64, inc & mask], dtype=np.uint64)
+    out = np.empty(n, dtype=np.int32)
+    after = np.zeros(4, dtype=np.uint64)
+    _lib.call_host("pk_pcg64_permutation", words.ctypes.data, int(st["has_uint32"]), int(st["uinteger"]), n,
+                   out.ctypes.data, after.ctypes.data)
+    st["state"]["state"] = (int(after[0]) << 64) | int(after[1])
+    st["has_uint32"] = int(after[2])
+    st["uinteger"] = int(after[3])
+    bg.state = st
+    return out
 
 
 # batches smaller than this run replicated on every rank of a sharded build
@@ -239,7 +261,7 @@ def build_graph_device(p: PointSet, R: int, L_build: int, alpha: float, starts: 
     adj = torch.empty((p.n, R), dtype=torch.int32, device=dev)
     deg = torch.empty(p.n, dtype=torch.int32, device=dev)
     st = starts_t if starts_t is not None else _lib.to_dev(starts.astype(np.int32))
-    od = order_t if order_t is not None else _lib.to_dev(order.astype(np.int32))
+    od = order_t if order_t is not None else _lib.to_dev(np.asarray(order, dtype=np.int32))
     if stats is None:
         stats = STATS["build"]
     if comm is None or comm.world == 1:

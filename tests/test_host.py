@@ -163,3 +163,22 @@ def test_workload_generators_are_deterministic():
 def test_product_path_fails_loudly_without_gpu():
     with pytest.raises(RuntimeError, match="CUDA"):
         pk.build_bruteforce(pk.PointSet(FIG_COORDS)).knn_all(1)
+
+
+def test_permutation_matches_numpy_stream():
+    """The library's PCG64 shuffle (int32 insertion order) equals numpy's
+    Generator.permutation and leaves the generator in the same state."""
+    from paper_2312_03940_b200 import vamana
+
+    for seed in (0, 1, 42, 2**40 + 7):
+        for n in (1, 2, 3, 17, 1000, 70_001):
+            a = np.random.default_rng(seed)
+            b = np.random.default_rng(seed)
+            a.choice(max(n, 1), size=1, replace=False)  # odd number of 32-bit halves drawn first
+            b.choice(max(n, 1), size=1, replace=False)
+            got = vamana.permutation_int32(a, n)
+            want = b.permutation(n)
+            assert got.dtype == np.int32
+            assert np.array_equal(got, want), (seed, n)
+            assert a.bit_generator.state == b.bit_generator.state
+            assert a.integers(0, 2**62) == b.integers(0, 2**62)
