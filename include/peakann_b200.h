@@ -160,6 +160,11 @@ int pk_build_vamana_sharded(const float* x, int64_t n, int64_t dp, const uint32_
 int pk_pcg64_permutation(const uint64_t* state, int has_uint32, uint32_t uinteger, int64_t n, int32_t* out,
                          uint64_t* state_out);
 
+/* Host helper: index of the first non-finite value of x[0, count) in
+ * row-major order (-1 if none) -> *first_bad; all host threads scan.  The
+ * PointSet finiteness check (core.py:17-54). */
+int pk_find_nonfinite(const float* x, int64_t count, int64_t* first_bad);
+
 /* RobustPrune of vertex p over explicit candidates (ids, squared distances)
  * merged with its current out-list cur_ids (distances recomputed).  Replaces
  * _kernels.robust_prune_standalone (_kernels.py:318-335).  out (R,) int64,

@@ -143,14 +143,37 @@ def _u8(n):
     return torch.zeros(n, dtype=torch.uint8, device=_lib.device())
 
 
-def _ids_of(flags_t) -> np.ndarray:
+def _ids_of_device(flags_t):
     import torch
 
     n = flags_t.shape[0]
     out = torch.empty(max(n, 1), dtype=torch.int64, device=flags_t.device)
     cnt = torch.zeros(1, dtype=torch.int64, device=flags_t.device)
     _lib.call("pk_flags_to_ids", flags_t, n, out, cnt, _lib.stream())
-    return _lib.to_host(out[: int(cnt.item())])
+    return out[: int(cnt.item())]
+
+
+def _ids_of(flags_t) -> np.ndarray:
+    return _lib.to_host(_ids_of_device(flags_t))
+
+
+def _to_host_many(tensors):
+    """Device tensors -> numpy arrays: async copies into one pinned staging
+    buffer (torch's caching host allocator), one stream sync."""
+    import torch
+
+    offs, total = [], 0
+    for t in tensors:
+        offs.append(total)
+        total += (t.numel() * t.element_size() + 63) // 64 * 64
+    buf = torch.empty(max(total, 64), dtype=torch.uint8, pin_memory=True)
+    views = []
+    for t, o in zip(tensors, offs):
+        v = buf[o:o + t.numel() * t.element_size()].view(t.dtype).view(t.shape)
+        v.copy_(t, non_blocking=True)
+        views.append(v)
+    torch.cuda.current_stream().synchronize()
+    return [v.numpy() for v in views]
 
 
 def _noise_flags(rho_t, rho_min: float):
@@ -424,8 +447,9 @@ def run_pipeline(
     rank returns the full result."""
     out = run_pipeline_device(p, index_config, k, density_kind, center_policy, noise_policy, doubling_params,
                               comm=comm)
-    state = DpcState(rho=_lib.to_host(out["rho"]),
-                     dependents=Dependents(_lib.to_host(out["lam"]), _lib.to_host(out["delta"])),
-                     neighbors=Neighborhoods(_lib.to_host(out["ids"]), _lib.to_host(out["dists"])))
-    clustering = Clustering(_lib.to_host(out["labels"]), _ids_of(out["centers"]), _ids_of(out["noise"]))
+    rho, lam, delta, ids, dists, labels, centers, noise = _to_host_many(
+        [out["rho"], out["lam"], out["delta"], out["ids"], out["dists"], out["labels"],
+         _ids_of_device(out["centers"]), _ids_of_device(out["noise"])])
+    state = DpcState(rho=rho, dependents=Dependents(lam, delta), neighbors=Neighborhoods(ids, dists))
+    clustering = Clustering(labels, centers, noise)
     return PipelineResult(clustering=clustering, state=state, timings=out["timings"])

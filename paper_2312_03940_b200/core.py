@@ -27,6 +27,23 @@ import numpy as np
 __all__ = ["PointSet", "distance", "squared_distance"]
 
 
+def _first_nonfinite(arr: np.ndarray) -> int:
+    """Flat index of the first inf / nan (row-major), -1 if none; scanned by all
+    host threads in the library when it is built, else by numpy."""
+    try:
+        from . import _lib
+
+        L = _lib.lib()
+    except Exception:  # noqa: BLE001 -- host validation must work before the library is built
+        finite = np.isfinite(arr)
+        return -1 if finite.all() else int(np.flatnonzero(~finite.ravel())[0])
+    import ctypes
+
+    out = ctypes.c_int64(-1)
+    L.pk_find_nonfinite(arr.ctypes.data, arr.size, ctypes.byref(out))
+    return int(out.value)
+
+
 class PointSet:
     """Immutable n x d matrix of float32 points, identified by row index."""
 
@@ -36,10 +53,9 @@ class PointSet:
             raise ValueError(f"points must be a 2-D array, got shape {arr.shape}")
         if arr.shape[0] < 1 or arr.shape[1] < 1:
             raise ValueError(f"need at least one point and one dimension, got shape {arr.shape}")
-        finite = np.isfinite(arr)
-        if not finite.all():
-            bad = np.argwhere(~finite)[0]
-            raise ValueError(f"non-finite coordinate at point {bad[0]}, dimension {bad[1]}")
+        bad = _first_nonfinite(arr)
+        if bad >= 0:
+            raise ValueError(f"non-finite coordinate at point {bad // arr.shape[1]}, dimension {bad % arr.shape[1]}")
         arr.flags.writeable = False
         self.data = arr
         self._dev = None
@@ -132,9 +148,18 @@ def upload_points(data: np.ndarray):
 
     n, d = data.shape
     dp = (d + 3) // 4 * 4
-    host = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32))
-    dev = torch.zeros((n, dp), dtype=torch.float32, device=_lib.device())
-    dev[:, :d].copy_(host, non_blocking=False)
+    arr = np.ascontiguousarray(data, dtype=np.float32)
+    import warnings
+
+    with warnings.catch_warnings():  # PointSet arrays are read-only; the tensor is only read
+        warnings.simplefilter("ignore", UserWarning)
+        host = torch.from_numpy(arr)
+    if dp == d:
+        dev = torch.empty((n, dp), dtype=torch.float32, device=_lib.device())
+        dev.copy_(host)
+    else:
+        dev = torch.zeros((n, dp), dtype=torch.float32, device=_lib.device())
+        dev[:, :d].copy_(host)
     return dev
 
 

@@ -82,3 +82,48 @@ extern "C" int pk_pcg64_permutation(const uint64_t* state, int has_uint32, uint3
     }
     return 0;
 }
+
+// ---- PointSet validation ---------------------------------------------------------------
+// Index of the first non-finite float in x[0, count) (row-major), -1 if all are
+// finite.  Scanned by all host threads (the reference's np.isfinite check,
+// core.py:17-54, is the same predicate).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+static int64_t first_nonfinite(const float* x, int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+        uint32_t b;
+        std::memcpy(&b, x + i, 4);
+        if ((b & 0x7f800000u) == 0x7f800000u) return i;  // inf or nan: all-ones exponent
+    }
+    return -1;
+}
+
+extern "C" int pk_find_nonfinite(const float* x, int64_t count, int64_t* first_bad) {
+    if (!first_bad || (count > 0 && !x)) return 2;
+    const int64_t chunk = 1 << 20;
+    int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), (count + chunk - 1) / chunk);
+    if (nt <= 1) {
+        *first_bad = first_nonfinite(x, 0, count);
+        return 0;
+    }
+    std::vector<int64_t> res(nt, -1);
+    std::vector<std::thread> th;
+    const int64_t per = (count + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            const int64_t lo = t * per, hi = std::min(count, lo + per);
+            if (lo < hi) res[t] = first_nonfinite(x, lo, hi);
+        });
+    for (auto& h : th) h.join();
+    *first_bad = -1;
+    for (int t = 0; t < nt; ++t)
+        if (res[t] >= 0) {
+            *first_bad = res[t];
+            break;
+        }
+    return 0;
+}
