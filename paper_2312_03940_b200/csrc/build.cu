@@ -154,6 +154,8 @@ __device__ __forceinline__ int prune_candidates(const DataRef& D, const CandSmem
     if (MODE == MODE_EXACT_U8)
         return warp_prune_u8(D.X8, D.dw, C.kd, C.ki, C.kp, c, alpha2, R, C.alive, C.cbuf, out, C.rows, D.dw + 1,
                              staged, ev);
+    if (MODE == MODE_SEQ64 && D.dp <= 128 * QV)
+        return warp_prune_seq64s<QV>(D.X, D.dp, C.kd, C.ki, c, alpha2, R, C.alive, C.cbuf, out, ev);
     const MakeAt<MODE, QV> make{D};
     return warp_prune(D.X, C.kd, C.ki, c, alpha2, R, C.alive, C.cbuf, out, make, ev);
 }
@@ -1409,9 +1411,11 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
 template <int MODE>
 int dispatch_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
                    int* adj, int* deg, long long* stats, int hash_bits, const Shard& SH, cudaStream_t st) {
-    if (MODE == MODE_SEQ64)
-        return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
+    // QV: 128-float (SEQ64 / EXACT32) or 128-byte (u8) chunks per row; SEQ64 rows
+    // wider than 1024 floats run without the fp32 screen (QV = 0)
     const int qv = MODE == MODE_EXACT_U8 ? (D.dw + 31) / 32 : (D.dp + 127) / 128;
+    if (MODE == MODE_SEQ64 && qv > 8)  // prune_candidates checks dp <= 128 * QV before screening
+        return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
     if (qv <= 1) return run_build<MODE, 1>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
     if (qv <= 2) return run_build<MODE, 2>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);
     if (qv <= 4) return run_build<MODE, 4>(D, n, R, L, alpha, starts, s, order, adj, deg, stats, hash_bits, SH, st);

@@ -343,6 +343,63 @@ struct DistFor<MODE_EXACT_U8, QV> {
     }
 };
 
+// fp32 screening of float data (SEQ64 mode): the pick row is spread over the
+// warp as float4 chunks (lane l holds chunks l, l + 32, ...; QV = ceil(dp/128));
+// dist() is a warp-cooperative fp32 sum of (p_i - x_i)^2 with an xor-butterfly
+// reduction, so every lane gets the same value.  All terms are non-negative:
+// the result is within 40 * 2^-24 relative of the exact sum (<= 32 fma steps
+// per lane + 5 tree levels + the rounding of each difference), which callers
+// widen to kScreenEps before deciding anything without the exact value.
+constexpr double kScreenEps = 1e-5;
+
+template <int QV>
+struct Fp32Pick {
+    float4 v[QV];
+    __device__ __forceinline__ void load(const float* __restrict__ X, int dp, unsigned id) {
+        const float4* r = reinterpret_cast<const float4*>(X + (size_t)id * dp);
+        const int nv = dp >> 2, lane = lane_id();
+#pragma unroll
+        for (int j = 0; j < QV; ++j) {
+            const int f = lane + 32 * j;
+            v[j] = f < nv ? __ldg(r + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    __device__ __forceinline__ float partial(const float* __restrict__ X, int dp, unsigned id) const {
+        const float4* r = reinterpret_cast<const float4*>(X + (size_t)id * dp);
+        const int nv = dp >> 2, lane = lane_id();
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < QV; ++j) {
+            const int f = lane + 32 * j;
+            if (f < nv) {
+                const float4 x = __ldg(r + f);
+                const float a = v[j].x - x.x, b = v[j].y - x.y, c = v[j].z - x.z, d = v[j].w - x.w;
+                acc = fmaf(a, a, acc);
+                acc = fmaf(b, b, acc);
+                acc = fmaf(c, c, acc);
+                acc = fmaf(d, d, acc);
+            }
+        }
+        return acc;
+    }
+    __device__ __forceinline__ static float reduce(float s) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(PK_FULL, s, o);
+        return s;
+    }
+};
+
+// Verdict of "alpha2 * d <= k" from a screened d~ (fp32): 1 = true, 0 = false,
+// 2 = too close to call (the caller computes the exact float64 distance).
+__device__ __forceinline__ int screen_le(double alpha2, float dscr, double k) {
+    const double d = (double)dscr;
+    if (!(d > 1e-20) || !(d < 1e30) || !(k > 1e-20)) return 2;
+    const double a = alpha2 * d;
+    if (a * (1.0 + kScreenEps) < k) return 1;
+    if (a * (1.0 - kScreenEps) > k) return 0;
+    return 2;
+}
+
 // functor: id -> distance policy object for that query row
 template <int MODE, int QV>
 struct MakeAt {
