@@ -488,10 +488,67 @@ __device__ int warp_prune(const float* __restrict__ X, const double* kd, const u
     return sel;
 }
 
-// RobustPrune for float data (SEQ64): same picks as warp_prune, but each kill
-// test alpha2 * d(pick, u) <= d(p, u) is first decided from a warp-cooperative
-// fp32 distance (Fp32Pick) and only the pairs screen_le cannot call are
-// evaluated in the reference's float64 order (one lane per pair).
+// One warp's share of a kill pass for pick `ps` (float data): the alive
+// candidates in 32-position chunks base = first, first + stride, ... < end are
+// screened with the fp32 distance (two per step, independent loads and
+// reductions overlap); pairs screen_le cannot call are queued in cbuf (32
+// entries) and evaluated in the reference's float64 order, one lane each.
+// Returns the number of distance evaluations.
+template <int QV>
+__device__ long long screened_kill_pass(const float* __restrict__ X, int dp, unsigned ps, const Fp32Pick<QV>& pick,
+                                        const double* kd, const unsigned* ki, unsigned char* alive, unsigned* cbuf,
+                                        double alpha2, int first, int end, int stride) {
+    const int lane = lane_id();
+    int nunc = 0;
+    long long nev = 0;
+    auto flush = [&]() {
+        __syncwarp();
+        if (nunc) {
+            const Seq64Member dx{X + (size_t)ps * dp, dp};
+            const unsigned uu = lane < nunc ? cbuf[lane] : 0u;
+            const double duv = dx.eval(X, (int)(lane < nunc ? ki[uu] : ps), nunc);
+            if (lane < nunc && alpha2 * duv <= kd[uu]) alive[uu] = 0;
+            nev += nunc;
+        }
+        nunc = 0;
+        __syncwarp();
+    };
+    for (int base = first; base < end; base += stride) {
+        const int u = base + lane;
+        unsigned b = __ballot_sync(PK_FULL, u < end && alive[u]);
+        while (b) {
+            const int j0 = __ffs(b) - 1;
+            b &= b - 1;
+            const int j1 = b ? __ffs(b) - 1 : -1;
+            if (b) b &= b - 1;
+            const int u0 = base + j0, u1 = j1 >= 0 ? base + j1 : u0;
+            const float p0 = pick.partial(X, dp, ki[u0]);
+            const float p1 = pick.partial(X, dp, ki[u1]);
+            const float s0 = Fp32Pick<QV>::reduce(p0), s1 = Fp32Pick<QV>::reduce(p1);
+            const int v0 = screen_le(alpha2, s0, kd[u0]);
+            const int v1 = j1 >= 0 ? screen_le(alpha2, s1, kd[u1]) : 0;
+            nev += 1 + (j1 >= 0);
+            if (lane == 0) {
+                if (v0 == 1) alive[u0] = 0;
+                if (v1 == 1) alive[u1] = 0;
+            }
+            if (v0 == 2) {
+                if (lane == 0) cbuf[nunc] = (unsigned)u0;
+                ++nunc;
+            }
+            if (v1 == 2) {
+                if (lane == 0) cbuf[nunc] = (unsigned)u1;
+                ++nunc;
+            }
+            if (nunc >= 31) flush();
+        }
+    }
+    flush();
+    return nev;
+}
+
+// RobustPrune for float data (SEQ64): same picks as warp_prune, every kill test
+// alpha2 * d(pick, u) <= d(p, u) decided by screened_kill_pass.
 template <int QV>
 __device__ int warp_prune_seq64s(const float* __restrict__ X, int dp, const double* kd, const unsigned* ki, int c,
                                  double alpha2, int R, unsigned char* alive, unsigned* cbuf, int* out,
@@ -519,52 +576,7 @@ __device__ int warp_prune_seq64s(const float* __restrict__ X, int dp, const doub
         if (sel >= R) break;
         Fp32Pick<QV> pick;
         pick.load(X, dp, ps);
-        int nunc = 0;
-        int nev = 0;
-        auto flush = [&]() {
-            __syncwarp();
-            if (nunc) {
-                const Seq64Member dx{X + (size_t)ps * dp, dp};
-                const unsigned uu = lane < nunc ? cbuf[lane] : 0u;
-                const double duv = dx.eval(X, (int)(lane < nunc ? ki[uu] : ps), nunc);
-                if (lane < nunc && alpha2 * duv <= kd[uu]) alive[uu] = 0;
-                if (lane == 0) *evals += nunc;
-            }
-            nunc = 0;
-            __syncwarp();
-        };
-        for (int base = t + 1; base < c; base += 32) {
-            const int u = base + lane;
-            unsigned b = __ballot_sync(PK_FULL, u < c && alive[u]);
-            while (b) {
-                // two candidates per step: independent loads and reductions overlap
-                const int j0 = __ffs(b) - 1;
-                b &= b - 1;
-                const int j1 = b ? __ffs(b) - 1 : -1;
-                if (b) b &= b - 1;
-                const int u0 = base + j0, u1 = j1 >= 0 ? base + j1 : u0;
-                const float p0 = pick.partial(X, dp, ki[u0]);
-                const float p1 = pick.partial(X, dp, ki[u1]);
-                const float s0 = Fp32Pick<QV>::reduce(p0), s1 = Fp32Pick<QV>::reduce(p1);
-                const int v0 = screen_le(alpha2, s0, kd[u0]);
-                const int v1 = j1 >= 0 ? screen_le(alpha2, s1, kd[u1]) : 0;
-                nev += 1 + (j1 >= 0);
-                if (lane == 0) {
-                    if (v0 == 1) alive[u0] = 0;
-                    if (v1 == 1) alive[u1] = 0;
-                }
-                if (v0 == 2) {
-                    if (lane == 0) cbuf[nunc] = (unsigned)u0;
-                    ++nunc;
-                }
-                if (v1 == 2) {
-                    if (lane == 0) cbuf[nunc] = (unsigned)u1;
-                    ++nunc;
-                }
-                if (nunc >= 31) flush();
-            }
-        }
-        flush();
+        const long long nev = screened_kill_pass<QV>(X, dp, ps, pick, kd, ki, alive, cbuf, alpha2, t + 1, c, 32);
         if (lane == 0) *evals += nev;
         ++t;
     }

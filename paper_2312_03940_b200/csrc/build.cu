@@ -154,7 +154,7 @@ __device__ __forceinline__ int prune_candidates(const DataRef& D, const CandSmem
     if (MODE == MODE_EXACT_U8)
         return warp_prune_u8(D.X8, D.dw, C.kd, C.ki, C.kp, c, alpha2, R, C.alive, C.cbuf, out, C.rows, D.dw + 1,
                              staged, ev);
-    if (MODE == MODE_SEQ64 && D.dp <= 128 * QV)
+    if (MODE == MODE_SEQ64 && D.dp <= 128 * QV && D.screen)
         return warp_prune_seq64s<QV>(D.X, D.dp, C.kd, C.ki, c, alpha2, R, C.alive, C.cbuf, out, ev);
     const MakeAt<MODE, QV> make{D};
     return warp_prune(D.X, C.kd, C.ki, c, alpha2, R, C.alive, C.cbuf, out, make, ev);
@@ -921,8 +921,10 @@ constexpr int kBigThreads = 256;
 // Candidates are sorted by (dist, id) with a block bitonic sort; duplicates
 // and the vertex itself are marked dead instead of compacted; the RobustPrune
 // picks stay sequential, each kill step runs over all block threads.
-template <int MODE>
+template <int MODE, int QV>
 __global__ void __launch_bounds__(kBigThreads) reverse_big_kernel(RevArgs A) {
+    __shared__ unsigned wbuf[kBigThreads];  // per-warp queues of the fp32 screen
+    const bool screen = MODE == MODE_SEQ64 && A.D.dp <= 128 * QV && A.D.screen;
     extern __shared__ __align__(16) unsigned char smem[];
     double* kd = reinterpret_cast<double*>(smem);
     unsigned* ki = reinterpret_cast<unsigned*>(smem + (size_t)A.capB * 8);
@@ -988,10 +990,20 @@ __global__ void __launch_bounds__(kBigThreads) reverse_big_kernel(RevArgs A) {
             ++sel;
             if (sel >= A.R) break;
             const unsigned ps = ki[t];
-            for (int x = t + 1 + tid; x < c0; x += kBigThreads) {
-                if (alive[x]) {
-                    ++ev;
-                    if (A.alpha2 * thread_dist<MODE>(A.D, ps, ki[x]) <= kd[x]) alive[x] = 0;
+            if (screen) {
+                // float data: each warp screens its 32-position chunks of the alive tail
+                Fp32Pick<QV> pick;
+                pick.load(A.D.X, A.D.dp, ps);
+                const int wid = tid >> 5;
+                const long long nev = screened_kill_pass<QV>(A.D.X, A.D.dp, ps, pick, kd, ki, alive, wbuf + 32 * wid,
+                                                             A.alpha2, t + 1 + 32 * wid, c0, kBigThreads);
+                if ((tid & 31) == 0) ev += nev;
+            } else {
+                for (int x = t + 1 + tid; x < c0; x += kBigThreads) {
+                    if (alive[x]) {
+                        ++ev;
+                        if (A.alpha2 * thread_dist<MODE>(A.D, ps, ki[x]) <= kd[x]) alive[x] = 0;
+                    }
                 }
             }
             ++t;
@@ -1170,7 +1182,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     }
     const int capB = 8192;
     const size_t big_bytes = (size_t)capB * 13 + 16;
-    auto bigk = reverse_big_kernel<MODE>;
+    auto bigk = reverse_big_kernel<MODE, QV>;
     PK_CHECK(cudaFuncSetAttribute(bigk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_bytes));
     const int grid_big = 2 * sm_count();
     int* biglist = nullptr;
@@ -1434,7 +1446,8 @@ static int build_entry(const float* x, int64_t n, int64_t dp, const uint32_t* x8
                        void* stream) {
     cudaStream_t st = as_stream(stream);
     long long* ls = reinterpret_cast<long long*>(stats);
-    const DataRef D{x, (int)dp, x8, (int)dw};
+    DataRef D{x, (int)dp, x8, (int)dw};
+    D.screen = env_int("PK_SCREEN", 1) == 1;  // fp32 screen of float-data kill tests (tests compare both)
     if (mode == MODE_EXACT_U8 && !x8) {
         set_error("u8 mode needs the packed rows");
         return 2;

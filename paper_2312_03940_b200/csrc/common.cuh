@@ -311,6 +311,7 @@ struct DataRef {
     int dp;
     const unsigned* X8;
     int dw;
+    int screen = 1;  // float data: decide RobustPrune kill tests from the fp32 screen when certain
 };
 
 constexpr int MODE_SEQ64 = 0;

@@ -230,3 +230,22 @@ def test_tensor_core_knn_equals_float64_path(case, monkeypatch):
 def test_c1brute_golden_without_tensor_cores(monkeypatch):
     monkeypatch.setenv("PEAKANN_B200_TC", "0")
     test_config_pipelines_golden("c1brute", "C1", 4_000, 10, True)
+
+
+def test_fp32_screened_prune_equals_float64_prune(monkeypatch):
+    """Float data: the screened RobustPrune (build prune, reverse re-prune,
+    hub groups) builds exactly the graph of the all-float64 prune."""
+    rng = np.random.default_rng(5)
+    hubs = rng.normal(size=(12, 384)).astype(np.float32)
+    lab = rng.integers(0, 12, 6_000)
+    x = (hubs[lab] + 0.05 * rng.normal(size=(6_000, 384))).astype(np.float32)
+    x[:40] = hubs[lab[:40]]  # exact duplicates of cluster centres: ties and zero distances
+    p = pk.PointSet(x)
+    assert p.mode == _lib.MODE_SEQ64
+    starts, order = vamana.sample_starts(p.n, None, 0, False, p)
+    monkeypatch.setenv("PK_SCREEN", "0")
+    a0, d0 = vamana.build_graph_device(p, 24, 48, 1.2, starts, order)
+    monkeypatch.setenv("PK_SCREEN", "1")
+    a1, d1 = vamana.build_graph_device(p, 24, 48, 1.2, starts, order)
+    assert torch.equal(d0, d1)
+    assert torch.equal(a0, a1)
