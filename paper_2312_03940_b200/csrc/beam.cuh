@@ -64,9 +64,9 @@ struct SearchParams {
     const int* deg;          // (n,)
     const int* starts;       // (s,)
     int s;
-    const unsigned* start_bm;  // bitmap of the start set (may be null)
     const unsigned* X8;        // packed u8 rows (u8 mode only)
     int dw;
+    int screen = 1;            // float data: fp32 pre-screen against a full beam (PK_SCREEN)
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -265,7 +265,6 @@ struct WarpBeam {
             for (int e0 = 0; e0 < nd; e0 += 32) {
                 int w = e0 + lane < nd ? (e0 == 0 ? w_a : e0 == 32 ? w_b : __ldg(row + e0 + lane)) : -1;
                 bool cand = w >= 0;
-                if (cand && P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u)) cand = false;
                 if (cand && seen_or_insert(sm.hash, sm.hmask, sm.hbits, (unsigned)w)) cand = false;
                 unsigned b = __ballot_sync(PK_FULL, cand);
                 const int nb = __popc(b);
@@ -287,10 +286,34 @@ struct WarpBeam {
         const int lane = lane_id();
         __syncwarp();
         for (int g = 0; g < c; g += 32) {
-            const int cnt = min(32, c - g);
+            int cnt = min(32, c - g);
             unsigned cid = lane < cnt ? sm.cbuf[g + lane] : 0u;
-            double dd = dist.eval(P.X, (int)cid, cnt);
             if (lane == 0) evals += cnt;
+            if constexpr (has_screen<D>::value) {
+                // float data, full beam: drop the candidates whose fp32 lower bound
+                // already exceeds the worst key (they would be rejected by merge);
+                // only the rest pay the sequential float64 evaluation
+                if (bl == L && P.screen && P.dp >= 256 && P.dp <= 128 * D::kQV) {
+                    const double wd = sm.bd[L - 1];
+                    bool drop = false;
+                    for (int j = 0; j < cnt; j += 2) {
+                        const int j1 = j + 1 < cnt ? j + 1 : j;
+                        const float s0 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j));
+                        const float s1 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j1));
+                        if (lane == j && s0 > 1e-20f && s0 < 1e30f && (double)s0 * (1.0 - kScreenEps) > wd) drop = true;
+                        if (lane == j1 && s1 > 1e-20f && s1 < 1e30f && (double)s1 * (1.0 - kScreenEps) > wd) drop = true;
+                    }
+                    const bool keep = lane < cnt && !drop;
+                    const unsigned b = __ballot_sync(PK_FULL, keep);
+                    cnt = __popc(b);
+                    if (!cnt) continue;
+                    __syncwarp();
+                    if (keep) sm.cbuf[g + warp_excl_prefix(b)] = cid;
+                    __syncwarp();
+                    cid = lane < cnt ? sm.cbuf[g + lane] : 0u;
+                }
+            }
+            double dd = dist.eval(P.X, (int)cid, cnt);
             merge<false>(dd, cid, lane < cnt);
         }
         __syncwarp();

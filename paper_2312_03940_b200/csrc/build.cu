@@ -1241,7 +1241,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     PK_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)n, st));
     PK_CHECK(cudaMemsetAsync(err, 0, sizeof(unsigned), st));
 
-    A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s, nullptr};
+    A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s};
+    A.P.screen = D.screen;
     A.D = D;
     A.L = L;
     A.H = H;

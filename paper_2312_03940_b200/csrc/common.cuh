@@ -318,12 +318,52 @@ constexpr int MODE_SEQ64 = 0;
 constexpr int MODE_EXACT32 = 1;
 constexpr int MODE_EXACT_U8 = 2;
 
+// Seq64 member query with an fp32 pre-screen for the beam searches: screen()
+// is a warp-cooperative fp32 squared distance (same value on every lane,
+// within kScreenEps relative of the exact one when dp <= 128 * QV), used only
+// to drop candidates that provably cannot enter a full beam; every distance
+// that is stored or compared exactly still comes from eval_one().
+template <int QV>
+struct Seq64Screened : Seq64Member {
+    static constexpr int kQV = QV;
+    __device__ __forceinline__ float screen(const float* __restrict__ X, unsigned id) const {
+        const float4* a = reinterpret_cast<const float4*>(q);
+        const float4* r = reinterpret_cast<const float4*>(X + (size_t)id * dp);
+        const int nv = dp >> 2, lane = lane_id();
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < QV; ++j) {
+            const int f = lane + 32 * j;
+            if (f < nv) {
+                const float4 y = __ldg(a + f), x = __ldg(r + f);
+                const float d0 = y.x - x.x, d1 = y.y - x.y, d2 = y.z - x.z, d3 = y.w - x.w;
+                acc = fmaf(d0, d0, acc);
+                acc = fmaf(d1, d1, acc);
+                acc = fmaf(d2, d2, acc);
+                acc = fmaf(d3, d3, acc);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, o);
+        return acc;
+    }
+};
+
+template <class D>
+struct has_screen {
+    static constexpr bool value = false;
+};
+template <int QV>
+struct has_screen<Seq64Screened<QV>> {
+    static constexpr bool value = true;
+};
+
 template <int MODE, int QV>
 struct DistFor;
 template <int QV>
 struct DistFor<MODE_SEQ64, QV> {
-    using T = Seq64Member;
-    __device__ static T make(const DataRef& D, unsigned id) { return T{D.X + (size_t)id * D.dp, D.dp}; }
+    using T = Seq64Screened<QV>;
+    __device__ static T make(const DataRef& D, unsigned id) { return T{{D.X + (size_t)id * D.dp, D.dp}}; }
 };
 template <int QV>
 struct DistFor<MODE_EXACT32, QV> {

@@ -359,8 +359,9 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
 template <int MODE>
 int dispatch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, int kk, int H,
                       long long* out_ids, double* out_d, long long* counts, long long* evals, cudaStream_t st) {
-    if (MODE == MODE_SEQ64) return launch_beam_knn<MODE, 1>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
     int qv = MODE == MODE_EXACT_U8 ? (P.dw + 31) / 32 : (P.dp + 127) / 128;
+    if (MODE == MODE_SEQ64 && qv > 8)  // no fp32 screen for rows wider than 1024 floats
+        return launch_beam_knn<MODE, 1>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
     if (qv <= 1) return launch_beam_knn<MODE, 1>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
     if (qv <= 2) return launch_beam_knn<MODE, 2>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
     if (qv <= 4) return launch_beam_knn<MODE, 4>(P, qids, m, L, kk, H, out_ids, out_d, counts, evals, st);
@@ -469,7 +470,8 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
     // Start points re-met as neighbours are simply re-evaluated (and dropped
     // by the key-equality check when already in the beam): cheaper than a
     // dependent bitmap load on every neighbour.
-    SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, nullptr, x8, (int)dw};
+    SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, x8, (int)dw};
+    P.screen = env_int("PK_SCREEN", 1) == 1;
     int H = choose_hash((int)L, hash_bits, n);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);
@@ -521,7 +523,7 @@ extern "C" int pk_beam_search_single(const float* x, int64_t n, int64_t dp, cons
         set_error("beam width L must be >= k");
         return 2;
     }
-    SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, nullptr};
+    SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s};
     int H = choose_hash((int)L, 0, n);
     size_t bytes = align16(beam_smem_bytes((int)L, H));
     unsigned* vi = nullptr;

@@ -249,3 +249,20 @@ def test_fp32_screened_prune_equals_float64_prune(monkeypatch):
     a1, d1 = vamana.build_graph_device(p, 24, 48, 1.2, starts, order)
     assert torch.equal(d0, d1)
     assert torch.equal(a0, a1)
+
+
+def test_fp32_screened_beam_search_equals_float64(monkeypatch):
+    """Float data with d >= 256: the beam searches' fp32 pre-screen against a
+    full beam changes nothing -- same graph, same kNN rows and counts."""
+    from paper_2312_03940_b200 import index as _idx  # noqa: F401
+
+    data, _ = workloads.generate("C4", n=8_000, components=40)
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PK_SCREEN", flag)
+        p = pk.PointSet(data)
+        g = pk.build_vamana(p, R=32, L_build=64, alpha=1.1, seed=0, query_beam=64)
+        nb = g.knn_all(16)
+        out[flag] = (g.graph.adjacency.copy(), nb.ids.copy(), nb.dists.copy())
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
