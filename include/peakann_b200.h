@@ -165,6 +165,12 @@ int pk_pcg64_permutation(const uint64_t* state, int has_uint32, uint32_t uintege
  * PointSet finiteness check (core.py:17-54). */
 int pk_find_nonfinite(const float* x, int64_t count, int64_t* first_bad);
 
+/* One pass over a freshly uploaded point set: out[0] = the pk_check_exact32
+ * flag (0 / 1 / 2), out[1] = flat index (row * d + column) of the first
+ * non-finite coordinate, -1 if none (device int64[2]).  The PointSet
+ * validation of core.py:17-54 fused with the distance-policy check. */
+int pk_scan_points(const float* x, int64_t n, int64_t dp, int64_t d, int64_t* out, void* stream);
+
 /* RobustPrune of vertex p over explicit candidates (ids, squared distances)
  * merged with its current out-list cur_ids (distances recomputed).  Replaces
  * _kernels.robust_prune_standalone (_kernels.py:318-335).  out (R,) int64,

@@ -27,6 +27,32 @@ import numpy as np
 __all__ = ["PointSet", "distance", "squared_distance"]
 
 
+def _device_ready() -> bool:
+    """CUDA device present and the library built (else PointSet validates on the host)."""
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            return False
+        from . import _lib
+
+        return os.path.exists(_lib.LIB_PATH)
+    except Exception:  # noqa: BLE001
+        return False
+
+
+def _mode_from_flag(flag: int) -> int:
+    """pk_check_exact32 flag -> distance policy, honouring PEAKANN_B200_MODE."""
+    from . import _lib
+
+    forced = os.environ.get("PEAKANN_B200_MODE", "auto").lower()
+    if forced == "seq64":
+        return _lib.MODE_SEQ64
+    if flag == 2 and forced == "exact32":
+        flag = 1
+    return {2: _lib.MODE_EXACT_U8, 1: _lib.MODE_EXACT32}.get(flag, _lib.MODE_SEQ64)
+
+
 def _first_nonfinite(arr: np.ndarray) -> int:
     """Flat index of the first inf / nan (row-major), -1 if none; scanned by all
     host threads in the library when it is built, else by numpy."""
@@ -53,14 +79,20 @@ class PointSet:
             raise ValueError(f"points must be a 2-D array, got shape {arr.shape}")
         if arr.shape[0] < 1 or arr.shape[1] < 1:
             raise ValueError(f"need at least one point and one dimension, got shape {arr.shape}")
-        bad = _first_nonfinite(arr)
-        if bad >= 0:
-            raise ValueError(f"non-finite coordinate at point {bad // arr.shape[1]}, dimension {bad % arr.shape[1]}")
-        arr.flags.writeable = False
-        self.data = arr
         self._dev = None
         self._mode = None
         self._x8 = None
+        if _device_ready():
+            # upload once and validate on the device: one pass gives the first
+            # non-finite coordinate and the distance-policy flag (pk_scan_points)
+            bad = self._upload_and_scan(arr)
+        else:
+            bad = _first_nonfinite(arr)
+        if bad >= 0:
+            self._dev = None
+            raise ValueError(f"non-finite coordinate at point {bad // arr.shape[1]}, dimension {bad % arr.shape[1]}")
+        arr.flags.writeable = False
+        self.data = arr
 
     @property
     def n(self) -> int:
@@ -87,6 +119,19 @@ class PointSet:
         return i
 
     # ---- device side --------------------------------------------------------
+    def _upload_and_scan(self, arr) -> int:
+        import torch
+
+        from . import _lib
+
+        n, d = arr.shape
+        self._dev = upload_points(arr)
+        res = torch.empty(2, dtype=torch.int64, device=self._dev.device)
+        _lib.call("pk_scan_points", self._dev, n, (d + 3) // 4 * 4, d, res, _lib.stream())
+        flag, bad = (int(v) for v in res.tolist())
+        self._mode = _mode_from_flag(flag)
+        return bad
+
     def device(self):
         """(n, dp) float32 CUDA tensor, uploaded once."""
         if self._dev is None:
@@ -99,26 +144,21 @@ class PointSet:
         """Use an already-resident (n, dp) float32 tensor as the device copy
         (bench path: inputs resident in HBM before the timed region)."""
         self._dev = dev_tensor
+        self._mode = None
+        self._x8 = None
         return self
 
     @property
     def mode(self) -> int:
         """Distance policy code (see module docstring)."""
         if self._mode is None:
+            import torch
+
             from . import _lib
 
-            forced = os.environ.get("PEAKANN_B200_MODE", "auto").lower()
-            if forced == "seq64":
-                self._mode = _lib.MODE_SEQ64
-            else:
-                import torch
-
-                flag = torch.zeros(1, dtype=torch.int32, device=_lib.device())
-                _lib.call("pk_check_exact32", self.device(), self.n, self.dp, self.d, flag, _lib.stream())
-                f = int(flag.item())
-                if f == 2 and forced == "exact32":
-                    f = 1
-                self._mode = {2: _lib.MODE_EXACT_U8, 1: _lib.MODE_EXACT32}.get(f, _lib.MODE_SEQ64)
+            flag = torch.zeros(1, dtype=torch.int32, device=_lib.device())
+            _lib.call("pk_check_exact32", self.device(), self.n, self.dp, self.d, flag, _lib.stream())
+            self._mode = _mode_from_flag(int(flag.item()))
         return self._mode
 
     @property

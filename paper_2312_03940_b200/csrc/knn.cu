@@ -243,12 +243,16 @@ __device__ __forceinline__ float from_ordered(unsigned k) {
 }
 
 // range[0] = ordered max, range[1] = ordered min over the real coordinates
-__global__ void check_exact32_kernel(const float* x, long long total, int dp, int d, int* bad, unsigned* range) {
+__global__ void check_exact32_kernel(const float* x, long long total, int dp, int d, int* bad, unsigned* range,
+                                     unsigned long long* first_nonfinite) {
     unsigned hi = 0u, lo = 0xffffffffu;
     int b = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-        if ((int)(i % dp) >= d) continue;
+        const int col = (int)(i % dp);
+        if (col >= d) continue;
         float v = x[i];
+        if (first_nonfinite && !isfinite(v))
+            atomicMin(first_nonfinite, (unsigned long long)(i / dp) * (unsigned long long)d + (unsigned long long)col);
         if (v != rintf(v)) b = 1;
         unsigned k = ordered_key(v);
         hi = max(hi, k);
@@ -416,7 +420,7 @@ extern "C" int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d
     long long total = n * dp;
     {
         ProfScope _ps("check_exact32_kernel", st);
-        check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx);
+        check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx, nullptr);
     }
     {
         ProfScope _ps("finish_exact32_kernel", st);
@@ -425,6 +429,39 @@ extern "C" int pk_check_exact32(const float* x, int64_t n, int64_t dp, int64_t d
     PK_CHECK_LAUNCH("check_exact32");
     release(bad, st);
     release(mx, st);
+    return 0;
+}
+
+__global__ void scan_result_kernel(const int* flag, const unsigned long long* first, long long* out) {
+    out[0] = *flag;
+    out[1] = *first == ~0ull ? -1ll : (long long)*first;
+}
+
+extern "C" int pk_scan_points(const float* x, int64_t n, int64_t dp, int64_t d, int64_t* out, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    int *bad = nullptr, *flag = nullptr;
+    unsigned* mx = nullptr;
+    unsigned long long* first = nullptr;
+    PK_CHECK(scratch(&bad, 1, st));
+    PK_CHECK(scratch(&flag, 1, st));
+    PK_CHECK(scratch(&mx, 2, st));
+    PK_CHECK(scratch(&first, 1, st));
+    PK_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    PK_CHECK(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
+    PK_CHECK(cudaMemsetAsync(mx + 1, 0xff, sizeof(unsigned), st));
+    PK_CHECK(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), st));
+    long long total = n * dp;
+    {
+        ProfScope _ps("check_exact32_kernel", st);
+        check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx, first);
+    }
+    {
+        ProfScope _ps("finish_exact32_kernel", st);
+        finish_exact32_kernel<<<1, 1, 0, st>>>(bad, mx, (int)d, flag);
+        scan_result_kernel<<<1, 1, 0, st>>>(flag, first, reinterpret_cast<long long*>(out));
+    }
+    PK_CHECK_LAUNCH("scan_points");
+    for (void* p : {(void*)bad, (void*)flag, (void*)mx, (void*)first}) release(p, st);
     return 0;
 }
 
@@ -440,7 +477,7 @@ extern "C" int pk_pack_u8(const float* x, int64_t n, int64_t dp, int64_t d, uint
     long long total = n * dp;
     {
         ProfScope _ps("check_exact32_kernel", st);
-        check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx);
+        check_exact32_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, total, (int)dp, (int)d, bad, mx, nullptr);
     }
     {
         ProfScope _ps("pack_u8_kernel", st);

@@ -266,3 +266,15 @@ def test_fp32_screened_beam_search_equals_float64(monkeypatch):
         out[flag] = (g.graph.adjacency.copy(), nb.ids.copy(), nb.dists.copy())
     for a, b in zip(out["0"], out["1"]):
         assert np.array_equal(a, b)
+
+
+def test_pointset_device_validation_reports_first_nonfinite():
+    """With a GPU the PointSet check runs on the device (pk_scan_points); the
+    error names the same first (point, dimension) as numpy's argwhere."""
+    x = np.random.default_rng(0).normal(size=(5_000, 37)).astype(np.float32)
+    x[4_000, 36] = np.inf
+    x[1_234, 5] = np.nan
+    x[1_234, 9] = -np.inf
+    with pytest.raises(ValueError, match="point 1234, dimension 5"):
+        pk.PointSet(x.copy())
+    assert pk.PointSet(np.ones((3, 5), np.float32)).mode in (_lib.MODE_EXACT_U8, _lib.MODE_EXACT32)
