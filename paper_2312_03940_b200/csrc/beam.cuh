@@ -142,11 +142,20 @@ struct WarpBeam {
             fb = __ballot_sync(PK_FULL, keep);
         }
         int rank = 0;
-        for (unsigned b = fb; b; b &= b - 1) {
-            int j = __ffs(b) - 1;
-            double dj = __shfl_sync(PK_FULL, cd, j);
-            unsigned ij = __shfl_sync(PK_FULL, cid, j);
-            if (key_lt(dj, ij, cd, cid)) ++rank;
+        if constexpr (int_keys<Dist>::value) {
+            // exact modes: distances are integers < 2^32, (dist, id) packs into one u64
+            const unsigned long long mk = ((unsigned long long)(unsigned)cd << 32) | cid;
+            for (unsigned b = fb; b; b &= b - 1) {
+                const unsigned long long kj = __shfl_sync(PK_FULL, mk, __ffs(b) - 1);
+                rank += kj < mk;
+            }
+        } else {
+            for (unsigned b = fb; b; b &= b - 1) {
+                int j = __ffs(b) - 1;
+                double dj = __shfl_sync(PK_FULL, cd, j);
+                unsigned ij = __shfl_sync(PK_FULL, cid, j);
+                if (key_lt(dj, ij, cd, cid)) ++rank;
+            }
         }
         const int c = __popc(fb);
         if (keep) sm.spos[rank] = pos;

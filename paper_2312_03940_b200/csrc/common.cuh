@@ -349,6 +349,20 @@ struct Seq64Screened : Seq64Member {
     }
 };
 
+// distance policies whose values are exact integers below 2^32 (packed keys)
+template <class D>
+struct int_keys {
+    static constexpr bool value = false;
+};
+template <int QV>
+struct int_keys<Exact32<QV>> {
+    static constexpr bool value = true;
+};
+template <int QV>
+struct int_keys<ExactU8<QV>> {
+    static constexpr bool value = true;
+};
+
 template <class D>
 struct has_screen {
     static constexpr bool value = false;
