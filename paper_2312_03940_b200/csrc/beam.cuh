@@ -70,6 +70,14 @@ struct SearchParams {
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
+// strictly increasing start list (every warp checks once per launch)
+__device__ __forceinline__ bool starts_increasing(const SearchParams& P) {
+    bool ok = true;
+    for (int i = lane_id(); i + 1 < P.s; i += 32)
+        if (!(__ldg(P.starts + i) < __ldg(P.starts + i + 1))) ok = false;
+    return __all_sync(PK_FULL, ok);
+}
+
 template <class Dist>
 struct WarpBeam {
     BeamSmem sm;
@@ -205,9 +213,11 @@ struct WarpBeam {
         __syncwarp();
     }
 
-    // Seed with the start set (batch insert of ceil(s/32) chunks).
+    // Seed with the start set (batch insert of ceil(s/32) chunks).  `unique`:
+    // the start list is strictly increasing (sample_starts' sorted draw), so a
+    // batch cannot hold equal keys and the duplicate pass of merge is skipped.
     template <class D>
-    __device__ void seed(const SearchParams& P, const D& dist, bool hash_starts) {
+    __device__ void seed(const SearchParams& P, const D& dist, bool hash_starts, bool unique) {
         const int lane = lane_id();
         for (int b = 0; b < P.s; b += 32) {
             const int cnt = min(32, P.s - b);
@@ -215,7 +225,8 @@ struct WarpBeam {
             if (hash_starts && lane < cnt) seen_or_insert(sm.hash, sm.hmask, sm.hbits, id);
             double dd = dist.eval(P.X, (int)id, cnt);
             if (lane == 0) evals += cnt;
-            merge<true>(dd, id, lane < cnt);
+            if (unique) merge<false>(dd, id, lane < cnt);
+            else merge<true>(dd, id, lane < cnt);
         }
     }
 

@@ -61,12 +61,13 @@ __global__ void __launch_bounds__(128, 8) build_search_kernel(BuildArgs A) {
     BeamSmem sm = carve_beam(smem + (size_t)wib * A.search_bytes, A.L, A.H);
     const MakeAt<MODE, QV> make{A.D};
     long long ev = 0, expansions = 0;
+    const bool uniq = starts_increasing(A.P);
     for (int t = blockIdx.x * wpb + wib; t < A.m; t += gridDim.x * wpb) {
         const unsigned p = (unsigned)A.bids[t];
         auto dist = make(p);
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, A.L, A.vlog_i + (size_t)t * A.vcap, A.vlog_d + (size_t)t * A.vcap, A.vcap, A.err);
-        wb.seed(A.P, dist, false);
+        wb.seed(A.P, dist, false, uniq);
         wb.walk(A.P, dist);
         ev += wb.evals;
         expansions += wb.vl;

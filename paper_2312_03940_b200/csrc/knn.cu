@@ -22,12 +22,13 @@ __global__ void __launch_bounds__(128, 8) beam_knn_kernel(SearchParams P, const 
     unsigned char* mine = smem + (size_t)wib * warp_bytes;
     BeamSmem sm = carve_beam(mine, L, H);
     long long ev = 0, ex = 0;
+    const bool uniq = starts_increasing(P);
     for (long long t = (long long)blockIdx.x * wpb + wib; t < m; t += (long long)gridDim.x * wpb) {
         const unsigned qi = (unsigned)qids[t];
         auto dist = DistFor<MODE, QV>::make(P.data(), qi);
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, L, nullptr, nullptr, 0, nullptr);
-        wb.seed(P, dist, false);
+        wb.seed(P, dist, false, uniq);
         wb.walk(P, dist);
         long long* oi = out_ids + t * kk;
         double* od = out_d + t * kk;
@@ -66,7 +67,7 @@ __global__ void single_search_kernel(SearchParams P, Dist dist, unsigned self, i
     __syncwarp();
     WarpBeam<Dist> wb;
     wb.init(sm, L, vtmp_i, vtmp_d, vcap, &s_err);
-    wb.seed(P, dist, true);
+    wb.seed(P, dist, true, false);
     wb.walk(P, dist);
     int got = wb.emit(self, k, top_ids, top_d);
     const int lane = lane_id();
