@@ -42,6 +42,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "points/sec end-to-end ANN-DPC at 1/2/4/8 B200; dep-point queries/s; % roofline"
+TIMED_KERNELS = ("build_search_kernel", "beam_knn_kernel", "build_prune_block_kernel", "reverse_block_kernel",
+                 "reverse_big_kernel", "build_prune_kernel", "reverse_kernel", "scan_denser_kernel")
 
 
 def parse():
@@ -95,7 +97,18 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_first(self, n=2, timeout=3.0):
+        """Block until the sampler has produced n lines (its start-up holds driver
+        locks that would otherwise stall the first timed steps)."""
+        t = time.perf_counter()
+        while self.proc is not None and len(self.lines) < n and time.perf_counter() - t < timeout:
+            time.sleep(0.01)
+
+    def mark(self, t0, t1):
+        """The timed region's host-time window (samples inside it are preferred)."""
+        self.window = (t0, t1)
 
     def stop(self):
         if self.proc is None:
@@ -109,7 +122,13 @@ class ClockSampler:
             self.thread.join(timeout=2)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        w = getattr(self, "window", None)
+        if w is not None:
+            inside = [x for x in lines if w[0] <= x[0] <= w[1]]
+            # short timed regions may fall between two 200 ms samples: keep the nearest
+            lines = inside or sorted(lines, key=lambda x: min(abs(x[0] - w[0]), abs(x[0] - w[1])))[:2]
+        for _, ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -283,6 +302,10 @@ def main_ours(args):
         if world > 1:
             dist.barrier()
 
+    # the clock sampler (an nvidia-smi process) starts before the warm-up so its
+    # start-up does not land in the timed steps; samples are filtered to the window
+    clocks = ClockSampler(local)
+    clocks.start()
     # warm-up (untimed)
     for _ in range(args.warmup):
         run_pipeline_device(p, **kw, comm=comm)
@@ -293,12 +316,16 @@ def main_ours(args):
     vamana.STATS["build"] = build_stats
     vamana.STATS["beam"] = beam_stats
     _lib.prof_collect(reset=True)
-    _lib.prof_enable(True)
-    clocks = ClockSampler(local)
-    clocks.start()
+    # event timing only for the kernels the roofline and the breakdown need (every
+    # launch is still counted); bracketing all ~300 launches per step costs ~1 ms
+    _lib.prof_only(TIMED_KERNELS)
+    _lib.prof_enable(os.environ.get("PK_BENCH_PROF", "1") == "1")
+    clocks.wait_first()
     total_ms = 0.0
+    t_win0 = time.perf_counter()
     step_ms = []
     stage = {"index": 0.0, "density": 0.0, "dependent": 0.0, "unionfind": 0.0}
+    step_stages = []
     rounds = []
     last = None
     stream = torch.cuda.current_stream()
@@ -318,7 +345,9 @@ def main_ours(args):
         total_ms += step_ms[-1]
         for kk_, v in last["timings"].items():
             stage[kk_] += v
+        step_stages.append({kk_: round(v * 1e3, 2) for kk_, v in last["timings"].items()})
         rounds = trace
+    clocks.mark(t_win0, time.perf_counter())
     clk = clocks.stop()
     _lib.prof_enable(False)
     prof = _lib.prof_collect(reset=True)
@@ -432,9 +461,12 @@ def main_ours(args):
             "clocks": clk,
             "stage_ms": {k_: v / args.steps * 1e3 for k_, v in stage.items()},
             "step_ms": [round(v, 3) for v in step_ms],
+            "step_stage_ms": step_stages,
             "dependent_rounds": rounds,
             "kernels_ms_per_step": {k_: round(v[1] / args.steps, 4) for k_, v in sorted(prof.items(),
-                                                                                      key=lambda kv: -kv[1][1])},
+                                                                                      key=lambda kv: -kv[1][1])
+                                    if k_ in TIMED_KERNELS},
+            "kernel_launches_per_step": {k_: v[0] / args.steps for k_, v in sorted(prof.items())},
             "counters_per_step": {"build": bs.tolist(), "beam": be.tolist()},
             "ari_vs_generator": ari_truth,
         }

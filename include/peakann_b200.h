@@ -51,6 +51,9 @@ int pk_device_info(int* sm_count, int* smem_optin);
  * "name count total_ms\n" lines into buf (host) and returns the full length;
  * reset != 0 clears the counters. */
 void pk_prof_enable(int on);
+/* Restrict event timing to the comma-separated kernel names ("" = all);
+ * launch counting is unaffected. */
+void pk_prof_only(const char* names);
 int pk_prof_collect(char* buf, int len, int reset);
 
 /* Distance-policy classification into *out_flag (device int): 2 when every

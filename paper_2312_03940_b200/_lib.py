@@ -93,6 +93,8 @@ def lib():
         L.pk_device_info.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
         L.pk_prof_enable.argtypes = [ctypes.c_int]
         L.pk_prof_enable.restype = None
+        L.pk_prof_only.argtypes = [ctypes.c_char_p]
+        L.pk_prof_only.restype = None
         L.pk_prof_collect.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
         L.pk_prof_collect.restype = ctypes.c_int
         _lib = L
@@ -149,6 +151,11 @@ def to_host(t: torch.Tensor) -> np.ndarray:
 
 def prof_enable(on: bool) -> None:
     lib().pk_prof_enable(1 if on else 0)
+
+
+def prof_only(names) -> None:
+    """Time only these kernels (iterable of names; empty = all)."""
+    lib().pk_prof_only(",".join(names).encode())
 
 
 def prof_collect(reset: bool = True) -> dict:

@@ -272,6 +272,13 @@ struct WarpBeam {
             int w_a = lane < P.R ? __ldg(row + lane) : -1;
             int w_b = lane + 32 < P.R ? __ldg(row + lane + 32) : -1;
             const int nd = __ldg(P.deg + p);
+            if (nd == 0) {
+                // empty row (early build batches: most start points are not inserted
+                // yet): expanding it changes nothing, and neither does expanding the
+                // following unvisited entries with empty rows -- visit that run at once
+                visit_empty_run(P);
+                continue;
+            }
             {
                 // prefetch the adjacency row of the next unvisited entry: it is
                 // the next expansion unless this one inserts something closer
@@ -298,6 +305,40 @@ struct WarpBeam {
             __syncwarp();
             flush(P, dist, c);
         }
+    }
+
+    // Visit, in beam order, the unvisited entries from the cursor on whose rows
+    // are empty, up to the first unvisited entry with a non-empty row.
+    __device__ void visit_empty_run(const SearchParams& P) {
+        const int lane = lane_id();
+        for (int base = cursor; base < bl; base += 32) {
+            const int e = base + lane;
+            const unsigned iv = e < bl ? sm.bi[e] : PK_VIS;
+            const bool unv = !(iv & PK_VIS);
+            const int dg = unv ? __ldg(P.deg + (iv & PK_IDMASK)) : 0;
+            const unsigned stop = __ballot_sync(PK_FULL, unv && dg > 0);
+            const unsigned before = stop ? (1u << (__ffs(stop) - 1)) - 1u : 0xffffffffu;
+            const unsigned run = __ballot_sync(PK_FULL, unv && dg == 0) & before;
+            if ((run >> lane) & 1u) {
+                sm.bi[e] = iv | PK_VIS;
+                if (vlog_i) {
+                    const int at = vl + __popc(run & ((1u << lane) - 1u));
+                    if (at < vcap) {
+                        vlog_i[at] = iv & PK_IDMASK;
+                        vlog_d[at] = sm.bd[e];
+                    } else {
+                        atomicOr(err, ERR_VISIT_OVERFLOW);
+                    }
+                }
+            }
+            vl += __popc(run);
+            if (stop) {
+                cursor = base + __ffs(stop) - 1;
+                break;
+            }
+            cursor = min(base + 32, bl);
+        }
+        __syncwarp();
     }
 
     // evaluate and merge the c candidates staged in cbuf

@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <set>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -71,10 +72,12 @@ static cudaEvent_t take_event() {
     return e;
 }
 
+static std::set<std::string> g_prof_only;  // empty: time every launch
+
 ProfScope::ProfScope(const char* n, cudaStream_t s) : name(n), st(s), slot(-1) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_counts[name] += 1;
-    if (g_prof_on) {
+    if (g_prof_on && (g_prof_only.empty() || g_prof_only.count(name))) {
         ProfRecord r{name, take_event(), take_event()};
         cudaEventRecord(r.a, st);
         g_records.push_back(r);
@@ -93,6 +96,28 @@ ProfScope::~ProfScope() {
 extern "C" void pk_prof_enable(int on) {
     std::lock_guard<std::mutex> lk(pk::g_prof_mu);
     pk::g_prof_on = on != 0;
+    // events are created up front: cudaEventCreate inside a timed region stalls
+    while (on && pk::g_event_pool.size() < 4096) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) break;
+        pk::g_event_pool.push_back(e);
+    }
+}
+
+// comma-separated kernel names whose launches get event timing ("" = all)
+extern "C" void pk_prof_only(const char* names) {
+    std::lock_guard<std::mutex> lk(pk::g_prof_mu);
+    pk::g_prof_only.clear();
+    std::string cur;
+    for (const char* c = names ? names : ""; ; ++c) {
+        if (*c == ',' || *c == 0) {
+            if (!cur.empty()) pk::g_prof_only.insert(cur);
+            cur.clear();
+            if (*c == 0) break;
+        } else {
+            cur += *c;
+        }
+    }
 }
 
 // "name count total_ms\n" per kernel; counts since the last reset, times of the

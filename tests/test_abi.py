@@ -36,7 +36,7 @@ def test_ctypes_table_covers_header():
     from paper_2312_03940_b200 import _lib
 
     names = set(declared()) - {"pk_version", "pk_last_error", "pk_device_info", "pk_prof_enable",
-                               "pk_prof_collect"}
+                               "pk_prof_collect", "pk_prof_only"}
     assert names == set(_lib.SIGNATURES), names ^ set(_lib.SIGNATURES)
 
 
