@@ -46,7 +46,7 @@ inline void release(void* p, cudaStream_t st) {
 
 // per-warp shared memory sizes
 inline size_t beam_smem_bytes(int L, int H) {
-    return (((size_t)L * 12 + (size_t)H * 2 + 15) & ~(size_t)15) + 128 + 4 * 64;
+    return (((((size_t)L * 12 + 7) & ~(size_t)7) + (size_t)H * 2 + 15) & ~(size_t)15) + 128 + 4 * 64;
 }
 inline size_t sort_smem_bytes(int cap) {
     return (size_t)cap * 13 + 128;

@@ -41,16 +41,17 @@ struct BeamSmem {
 
 constexpr int kCbuf = 64;  // compacted-candidate buffer (ids) per warp
 
-// per-warp layout: bd[L] | bi[L] | hash[H] (u16) | spos[32] | cbuf[kCbuf]
+// per-warp layout: bd[L] | bi[L] | (8-aligned) hash[H] (u16) | spos[32] | cbuf[kCbuf]
 // (host side: beam_smem_bytes in api.cuh)
 __device__ __forceinline__ BeamSmem carve_beam(unsigned char* base, int L, int H) {
     BeamSmem s;
     s.bd = reinterpret_cast<double*>(base);
     s.bi = reinterpret_cast<unsigned*>(base + (size_t)L * 8);
-    s.hash = reinterpret_cast<unsigned short*>(base + (size_t)L * 12);
+    const size_t hoff = ((size_t)L * 12 + 7) & ~(size_t)7;  // 8-byte aligned sets
+    s.hash = reinterpret_cast<unsigned short*>(base + hoff);
     s.hmask = (unsigned)H - 1u;
     s.hbits = __ffs(H) - 1;
-    const size_t tail = ((size_t)L * 12 + (size_t)H * 2 + 15) & ~(size_t)15;
+    const size_t tail = (hoff + (size_t)H * 2 + 15) & ~(size_t)15;
     s.spos = reinterpret_cast<int*>(base + tail);
     s.cbuf = reinterpret_cast<unsigned*>(base + tail + 128);
     return s;

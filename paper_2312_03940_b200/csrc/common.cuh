@@ -52,30 +52,25 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-// Per-query "seen" table: H = 2^hbits 16-bit slots, open addressing with a
-// linear probe window of 8.  The home slot is the id's low hbits (ids are a
-// random permutation's worth of indices, so the low bits spread well); a slot
-// stores (id >> hbits) << 3 | probe offset, which reconstructs the id exactly,
-// so nothing is ever reported seen falsely.  A full window overwrites the home
-// slot (lossy): a lost id only costs a re-evaluation.  Needs
-// (n-1) >> hbits < 8191 (choose_hash enforces it).  16-bit slots halve the
-// table and double the warps per SM of the search kernels.
+// Per-query "seen" table: H = 2^hbits 16-bit slots as H/4 sets of 4 ways.  A
+// set is picked by the id's low (hbits - 2) bits and each way stores the
+// quotient id >> (hbits - 2), which reconstructs the id exactly, so nothing is
+// ever reported seen falsely.  One 64-bit load reads a whole set (no probe
+// loop, no divergence); a full set overwrites a pseudo-random way (lossy): a
+// lost id only costs a re-evaluation.  Needs (n-1) >> (hbits-2) < 0xffff
+// (choose_hash enforces it); 0xffff marks an empty way.
 constexpr unsigned short kSeenEmpty = 0xffffu;
 
 __device__ __forceinline__ bool seen_or_insert(unsigned short* hash, unsigned mask, int hbits, unsigned id) {
-    const unsigned home = id & mask;
-    const unsigned tag = (id >> hbits) << 3;
-#pragma unroll
-    for (unsigned i = 0; i < 8; ++i) {
-        const unsigned s = (home + i) & mask;
-        const unsigned v = hash[s];
-        if (v == (tag | i)) return true;
-        if (v == kSeenEmpty) {
-            hash[s] = (unsigned short)(tag | i);
-            return false;
-        }
-    }
-    hash[home] = (unsigned short)tag;
+    const int sbits = hbits - 2;
+    const unsigned set = id & (mask >> 2);
+    const unsigned tag = id >> sbits;
+    const uint2 v = reinterpret_cast<const uint2*>(hash)[set];
+    const unsigned t2 = tag | (tag << 16);
+    if (__vcmpeq2(v.x, t2) | __vcmpeq2(v.y, t2)) return true;
+    const unsigned ex = __vcmpeq2(v.x, 0xffffffffu), ey = __vcmpeq2(v.y, 0xffffffffu);
+    const unsigned way = ex ? ((ex & 0xffffu) ? 0u : 1u) : ey ? ((ey & 0xffffu) ? 2u : 3u) : ((tag ^ (id >> 5)) & 3u);
+    hash[4 * set + way] = (unsigned short)tag;
     return false;
 }
 

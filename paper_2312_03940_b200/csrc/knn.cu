@@ -329,8 +329,8 @@ int choose_hash(int L, int hash_bits, long long n) {
         if (h < 512) h = 512;
         if (h > 8192) h = 8192;
     }
-    // 16-bit slots hold (id >> log2 h) << 3: keep the quotient below 8191
-    while (((n - 1) >> (__builtin_ctz((unsigned)h))) >= 8191) h <<= 1;
+    // 16-bit ways hold the quotient id >> log2(h / 4): keep it below 0xffff
+    while (((n - 1) >> (__builtin_ctz((unsigned)h) - 2)) >= 0xffff) h <<= 1;
     return h;
 }
 
