@@ -85,6 +85,8 @@ class ClockSampler:
         self.thread = None
 
     def start(self):
+        if os.environ.get("PK_BENCH_NO_SMI") == "1":  # diagnosis only
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
