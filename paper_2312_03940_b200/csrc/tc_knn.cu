@@ -34,15 +34,17 @@ constexpr int TC_BM = 128;          // queries per tile (UMMA M)
 constexpr int TC_BN = 256;          // points per tile (UMMA N)
 constexpr int TC_BK = 64;           // fp16 elements per stage (128-byte rows)
 constexpr int TC_STAGES = 4;
-constexpr int TC_KP = 64;           // screened candidates kept per row (K')
-constexpr int TC_THREADS = 192;     // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int TC_KP = 64;           // screened candidates kept per row (K'), two halves
+constexpr int TC_KPH = TC_KP / 2;   // one max-heap per (row, column half of the tile)
+constexpr int TC_EPI = 8;           // epilogue warps: 2 per TMEM lane group (column halves)
+constexpr int TC_THREADS = 64 + 32 * TC_EPI;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_B_BYTES = (TC_BN / 2) * TC_BK * 2;  // each CTA of the pair holds half the point tile
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_LIST_BYTES = TC_KP * TC_BM * 8;
 constexpr int TC_CH = 16;           // accumulator columns per tcgen05.ld in the epilogue
 constexpr size_t TC_SMEM =
-    1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256 + 2 * TC_BN * 4 + TC_CH * TC_BM * 4;
+    1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256 + 2 * TC_BN * 4 + TC_CH * 32 * TC_EPI * 4;
 
 struct TcArgs {
     const float* qn;       // (m,) ||q||^2 of the fp16-rounded-from rows (fp32 originals)
@@ -174,7 +176,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
     unsigned long long* tempty = bars + 2 * TC_STAGES + 2;
     unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * TC_STAGES + 4);
     float* pn_s = reinterpret_cast<float*>(bars + 2 * TC_STAGES + 8);  // [2][TC_BN]
-    float* stg = pn_s + 2 * TC_BN;                                     // [TC_CH][TC_BM]
+    float* stg = pn_s + 2 * TC_BN;  // [TC_CH][32 * TC_EPI] chunk distances per epilogue thread
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
@@ -192,7 +194,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 8);  // one arrival per epilogue warp of both CTAs
+            mbar_init(tempty + a, 2 * TC_EPI);  // one arrival per epilogue warp of both CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -266,32 +268,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
             if (acc == 0) aphase ^= 1;
         }
     } else if (warp >= 2) {
-        // epilogue: thread owns TMEM lane (query row) 32 * (warp % 4) + lane
+        // epilogue: thread owns TMEM lane (query row) 32 * (warp % 4) + lane and
+        // one column half of every tile (warps 2-5: columns 0-127, 6-9: 128-255)
         const int ew = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int et = (warp - 2) * 32 + lane;  // epilogue thread 0..255
         const int row = ew * 32 + lane;
         const int tid = row;  // list column
+        float* hd = lst_d + (size_t)half * TC_KPH * TC_BM;  // this half's heap, [TC_KPH][TC_BM]
+        int* hi = lst_i + (size_t)half * TC_KPH * TC_BM;
         const int q = qblock * TC_BM + row;
         const bool live = q < A.m;
         const long long self = (live && A.qids) ? A.qids[q] : -1;
         const float qn = live ? A.qn[q] : 0.f;
-        for (int k = 0; k < TC_KP; ++k) {
-            lst_d[k * TC_BM + tid] = __int_as_float(0x7f800000);
-            lst_i[k * TC_BM + tid] = -1;
+        for (int k = 0; k < TC_KPH; ++k) {
+            hd[k * TC_BM + tid] = __int_as_float(0x7f800000);
+            hi[k * TC_BM + tid] = -1;
         }
         float thr = __int_as_float(0x7f800000);
         int acc = 0;
         unsigned aphase = 0;
+        constexpr int kChunks = TC_BN / TC_CH / 2;  // chunks per column half
         for (int t = t0; t < t1; ++t) {
-            // this tile's point norms, staged once for the 128 epilogue threads
-            for (int x = tid; x < TC_BN; x += TC_BM) {
+            // this tile's point norms, staged once for the 256 epilogue threads
+            for (int x = et; x < TC_BN; x += 32 * TC_EPI) {
                 const int col = t * TC_BN + x;
                 pn_s[acc * TC_BN + x] = col < A.n ? __ldg(A.pn + col) : 0.f;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI) : "memory");
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
             const unsigned taddr = tmem + ((unsigned)(ew * 32) << 16) + (unsigned)(acc * TC_BN);
-            for (int ch = 0; ch < TC_BN / TC_CH; ++ch) {
+            for (int cc = 0; cc < kChunks; ++cc) {
+                const int ch = half * kChunks + cc;
                 unsigned v[TC_CH];
                 __syncwarp();
                 asm volatile(
@@ -305,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
                 if (A.dbg & 1) continue;  // warp-uniform (profiling aid)
                 const int cbase = t * TC_BN + ch * TC_CH;
                 const float* pnt = pn_s + acc * TC_BN + ch * TC_CH;
-                // distances of the chunk to smem, bit mask of the ones below the K'-th
+                // distances of the chunk, bit mask of the ones below this half's K'-th
                 float pv[TC_CH];
 #pragma unroll
                 for (int j = 0; j < TC_CH; j += 4) {
@@ -325,7 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
                 if (!live) mask = 0;
                 if (__any_sync(PK_FULL, mask != 0)) {
 #pragma unroll
-                    for (int j = 0; j < TC_CH; ++j) stg[j * TC_BM + tid] = __uint_as_float(v[j]);
+                    for (int j = 0; j < TC_CH; ++j) stg[j * 32 * TC_EPI + et] = __uint_as_float(v[j]);
                 }
                 if (cbase + TC_CH > A.n) mask &= A.n > cbase ? (1u << (A.n - cbase)) - 1u : 0u;
                 if (self >= cbase && self < cbase + TC_CH) mask &= ~(1u << (int)(self - cbase));
@@ -334,26 +343,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
                 while (mask) {
                     const int j = __ffs(mask) - 1;
                     mask &= mask - 1u;
-                    const float dd = stg[j * TC_BM + tid];
+                    const float dd = stg[j * 32 * TC_EPI + et];
                     if (!(dd < thr)) continue;
-                    // the list is a binary max-heap: replace the root, sift down
+                    // binary max-heap: replace the root, sift down
                     int i = 0;
                     for (;;) {
                         const int l = 2 * i + 1;
-                        if (l >= TC_KP) break;
+                        if (l >= TC_KPH) break;
                         const int r = l + 1;
-                        const float dl = lst_d[l * TC_BM + tid];
-                        const float dr = r < TC_KP ? lst_d[r * TC_BM + tid] : -1.f;
+                        const float dl = hd[l * TC_BM + tid];
+                        const float dr = r < TC_KPH ? hd[r * TC_BM + tid] : -1.f;
                         const int cidx = dr > dl ? r : l;
                         const float dc = dr > dl ? dr : dl;
                         if (dc <= dd) break;
-                        lst_d[i * TC_BM + tid] = dc;
-                        lst_i[i * TC_BM + tid] = lst_i[cidx * TC_BM + tid];
+                        hd[i * TC_BM + tid] = dc;
+                        hi[i * TC_BM + tid] = hi[cidx * TC_BM + tid];
                         i = cidx;
                     }
-                    lst_d[i * TC_BM + tid] = dd;
-                    lst_i[i * TC_BM + tid] = cbase + j;
-                    thr = lst_d[tid];
+                    hd[i * TC_BM + tid] = dd;
+                    hi[i * TC_BM + tid] = cbase + j;
+                    thr = hd[tid];
                 }
             }
             tc_fence_before();
@@ -363,10 +372,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
             if (acc == 0) aphase ^= 1;
         }
         if (live) {
-            const size_t base = ((size_t)q * A.nsplit + split) * TC_KP;
-            for (int k = 0; k < TC_KP; ++k) {
-                A.out_id[base + k] = lst_i[k * TC_BM + tid];
-                A.out_d[base + k] = lst_d[k * TC_BM + tid];
+            const size_t base = ((size_t)q * A.nsplit + split) * TC_KP + (size_t)half * TC_KPH;
+            for (int k = 0; k < TC_KPH; ++k) {
+                A.out_id[base + k] = hi[k * TC_BM + tid];
+                A.out_d[base + k] = hd[k * TC_BM + tid];
             }
         }
     }
@@ -472,11 +481,12 @@ __global__ void tc_rescore_kernel(const float* __restrict__ X, int dp, const lon
         // certificate
         const double tk = kd[kk - 1];
         bool ok = true;
-        for (int s = lane; s < nsplit; s += 32) {
+        // one heap per (split, column half): each full heap bounds what it screened out
+        for (int s = lane; s < 2 * nsplit; s += 32) {
             float worst = -1.f;
             bool full = true;
-            for (int k = 0; k < TC_KP; ++k) {
-                const size_t o = (size_t)t * c + (size_t)s * TC_KP + k;
+            for (int k = 0; k < TC_KPH; ++k) {
+                const size_t o = (size_t)t * c + (size_t)s * TC_KPH + k;
                 if (cand_i[o] < 0) full = false;
                 worst = fmaxf(worst, cand_d[o]);
             }
