@@ -174,6 +174,16 @@ int pk_find_nonfinite(const float* x, int64_t count, int64_t* first_bad);
  * validation of core.py:17-54 fused with the distance-policy check. */
 int pk_scan_points(const float* x, int64_t n, int64_t dp, int64_t d, int64_t* out, void* stream);
 
+/* Nearest strictly denser point of each query (rank[p] > rank[q], order
+ * (dist, id)) through the tensor-core screen of pk_brute_knn_tc restricted to
+ * denser points, float64 rescoring and the same error-bound certificate.
+ * Replaces _kernels.dp_scan_all (_kernels.py:442-462) for batches; rows the
+ * certificate rejects are flagged (row_flags, *uncertified) and must be
+ * recomputed with pk_dp_scan.  out_id (m,) int64 (-1 = none), out_sqd (m,)
+ * float64. */
+int pk_dp_scan_tc(const float* x, int64_t n, int64_t dp, const int64_t* rank, const int64_t* qids, int64_t m,
+                  int64_t* out_id, double* out_sqd, uint8_t* row_flags, uint64_t* uncertified, void* stream);
+
 /* RobustPrune of vertex p over explicit candidates (ids, squared distances)
  * merged with its current out-list cur_ids (distances recomputed).  Replaces
  * _kernels.robust_prune_standalone (_kernels.py:318-335).  out (R,) int64,

@@ -39,6 +39,7 @@ SIGNATURES = {
     "pk_brute_knn": [_P, _I, _I, _P, _I, _I, _P, _P, _P],
     "pk_brute_knn_vector": [_P, _I, _I, _P, _I, _P, _P, _P],
     "pk_brute_knn_tc": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P],
+    "pk_dp_scan_tc": [_P, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P],
     "pk_build_vamana": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P],
     "pk_build_vamana_sharded": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _i, _i, _I,
                                 EXCHANGE_FN, _P, _P, _P, _P, _P, _P, _P],

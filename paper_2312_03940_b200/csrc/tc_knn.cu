@@ -44,7 +44,8 @@ constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_LIST_BYTES = TC_KP * TC_BM * 8;
 constexpr int TC_CH = 16;           // accumulator columns per tcgen05.ld in the epilogue
 constexpr size_t TC_SMEM =
-    1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256 + 2 * TC_BN * 4 + TC_CH * 32 * TC_EPI * 4;
+    1024 + (size_t)TC_STAGES * TC_STAGE_BYTES + TC_LIST_BYTES + 256 + 2 * TC_BN * 4 + TC_CH * 32 * TC_EPI * 4 +
+    2 * TC_BN * 4;
 
 struct TcArgs {
     const float* qn;       // (m,) ||q||^2 of the fp16-rounded-from rows (fp32 originals)
@@ -56,6 +57,8 @@ struct TcArgs {
     int nsplit;
     int* out_id;           // (m, nsplit, K') screened ids (-1 = empty)
     float* out_d;          // (m, nsplit, K') screened distances
+    const int* prank;      // (n,) density rank: only points with prank > qrank[row] are kept
+    const int* qrank;      // (m,) (both null: plain kNN)
 };
 
 // ---- small PTX wrappers ---------------------------------------------------------------
@@ -177,6 +180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
     unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * TC_STAGES + 4);
     float* pn_s = reinterpret_cast<float*>(bars + 2 * TC_STAGES + 8);  // [2][TC_BN]
     float* stg = pn_s + 2 * TC_BN;  // [TC_CH][32 * TC_EPI] chunk distances per epilogue thread
+    int* rk_s = reinterpret_cast<int*>(stg + TC_CH * 32 * TC_EPI);  // [2][TC_BN] point ranks (dp scan)
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
@@ -281,6 +285,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
         const bool live = q < A.m;
         const long long self = (live && A.qids) ? A.qids[q] : -1;
         const float qn = live ? A.qn[q] : 0.f;
+        const int myrank = (A.prank && live) ? A.qrank[q] : 0;
         for (int k = 0; k < TC_KPH; ++k) {
             hd[k * TC_BM + tid] = __int_as_float(0x7f800000);
             hi[k * TC_BM + tid] = -1;
@@ -294,6 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
             for (int x = et; x < TC_BN; x += 32 * TC_EPI) {
                 const int col = t * TC_BN + x;
                 pn_s[acc * TC_BN + x] = col < A.n ? __ldg(A.pn + col) : 0.f;
+                if (A.prank) rk_s[acc * TC_BN + x] = col < A.n ? __ldg(A.prank + col) : -1;
             }
             asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI) : "memory");
             mbar_wait(tfull + acc, aphase);
@@ -330,6 +336,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
                     const float dd = qn + pv[j] - 2.f * __uint_as_float(v[j]);
                     v[j] = __float_as_uint(dd);
                     mask |= (dd < thr ? 1u : 0u) << j;
+                }
+                if (A.prank) {  // nearest-denser search: only strictly denser points compete
+                    const int* rk = rk_s + acc * TC_BN + ch * TC_CH;
+#pragma unroll
+                    for (int j = 0; j < TC_CH; ++j)
+                        if (rk[j] <= myrank) mask &= ~(1u << j);
                 }
                 if (!live) mask = 0;
                 if (__any_sync(PK_FULL, mask != 0)) {
@@ -556,11 +568,11 @@ bool tc_supported() {
 
 using namespace pk;
 
-extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
-                               int64_t* out_ids, double* out_sqd, uint8_t* row_flags, uint64_t* uncertified,
-                               void* stream) {
-    cudaStream_t st = as_stream(stream);
-    const int64_t kk = k < n - 1 ? k : n - 1;
+// shared host driver: exact kNN (prank == null) or nearest strictly denser
+// point (prank / qrank, kk = 1) through tensor-core screening + rescoring
+static int tc_knn_core(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t kk,
+                       const int* prank, const int* qrank, int64_t* out_ids, double* out_sqd, uint8_t* row_flags,
+                       uint64_t* uncertified, cudaStream_t st) {
     if (kk <= 0 || m <= 0) return 0;
     if (kk > TC_KP / 2) {
         set_error("tensor-core kNN keeps k <= 32");
@@ -611,6 +623,8 @@ extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int6
     A.tiles_per_split = per;
     A.nsplit = nsplit;
     A.dbg = getenv("PK_TC_DEBUG") ? atoi(getenv("PK_TC_DEBUG")) : 0;
+    A.prank = prank;
+    A.qrank = qrank;
     PK_CHECK(scratch(&A.out_id, (size_t)m * nsplit * TC_KP, st));
     PK_CHECK(scratch(&A.out_d, (size_t)m * nsplit * TC_KP, st));
     PK_CHECK(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
@@ -642,4 +656,43 @@ extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int6
         release(p, st);
     (void)iota;
     return 0;
+}
+
+extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
+                               int64_t* out_ids, double* out_sqd, uint8_t* row_flags, uint64_t* uncertified,
+                               void* stream) {
+    const int64_t kk = k < n - 1 ? k : n - 1;
+    return tc_knn_core(x, n, dp, qids, m, kk, nullptr, nullptr, out_ids, out_sqd, row_flags, uncertified,
+                       as_stream(stream));
+}
+
+__global__ void rank32_kernel(const long long* rank, long long n, const long long* qids, long long m, int* prank,
+                              int* qrank) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n + m; i += (long long)gridDim.x * blockDim.x) {
+        if (i < n) prank[i] = (int)rank[i];
+        else qrank[i - n] = (int)rank[qids[i - n]];
+    }
+}
+
+extern "C" int pk_dp_scan_tc(const float* x, int64_t n, int64_t dp, const int64_t* rank, const int64_t* qids, int64_t m,
+                             int64_t* out_id, double* out_sqd, uint8_t* row_flags, uint64_t* uncertified, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (m <= 0) return 0;
+    if (n >= (1ll << 31)) {
+        set_error("tensor-core dp scan needs n < 2^31");
+        return 2;
+    }
+    int *prank = nullptr, *qrank = nullptr;
+    PK_CHECK(scratch(&prank, (size_t)n, st));
+    PK_CHECK(scratch(&qrank, (size_t)m, st));
+    {
+        ProfScope _ps("rank32_kernel", st);
+        rank32_kernel<<<grid_for(n + m, 256), 256, 0, st>>>(reinterpret_cast<const long long*>(rank), n,
+                                                            reinterpret_cast<const long long*>(qids), m, prank, qrank);
+    }
+    PK_CHECK_LAUNCH("rank32_kernel");
+    const int rc = tc_knn_core(x, n, dp, qids, m, 1, prank, qrank, out_id, out_sqd, row_flags, uncertified, st);
+    release(prank, st);
+    release(qrank, st);
+    return rc;
 }

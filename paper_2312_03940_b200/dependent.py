@@ -152,6 +152,33 @@ def _resolve_short(p: PointSet, rank_t, short_t, ms: int, kk: int, lam_t, delta_
     return out[:c], c
 
 
+def _dp_scan_on_tensor_cores(p: PointSet, m: int) -> bool:
+    """Float data, enough work for a tensor-core screen (exact integer modes
+    already scan with exact fp32 / u8 arithmetic)."""
+    from .index import use_tensor_cores
+
+    return p.mode == _lib.MODE_SEQ64 and m >= 64 and p.n >= 4096 and use_tensor_cores(p, max(m, 256), 1)
+
+
+def _dp_scan_tc(p: PointSet, rank_t, q, m: int, sid, ssq):
+    """pk_dp_scan_tc, then the exact scan for the rows its certificate rejects."""
+    import torch
+
+    flags = torch.zeros(m, dtype=torch.uint8, device=q.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=q.device)
+    _lib.call("pk_dp_scan_tc", p.device(), p.n, p.dp, rank_t, q, m, sid, ssq, flags, cnt, _lib.stream())
+    nbad = int(cnt.item())
+    if nbad:
+        bad = torch.nonzero(flags, as_tuple=True)[0]
+        bq = q[bad].contiguous()
+        bi = torch.empty(nbad, dtype=torch.int64, device=q.device)
+        bs = torch.empty(nbad, dtype=torch.float64, device=q.device)
+        _lib.call("pk_dp_scan", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, rank_t, bq, nbad, bi, bs,
+                  _lib.stream())
+        sid[bad] = bi
+        ssq[bad] = bs
+
+
 def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: DoublingParams, trace=None,
                       comm=None):
     """(lam_t, delta_t) on device; `trace` collects (unresolved, kq) per round.
@@ -216,8 +243,11 @@ def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: D
         if mq:
             sid = torch.empty(mq, dtype=torch.int64, device=dev)
             ssq = torch.empty(mq, dtype=torch.float64, device=dev)
-            _lib.call("pk_dp_scan", p.device(), n, p.dp, p.packed(), p.dw, p.mode, rank_t, q, mq, sid, ssq,
-                      _lib.stream())
+            if _dp_scan_on_tensor_cores(p, mq):
+                _dp_scan_tc(p, rank_t, q, mq, sid, ssq)
+            else:
+                _lib.call("pk_dp_scan", p.device(), n, p.dp, p.packed(), p.dw, p.mode, rank_t, q, mq, sid, ssq,
+                          _lib.stream())
             _lib.call("pk_scatter_dependents", q, mq, sid, ssq, lam_t, delta_t, _lib.stream())
     if comm is not None:
         # each point was resolved by exactly one rank; the others hold -1 / +inf

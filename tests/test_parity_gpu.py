@@ -278,3 +278,29 @@ def test_pointset_device_validation_reports_first_nonfinite():
     with pytest.raises(ValueError, match="point 1234, dimension 5"):
         pk.PointSet(x.copy())
     assert pk.PointSet(np.ones((3, 5), np.float32)).mode in (_lib.MODE_EXACT_U8, _lib.MODE_EXACT32)
+
+
+@pytest.mark.parametrize("case", ["gauss", "c5", "grid"])
+def test_tensor_core_dp_scan_equals_exact_scan(case):
+    """pk_dp_scan_tc (denser-only tensor-core screen + float64 rescoring +
+    certificate, uncertified rows rescanned) == pk_dp_scan."""
+    from paper_2312_03940_b200 import density, dependent
+
+    data = _tc_cases()[case]
+    p = pk.PointSet(data)
+    p._mode = _lib.MODE_SEQ64  # the scan the tensor cores replace (float data)
+    rng = np.random.default_rng(2)
+    rho = torch.from_numpy(rng.integers(0, 50, p.n).astype(np.float64)).cuda()  # many density ties
+    rank = density.rank_order_device(rho)
+    q = torch.from_numpy(rng.choice(p.n, 700, replace=False).astype(np.int64)).cuda()
+    top = int(torch.argmax(rank).item())
+    q = q[q != top].contiguous()
+    m = q.shape[0]
+    i0 = torch.empty(m, dtype=torch.int64, device="cuda")
+    s0 = torch.empty(m, dtype=torch.float64, device="cuda")
+    _lib.call("pk_dp_scan", p.device(), p.n, p.dp, None, 0, p.mode, rank, q, m, i0, s0, _lib.stream())
+    i1 = torch.empty_like(i0)
+    s1 = torch.empty_like(s0)
+    dependent._dp_scan_tc(p, rank, q, m, i1, s1)
+    assert torch.equal(i0, i1)
+    assert torch.equal(s0, s1)
