@@ -610,7 +610,9 @@ static int tc_knn_core(const float* x, int64_t n, int64_t dp, const int64_t* qid
     if (rc) return rc;
     const int qblocks = (int)((m + 2 * TC_BM - 1) / (2 * TC_BM)) * 2;  // whole CTA pairs
     const int ntiles = (int)((n + TC_BN - 1) / TC_BN);
-    int nsplit = std::max(1, std::min(ntiles, (2 * sm_count() + qblocks - 1) / qblocks));
+    // column splits fill the GPU for small query counts; at most 16 so the rescoring
+    // list (nsplit * K' per row) stays within one warp's shared memory budget
+    int nsplit = std::max(1, std::min(std::min(ntiles, 16), (2 * sm_count() + qblocks - 1) / qblocks));
     const int per = (ntiles + nsplit - 1) / nsplit;
     nsplit = (ntiles + per - 1) / per;
     TcArgs A;
