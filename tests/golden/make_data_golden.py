@@ -74,6 +74,19 @@ def main():
         data[f"g{i}__sha_points"] = np.array(sha(pts.data))
         data[f"g{i}__sha_labels"] = np.array(sha(lab))
         data[f"g{i}__head"] = pts.data[:4]
+    rng = np.random.default_rng(11)
+    for i in range(6):
+        n = int(rng.integers(2, 3000))
+        a = rng.integers(0, int(rng.integers(1, 40)), n) * 3 - 7
+        b = rng.integers(0, int(rng.integers(1, 40)), n)
+        ct = ref.contingency(a, b)
+        h, c = ref.homogeneity_completeness(a, b)
+        data[f"m{i}__a"] = a
+        data[f"m{i}__b"] = b
+        data[f"m{i}__ari"] = np.array([ref.ari(a, b)])
+        data[f"m{i}__hc"] = np.array([h, c])
+        for f in ("rows", "cols", "counts", "row_sums", "col_sums"):
+            data[f"m{i}__{f}"] = getattr(ct, f)
     with tempfile.TemporaryDirectory() as tmp:
         files = bad_files(tmp)
         for name, p in files.items():

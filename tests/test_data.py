@@ -79,3 +79,22 @@ def test_round_trips(tmp_path):
     assert json.load(open(tmp_path / "c.json")) == {"centers": [0, 3], "noise": [1]}
     with pytest.raises(ValueError):
         pk.read_vectors(str(tmp_path / "x.fvecs"), "npy")
+
+
+def test_metrics_bit_identical_to_reference():
+    from paper_2312_03940_b200 import metrics
+
+    z = golden("data")
+    for i in range(6):
+        a, b = z[f"m{i}__a"], z[f"m{i}__b"]
+        ct = metrics.contingency(a, b)
+        for f in ("rows", "cols", "counts", "row_sums", "col_sums"):
+            assert np.array_equal(getattr(ct, f), z[f"m{i}__{f}"]), (i, f)
+        assert ct.n == a.shape[0]
+        assert pk.ari(a, b) == float(z[f"m{i}__ari"][0])
+        assert pk.homogeneity_completeness(a, b) == tuple(float(v) for v in z[f"m{i}__hc"])
+    assert pk.ari([0, 0, 1, 1], [0, 1, 0, 1]) == -0.5
+    with pytest.raises(ValueError):
+        metrics.contingency([], [])
+    with pytest.raises(ValueError):
+        pk.ari([1], [1])

@@ -304,3 +304,21 @@ def test_tensor_core_dp_scan_equals_exact_scan(case):
     dependent._dp_scan_tc(p, rank, q, m, i1, s1)
     assert torch.equal(i0, i1)
     assert torch.equal(s0, s1)
+
+
+def test_device_contingency_equals_host():
+    from paper_2312_03940_b200 import metrics
+
+    rng = np.random.default_rng(9)
+    a = rng.integers(-50, 900, 300_000)
+    b = rng.integers(0, 1_000, 300_000)
+    dev = metrics._contingency_device(a, b)
+    metrics_min, metrics.DEVICE_MIN = metrics.DEVICE_MIN, 10**12
+    try:
+        host = metrics.contingency(a, b)
+        h_ari = pk.ari(a, b)
+    finally:
+        metrics.DEVICE_MIN = metrics_min
+    for f in ("rows", "cols", "counts", "row_sums", "col_sums"):
+        assert np.array_equal(getattr(dev, f), getattr(host, f)), f
+    assert pk.ari(a, b) == h_ari  # device path (n >= DEVICE_MIN)
