@@ -189,6 +189,32 @@ def brute_tc_sample(n=131_072, k=16, reps=3):
             "uncertified_rows": index.TC_STATS["uncertified"] // reps}
 
 
+# ---------------------------------------------------------------------------- counting pass
+
+
+def unique_evaluations(p, kw, vamana, comm):
+    """One untimed pipeline pass in the kernels' counting mode: per-warp global
+    bitmaps record every id a search evaluates, giving the exact number of
+    distinct evaluations (the roofline's U) next to the expansions (X)."""
+    import torch
+
+    from paper_2312_03940_b200.cluster import run_pipeline_device
+
+    bst = torch.zeros(5, dtype=torch.int64, device="cuda")
+    bem = torch.zeros(3, dtype=torch.int64, device="cuda")
+    vamana.STATS["build"], vamana.STATS["beam"] = bst, bem
+    os.environ["PK_COUNT_UNIQUE"] = "1"
+    try:
+        run_pipeline_device(p, **kw, comm=comm)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("PK_COUNT_UNIQUE", None)
+        vamana.STATS["build"] = vamana.STATS["beam"] = None
+    b, e = bst.tolist(), bem.tolist()
+    return {"build_unique": b[4], "build_evals": b[0], "build_expansions": b[3],
+            "beam_unique": e[2], "beam_evals": e[0], "beam_expansions": e[1]}
+
+
 # ---------------------------------------------------------------------------- CPU baseline
 
 
@@ -313,8 +339,8 @@ def main_ours(args):
         run_pipeline_device(p, **kw, comm=comm)
     torch.cuda.synchronize()
 
-    build_stats = torch.zeros(4, dtype=torch.int64, device="cuda")
-    beam_stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    build_stats = torch.zeros(5, dtype=torch.int64, device="cuda")
+    beam_stats = torch.zeros(3, dtype=torch.int64, device="cuda")
     vamana.STATS["build"] = build_stats
     vamana.STATS["beam"] = beam_stats
     _lib.prof_collect(reset=True)
@@ -403,16 +429,20 @@ def main_ours(args):
     dom_name, (dom_cnt, dom_ms) = dom
     bs = _lib.to_host(build_stats) / args.steps
     be = _lib.to_host(beam_stats) / args.steps
+    # untimed counting pass: the exact number of DISTINCT ids each search
+    # evaluated (U of SURVEY.md 8(d); the lossy seen table re-evaluates a few)
+    uniq = unique_evaluations(p, kw, vamana, comm)
+    queries_beam = n + sum(r[0] for r in rounds if isinstance(r[1], int))
     s = int(np.ceil(np.sqrt(n)))
     d4 = w.d * 4
     if dom_name.startswith("build_search"):
         # per inserted point: non-seed unique search evaluations + adjacency rows + current out-row
-        evals_nonseed = bs[0] - n * s
-        alg_bytes = evals_nonseed * d4 + bs[3] * w.R * 4
+        evals_nonseed = uniq["build_unique"] - n * s
+        alg_bytes = evals_nonseed * d4 + uniq["build_expansions"] * w.R * 4
         unit_desc = "search gather bytes (unique non-seed evals x 4d + expansions x 4R) over all inserted points"
     elif dom_name.startswith("beam_knn"):
-        evals_nonseed = be[0] - (n * s)
-        alg_bytes = evals_nonseed * d4 + be[1] * w.R * 4
+        evals_nonseed = uniq["beam_unique"] - queries_beam * s
+        alg_bytes = evals_nonseed * d4 + uniq["beam_expansions"] * w.R * 4
         unit_desc = "gather bytes (unique non-seed evals x 4d + expansions x 4R) over all queries"
     else:
         alg_bytes = None
@@ -469,7 +499,10 @@ def main_ours(args):
                                                                                       key=lambda kv: -kv[1][1])
                                     if k_ in TIMED_KERNELS},
             "kernel_launches_per_step": {k_: v[0] / args.steps for k_, v in sorted(prof.items())},
-            "counters_per_step": {"build": bs.tolist(), "beam": be.tolist()},
+            "counters_per_step": {"build": bs.tolist(), "beam": be.tolist(),
+                                  "legend": "build [evals, prune evals, reverse evals, expansions]; "
+                                            "beam [evals, expansions] (timed steps)"},
+            "unique_evaluations": uniq,
             "ari_vs_generator": ari_truth,
         }
         print(json.dumps(line), flush=True)

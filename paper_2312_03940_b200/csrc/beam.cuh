@@ -68,6 +68,9 @@ struct SearchParams {
     const unsigned* X8;        // packed u8 rows (u8 mode only)
     int dw;
     int screen = 1;            // float data: fp32 pre-screen against a full beam (PK_SCREEN)
+    unsigned* ubm = nullptr;   // counting mode: per-warp bitmaps of evaluated ids (exact unique count)
+    int uwords = 0;            // 32-bit words per bitmap
+    long long n_points = 0;    // n (bitmap size in counting mode)
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -94,6 +97,8 @@ struct WarpBeam {
     int vl;
     unsigned* err;
     long long evals;  // distance evaluations (lane 0 count)
+    unsigned* ubm;    // counting mode only: this warp's bitmap of evaluated ids
+    long long uniq;   // distinct ids evaluated (the roofline's U)
 
     __device__ void init(const BeamSmem& s_, int L_, unsigned* vi, double* vd, int vcap_, unsigned* err_) {
         sm = s_;
@@ -108,6 +113,8 @@ struct WarpBeam {
         vl = 0;
         err = err_;
         evals = 0;
+        ubm = nullptr;
+        uniq = 0;
         unsigned* h32 = reinterpret_cast<unsigned*>(sm.hash);
         for (unsigned h = lane_id(); h <= sm.hmask / 2; h += 32) h32[h] = 0xffffffffu;
         __syncwarp();
@@ -214,6 +221,23 @@ struct WarpBeam {
         __syncwarp();
     }
 
+    // counting mode: mark the ids held by lanes < cnt, count the first sightings
+    __device__ void count_unique(unsigned id, int cnt) {
+        if (!ubm) return;
+        const int lane = lane_id();
+        bool fresh = false;
+        if (lane < cnt) fresh = !(atomicOr(ubm + (id >> 5), 1u << (id & 31)) & (1u << (id & 31)));
+        const unsigned b = __ballot_sync(PK_FULL, fresh);
+        uniq += __popc(b);
+    }
+    __device__ void begin_counting(unsigned* bm, int words) {
+        ubm = bm;
+        if (!bm) return;
+        for (int w = lane_id(); w < words; w += 32) bm[w] = 0u;
+        __syncwarp();
+        __threadfence_block();
+    }
+
     // Seed with the start set (batch insert of ceil(s/32) chunks).  `unique`:
     // the start list is strictly increasing (sample_starts' sorted draw), so a
     // batch cannot hold equal keys and the duplicate pass of merge is skipped.
@@ -224,6 +248,7 @@ struct WarpBeam {
             const int cnt = min(32, P.s - b);
             unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
             if (hash_starts && lane < cnt) seen_or_insert(sm.hash, sm.hmask, sm.hbits, id);
+            count_unique(id, cnt);
             double dd = dist.eval(P.X, (int)id, cnt);
             if (lane == 0) evals += cnt;
             if (unique) merge<false>(dd, id, lane < cnt);
@@ -351,6 +376,7 @@ struct WarpBeam {
             int cnt = min(32, c - g);
             unsigned cid = lane < cnt ? sm.cbuf[g + lane] : 0u;
             if (lane == 0) evals += cnt;
+            count_unique(cid, cnt);
             if constexpr (has_screen<D>::value) {
                 // float data, full beam: drop the candidates whose fp32 lower bound
                 // already exceeds the worst key (they would be rejected by merge);

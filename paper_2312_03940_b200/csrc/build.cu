@@ -60,15 +60,17 @@ __global__ void __launch_bounds__(128, 8) build_search_kernel(BuildArgs A) {
     const int lane = lane_id();
     BeamSmem sm = carve_beam(smem + (size_t)wib * A.search_bytes, A.L, A.H);
     const MakeAt<MODE, QV> make{A.D};
-    long long ev = 0, expansions = 0;
+    long long ev = 0, expansions = 0, un = 0;
     const bool uniq = starts_increasing(A.P);
     for (int t = blockIdx.x * wpb + wib; t < A.m; t += gridDim.x * wpb) {
         const unsigned p = (unsigned)A.bids[t];
         auto dist = make(p);
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, A.L, A.vlog_i + (size_t)t * A.vcap, A.vlog_d + (size_t)t * A.vcap, A.vcap, A.err);
+        wb.begin_counting(A.P.ubm ? A.P.ubm + ((size_t)blockIdx.x * wpb + wib) * A.P.uwords : nullptr, A.P.uwords);
         wb.seed(A.P, dist, false, uniq);
         wb.walk(A.P, dist);
+        un += wb.uniq;
         ev += wb.evals;
         expansions += wb.vl;
         if (lane == 0) A.vlen[t] = min(wb.vl, A.vcap);
@@ -77,6 +79,7 @@ __global__ void __launch_bounds__(128, 8) build_search_kernel(BuildArgs A) {
     if (lane == 0 && A.stats) {
         atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 0), (unsigned long long)ev);
         atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 3), (unsigned long long)expansions);
+        if (A.P.ubm) atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 4), (unsigned long long)un);
     }
 }
 
@@ -1244,6 +1247,13 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
 
     A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s};
     A.P.screen = D.screen;
+    // counting mode (bench.py's untimed pass): exact distinct evaluations -> stats[4]
+    unsigned* ubm = nullptr;
+    if (stats && env_int("PK_COUNT_UNIQUE", 0) == 1) {
+        A.P.uwords = (n + 31) / 32;
+        PK_CHECK(scratch(&ubm, (size_t)grid_s * wpb_s * A.P.uwords, st));
+        A.P.ubm = ubm;
+    }
     A.D = D;
     A.L = L;
     A.H = H;
@@ -1412,7 +1422,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
-                    (void*)nmid, cub_tmp})
+                    (void*)nmid, (void*)ubm, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

@@ -21,15 +21,17 @@ __global__ void __launch_bounds__(128, 8) beam_knn_kernel(SearchParams P, const 
     const int lane = lane_id();
     unsigned char* mine = smem + (size_t)wib * warp_bytes;
     BeamSmem sm = carve_beam(mine, L, H);
-    long long ev = 0, ex = 0;
+    long long ev = 0, ex = 0, un = 0;
     const bool uniq = starts_increasing(P);
     for (long long t = (long long)blockIdx.x * wpb + wib; t < m; t += (long long)gridDim.x * wpb) {
         const unsigned qi = (unsigned)qids[t];
         auto dist = DistFor<MODE, QV>::make(P.data(), qi);
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, L, nullptr, nullptr, 0, nullptr);
+        wb.begin_counting(P.ubm ? P.ubm + ((size_t)blockIdx.x * wpb + wib) * P.uwords : nullptr, P.uwords);
         wb.seed(P, dist, false, uniq);
         wb.walk(P, dist);
+        un += wb.uniq;
         long long* oi = out_ids + t * kk;
         double* od = out_d + t * kk;
         int got = wb.emit(qi, kk, oi, od);
@@ -45,6 +47,7 @@ __global__ void __launch_bounds__(128, 8) beam_knn_kernel(SearchParams P, const 
     if (evals_out && lane == 0 && ev) {
         atomicAdd(reinterpret_cast<unsigned long long*>(evals_out), (unsigned long long)ev);
         atomicAdd(reinterpret_cast<unsigned long long*>(evals_out + 1), (unsigned long long)ex);
+        if (P.ubm) atomicAdd(reinterpret_cast<unsigned long long*>(evals_out + 2), (unsigned long long)un);
     }
 }
 
@@ -353,11 +356,21 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     long long cap = (long long)sm_count() * per_sm;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
+    // counting mode (bench.py's untimed pass): exact number of distinct ids
+    // evaluated, added to evals[2] (the caller then passes 3 counters)
+    SearchParams Pc = P;
+    unsigned* ubm = nullptr;
+    if (evals && env_int("PK_COUNT_UNIQUE", 0) == 1) {
+        Pc.uwords = (int)((P.n_points + 31) / 32);
+        PK_CHECK(scratch(&ubm, (size_t)grid * wpb * Pc.uwords, st));
+        Pc.ubm = ubm;
+    }
     {
         ProfScope _ps("beam_knn_kernel", st);
-        kern<<<grid, 32 * wpb, wb * wpb, st>>>(P, qids, m, L, kk, H, wb, out_ids, out_d, counts, evals);
+        kern<<<grid, 32 * wpb, wb * wpb, st>>>(Pc, qids, m, L, kk, H, wb, out_ids, out_d, counts, evals);
     }
     PK_CHECK_LAUNCH("beam_knn_kernel");
+    if (ubm) release(ubm, st);
     return 0;
 }
 
@@ -510,6 +523,7 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
     // dependent bitmap load on every neighbour.
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, x8, (int)dw};
     P.screen = env_int("PK_SCREEN", 1) == 1;
+    P.n_points = n;
     int H = choose_hash((int)L, hash_bits, n);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);
