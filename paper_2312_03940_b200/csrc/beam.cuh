@@ -71,6 +71,7 @@ struct SearchParams {
     unsigned* ubm = nullptr;   // counting mode: per-warp bitmaps of evaluated ids (exact unique count)
     int uwords = 0;            // 32-bit words per bitmap
     long long n_points = 0;    // n (bitmap size in counting mode)
+    int prefetch = 1;          // L1 prefetch of the next expansion's adjacency row
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -305,7 +306,7 @@ struct WarpBeam {
                 visit_empty_run(P);
                 continue;
             }
-            {
+            if (P.prefetch) {
                 // prefetch the adjacency row of the next unvisited entry: it is
                 // the next expansion unless this one inserts something closer
                 const int pn = next_unvisited();

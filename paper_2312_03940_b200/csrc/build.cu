@@ -1247,6 +1247,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
 
     A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s};
     A.P.screen = D.screen;
+    A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     // counting mode (bench.py's untimed pass): exact distinct evaluations -> stats[4]
     unsigned* ubm = nullptr;
     if (stats && env_int("PK_COUNT_UNIQUE", 0) == 1) {

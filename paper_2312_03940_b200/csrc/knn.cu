@@ -524,6 +524,7 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, x8, (int)dw};
     P.screen = env_int("PK_SCREEN", 1) == 1;
     P.n_points = n;
+    P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     int H = choose_hash((int)L, hash_bits, n);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);
