@@ -164,6 +164,7 @@ def brute_tc_sample(n=131_072, k=16, reps=3):
     index.brute_device(p, q[:4096], k)
     torch.cuda.synchronize()
     _lib.prof_collect(reset=True)
+    _lib.prof_only(["tc_screen_kernel", "tc_rescore_kernel"])
     _lib.prof_enable(True)
     index.TC_STATS.update(rows=0, uncertified=0)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
