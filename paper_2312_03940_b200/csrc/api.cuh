@@ -65,8 +65,9 @@ int choose_hash(int L, int hash_bits, long long n);
 inline int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     if (!v || !*v) return dflt;
-    int x = std::atoi(v);
-    return x > 0 ? x : dflt;
+    char* end = nullptr;
+    const long x = std::strtol(v, &end, 10);
+    return (end && *end == 0 && x >= 0) ? (int)x : dflt;  // "0" switches a default-on knob off
 }
 
 // ---- launch accounting -------------------------------------------------------

@@ -72,6 +72,7 @@ struct SearchParams {
     int uwords = 0;            // 32-bit words per bitmap
     long long n_points = 0;    // n (bitmap size in counting mode)
     int prefetch = 1;          // L1 prefetch of the next expansion's adjacency row
+    int lazy = 1;              // float data: lazy keys (fp32 screen values until a decision needs the exact one)
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -89,7 +90,7 @@ struct WarpBeam {
     int L;
     int bl;        // beam length (warp-uniform)
     int cursor;    // every entry below cursor is visited
-    double ev_d;   // best evicted visited entry (per-lane running min)
+    double ev_d;   // best evicted visited entry (warp-uniform; PK_APX in ev_i for a lazy key)
     unsigned ev_i;
     // optional visit log (build)
     unsigned* vlog_i;
@@ -100,6 +101,8 @@ struct WarpBeam {
     long long evals;  // distance evaluations (lane 0 count)
     unsigned* ubm;    // counting mode only: this warp's bitmap of evaluated ids
     long long uniq;   // distinct ids evaluated (the roofline's U)
+    bool lazy;        // lazy keys (float data, set by seed())
+    long long exact;  // exact float64 evaluations in lazy mode (lane 0 count)
 
     __device__ void init(const BeamSmem& s_, int L_, unsigned* vi, double* vd, int vcap_, unsigned* err_) {
         sm = s_;
@@ -116,6 +119,8 @@ struct WarpBeam {
         evals = 0;
         ubm = nullptr;
         uniq = 0;
+        lazy = false;
+        exact = 0;
         unsigned* h32 = reinterpret_cast<unsigned*>(sm.hash);
         for (unsigned h = lane_id(); h <= sm.hmask / 2; h += 32) h32[h] = 0xffffffffu;
         __syncwarp();
@@ -126,10 +131,11 @@ struct WarpBeam {
     // in a user start list) -- keep the lowest lane.  Graph neighbours of one
     // expansion are distinct, so the walk skips that pass.
     template <bool CheckDups>
-    __device__ void merge(double cd, unsigned cid, bool valid) {
+    __device__ void merge(double cd, unsigned cidf, bool valid) {
         const int lane = lane_id();
         double* bd = sm.bd;
         unsigned* bi = sm.bi;
+        const unsigned cid = cidf & PK_IDMASK;  // cidf may carry PK_APX (stored with the entry)
         int pos = 0;
         bool keep = valid;
         // a full beam rejects anything not better than its worst entry
@@ -179,6 +185,14 @@ struct WarpBeam {
         __syncwarp();
         const int minpos = sm.spos[0];
         const int nbl = min(L, bl + c);
+        // best evicted visited entry: every entry evicted by a merge is above
+        // every key left in the beam, and the beam's L-th key never increases,
+        // so later evictions are always below earlier ones -- the best one is
+        // the lowest-positioned visited entry of the latest evicting merge (no
+        // key comparison, so it also holds for lazy keys)
+        int evn = 0x7fffffff;
+        double evd = 0.0;
+        unsigned evi = 0u;
         // shift the tail [minpos, bl) right, top-down in chunks of 32
         for (int top = bl - 1; top >= minpos; top -= 32) {
             const int e = top - lane;
@@ -202,23 +216,235 @@ struct WarpBeam {
                 if (ne < L) {
                     bd[ne] = de;
                     bi[ne] = ie;
-                } else if ((ie & PK_VIS) && key_lt(de, ie & PK_IDMASK, ev_d, ev_i)) {
-                    ev_d = de;
-                    ev_i = ie & PK_IDMASK;
+                } else if ((ie & PK_VIS) && ne < evn) {
+                    evn = ne;
+                    evd = de;
+                    evi = ie & ~PK_VIS;
                 }
             }
             __syncwarp();
         }
+        int mev = evn;
+#pragma unroll
+        for (int s = 16; s; s >>= 1) mev = min(mev, __shfl_xor_sync(PK_FULL, mev, s));
+        if (mev != 0x7fffffff) {
+            const int src = __ffs(__ballot_sync(PK_FULL, evn == mev)) - 1;
+            ev_d = __shfl_sync(PK_FULL, evd, src);
+            ev_i = __shfl_sync(PK_FULL, evi, src);
+        }
         const int np = pos + rank;
         if (keep && np < L) {
             bd[np] = cd;
-            bi[np] = cid;
+            bi[np] = cidf;
         }
         int mn = (keep && np < L) ? np : 0x7fffffff;
 #pragma unroll
         for (int s = 16; s; s >>= 1) mn = min(mn, __shfl_xor_sync(PK_FULL, mn, s));
         if (mn < cursor) cursor = mn;
         bl = nbl;
+        __syncwarp();
+    }
+
+    // ---- lazy keys (float data) -------------------------------------------------
+    // Lane i < cnt: the level-1 lazy key of candidate cid (fp32 screen value,
+    // PK_APX|PK_A32 in cidf); where the fp32 value is unusable (underflow /
+    // overflow) the float64 one (PK_APX, or exact when it is 0).
+    template <class D>
+    __device__ double approx(const SearchParams& P, const D& dist, unsigned cid, int cnt, unsigned& cidf) {
+        const int lane = lane_id();
+        float mine = 0.f;
+        for (int j = 0; j < cnt; j += 2) {
+            const int j1 = j + 1 < cnt ? j + 1 : j;
+            const float s0 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j));
+            const float s1 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j1));
+            if (lane == j) mine = s0;
+            if (lane == j1) mine = s1;
+        }
+        double v = (double)mine;
+        cidf = cid | PK_APX | PK_A32;
+        const unsigned bad = __ballot_sync(PK_FULL, lane < cnt && !screen_usable(mine));
+        for (unsigned b = bad; b; b &= b - 1) {
+            const int j = __ffs(b) - 1;
+            const double d64 = dist.dscreen(P.X, __shfl_sync(PK_FULL, cid, j));
+            if (lane == j) {
+                v = d64;
+                cidf = d64 == 0.0 ? cid : (cid | PK_APX);
+            }
+        }
+        return v;
+    }
+
+    // One refinement step of a lazy key: A32 -> A64 (warp-cooperative float64,
+    // `coop` lanes one at a time) or A64 -> exact (lane-parallel sequential
+    // float64, `seq` lanes).  Lane j refines (v, f) of row id.
+    template <class D>
+    __device__ void refine(const SearchParams& P, const D& dist, unsigned coop, unsigned seq, unsigned id, double& v,
+                           unsigned& f) {
+        const int lane = lane_id();
+        for (unsigned b = coop; b; b &= b - 1) {
+            const int j = __ffs(b) - 1;
+            const double d64 = dist.dscreen(P.X, __shfl_sync(PK_FULL, id, j));
+            if (lane == j) {
+                v = d64;
+                f = d64 == 0.0 ? (f & ~PK_LAZYF) : ((f & ~PK_A32) | PK_APX);
+            }
+        }
+        if (seq) {
+            if ((seq >> lane) & 1u) {
+                v = dist.eval_one(P.X, (int)id);
+                f &= ~PK_LAZYF;
+            }
+            if (lane == 0) exact += __popc(seq);
+        }
+    }
+
+    // Make every ordering decision of the coming merge certain.  Candidates
+    // certainly above the worst entry of a full beam, and ids already in the
+    // beam (lossy seen table), are dropped.  Every other lazy key that is in an
+    // uncertain pair -- candidate vs beam entry, candidate vs candidate, and
+    // (after a refinement moved a beam key) adjacent beam entries -- is refined
+    // one level, until no uncertain pair is left.  Afterwards key_lt on the
+    // stored values is the exact (dist, id) order of every pair merge() compares.
+    template <class D>
+    __device__ void resolve(const SearchParams& P, const D& dist, double& cd, unsigned& cidf, bool& valid) {
+        const int lane = lane_id();
+        unsigned* bi = sm.bi;
+        double* bd = sm.bd;
+        int* work = sm.spos;  // beam positions to refine (merge() reuses spos afterwards)
+        const unsigned cid = cidf & PK_IDMASK;
+        bool dirty = false;   // a beam key was refined: re-check adjacent beam pairs
+        for (;;) {
+            const double clo = key_lo(cd, cidf), chi = key_hi(cd, cidf);
+            int first = 0, last = 0;
+            if (valid) {
+                // lo and hi are non-decreasing along the beam (adjacent pairs are certain)
+                int lo = 0, hi = bl;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (key_hi(bd[mid], bi[mid]) < clo) lo = mid + 1;
+                    else hi = mid;
+                }
+                first = lo;
+                hi = bl;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (key_lo(bd[mid], bi[mid]) <= chi) lo = mid + 1;
+                    else hi = mid;
+                }
+                last = lo;
+                if (bl == L && first == bl) {
+                    valid = false;  // certainly above the worst entry of the full beam
+                } else {
+                    for (int e = first; e < last; ++e)
+                        if ((bi[e] & PK_IDMASK) == cid) valid = false;  // already in the beam
+                }
+            }
+            const bool capx = valid && (cidf & PK_APX);
+            // candidate vs beam: an overlapping pair is uncertain unless both are exact
+            bool own = false;
+            if (capx && first < last) own = true;
+            // candidate vs candidate
+            const unsigned vb = __ballot_sync(PK_FULL, valid);
+            for (unsigned b = vb; b; b &= b - 1) {
+                const int j = __ffs(b) - 1;
+                const double dj = __shfl_sync(PK_FULL, cd, j);
+                const unsigned fj = __shfl_sync(PK_FULL, cidf, j);
+                if (capx && j != lane && !key_certain_lt(dj, fj, cd, cidf) && !key_certain_lt(cd, cidf, dj, fj))
+                    own = true;
+            }
+            // beam entries to refine: lazy entries overlapping a valid candidate
+            int nw = 0;
+            int e = valid ? first : last;
+            for (;;) {
+                while (e < last && !(bi[e] & PK_APX)) ++e;
+                const bool has = e < last;
+                const unsigned hb = __ballot_sync(PK_FULL, has);
+                if (!hb) break;
+                const int at = nw + warp_excl_prefix(hb);
+                if (has && at < 32) work[at] = e;
+                nw = min(32, nw + __popc(hb));
+                if (has) ++e;
+                if (nw >= 32) break;
+            }
+            // after a refinement of beam keys: adjacent beam pairs that became uncertain
+            if (dirty) {
+                for (int base = 0; base + 1 < bl && nw < 32; base += 32) {
+                    const int x = base + lane;
+                    bool unc = false;
+                    if (x + 1 < bl) unc = !key_certain_lt(bd[x], bi[x], bd[x + 1], bi[x + 1]);
+                    const unsigned ub = __ballot_sync(PK_FULL, unc);
+                    // refine both lazy members of each uncertain pair
+                    const bool w0 = unc && (bi[x] & PK_APX), w1 = unc && (bi[x + 1] & PK_APX);
+                    const unsigned b0 = __ballot_sync(PK_FULL, w0), b1 = __ballot_sync(PK_FULL, w1);
+                    int at = nw + warp_excl_prefix(b0);
+                    if (w0 && at < 32) work[at] = x;
+                    nw = min(32, nw + __popc(b0));
+                    at = nw + warp_excl_prefix(b1);
+                    if (w1 && at < 32) work[at] = x + 1;
+                    nw = min(32, nw + __popc(b1));
+                    (void)ub;
+                }
+            }
+            const unsigned ob = __ballot_sync(PK_FULL, own);
+            if (!ob && !nw) break;
+            __syncwarp();
+            // refine the candidates
+            {
+                const unsigned coop = __ballot_sync(PK_FULL, own && (cidf & PK_A32));
+                const unsigned seq = ob & ~coop;
+                double v = cd;
+                unsigned f = cidf;
+                refine(P, dist, coop, seq, cid, v, f);
+                if (own) {
+                    cd = v;
+                    cidf = f;
+                }
+            }
+            // refine the listed beam entries (lane j takes work[j]; duplicates refine twice, harmlessly)
+            if (nw) {
+                const int pos = lane < nw ? work[lane] : 0;
+                unsigned f = lane < nw ? bi[pos] : 0u;
+                double v = lane < nw ? bd[pos] : 0.0;
+                const bool lz = lane < nw && (f & PK_APX);
+                const unsigned coop = __ballot_sync(PK_FULL, lz && (f & PK_A32));
+                const unsigned seq = __ballot_sync(PK_FULL, lz) & ~coop;
+                refine(P, dist, coop, seq, f & PK_IDMASK, v, f);
+                __syncwarp();
+                if (lz) {
+                    bd[pos] = v;
+                    bi[pos] = f;
+                }
+                __syncwarp();
+                dirty = true;
+            }
+        }
+    }
+
+    // lazy-mode batch insert: approx -> resolve -> merge
+    template <bool CheckDups, class D>
+    __device__ void insert_lazy(const SearchParams& P, const D& dist, unsigned cid, int cnt) {
+        unsigned cidf;
+        double v = approx(P, dist, cid, cnt, cidf);
+        bool valid = lane_id() < cnt;
+        resolve(P, dist, v, cidf, valid);
+        merge<CheckDups>(v, cidf, valid);
+    }
+
+    // build: exact distances for the visit-log entries logged with lazy keys
+    template <class D>
+    __device__ void finalize_log(const SearchParams& P, const D& dist) {
+        const int lane = lane_id();
+        const int nl = min(vl, vcap);
+        for (int x = lane; x - lane < nl; x += 32) {
+            const unsigned id = x < nl ? vlog_i[x] : 0u;
+            const bool apx = x < nl && (id & PK_APX);
+            const unsigned nb_ = __ballot_sync(PK_FULL, apx);
+            if (lane == 0) exact += __popc(nb_);
+            if (apx) {
+                vlog_d[x] = dist.eval_one(P.X, (int)(id & PK_IDMASK));
+                vlog_i[x] = id & PK_IDMASK;
+            }
+        }
         __syncwarp();
     }
 
@@ -245,11 +471,20 @@ struct WarpBeam {
     template <class D>
     __device__ void seed(const SearchParams& P, const D& dist, bool hash_starts, bool unique) {
         const int lane = lane_id();
+        if constexpr (has_screen<D>::value) lazy = P.screen && P.lazy && P.dp <= 128 * D::kQV;
         for (int b = 0; b < P.s; b += 32) {
             const int cnt = min(32, P.s - b);
             unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
             if (hash_starts && lane < cnt) seen_or_insert(sm.hash, sm.hmask, sm.hbits, id);
             count_unique(id, cnt);
+            if constexpr (has_screen<D>::value) {
+                if (lazy) {
+                    if (lane == 0) evals += cnt;
+                    if (unique) insert_lazy<false>(P, dist, id, cnt);
+                    else insert_lazy<true>(P, dist, id, cnt);
+                    continue;
+                }
+            }
             double dd = dist.eval(P.X, (int)id, cnt);
             if (lane == 0) evals += cnt;
             if (unique) merge<false>(dd, id, lane < cnt);
@@ -276,14 +511,15 @@ struct WarpBeam {
         for (;;) {
             const int pos = next_unvisited();
             if (pos < 0) break;
-            const unsigned p = sm.bi[pos] & PK_IDMASK;
+            const unsigned pf = sm.bi[pos] & PK_IDAPX;
+            const unsigned p = pf & PK_IDMASK;
             const double pd = sm.bd[pos];
             __syncwarp();
             if (lane == 0) {
-                sm.bi[pos] = p | PK_VIS;
+                sm.bi[pos] = pf | PK_VIS;
                 if (vlog_i) {
                     if (vl < vcap) {
-                        vlog_i[vl] = p;
+                        vlog_i[vl] = pf;
                         vlog_d[vl] = pd;
                     } else {
                         atomicOr(err, ERR_VISIT_OVERFLOW);
@@ -351,7 +587,7 @@ struct WarpBeam {
                 if (vlog_i) {
                     const int at = vl + __popc(run & ((1u << lane) - 1u));
                     if (at < vcap) {
-                        vlog_i[at] = iv & PK_IDMASK;
+                        vlog_i[at] = iv & PK_IDAPX;
                         vlog_d[at] = sm.bd[e];
                     } else {
                         atomicOr(err, ERR_VISIT_OVERFLOW);
@@ -378,6 +614,12 @@ struct WarpBeam {
             unsigned cid = lane < cnt ? sm.cbuf[g + lane] : 0u;
             if (lane == 0) evals += cnt;
             count_unique(cid, cnt);
+            if constexpr (has_screen<D>::value) {
+                if (lazy) {
+                    insert_lazy<false>(P, dist, cid, cnt);
+                    continue;
+                }
+            }
             if constexpr (has_screen<D>::value) {
                 // float data, full beam: drop the candidates whose fp32 lower bound
                 // already exceeds the worst key (they would be rejected by merge);
@@ -411,34 +653,42 @@ struct WarpBeam {
     // Member-query output: first kk entries of the beam without `self`, then
     // the best evicted visited entry if still short.  Returns the count.
     __device__ int emit(unsigned self, int kk, long long* out_ids, double* out_d) {
+        return emit(self, kk, out_ids, out_d, [](unsigned) { return 0.0; });
+    }
+    // lazy keys: emitted entries get their exact value from exact_of(id)
+    template <class F>
+    __device__ int emit(unsigned self, int kk, long long* out_ids, double* out_d, const F& exact_of) {
         const int lane = lane_id();
         int got = 0;
         for (int base = 0; base < bl && got < kk; base += 32) {
             int e = base + lane;
-            unsigned id = e < bl ? (sm.bi[e] & PK_IDMASK) : self;
+            const unsigned f = e < bl ? sm.bi[e] : 0u;
+            unsigned id = e < bl ? (f & PK_IDMASK) : self;
             bool ok = e < bl && id != self;
             unsigned b = __ballot_sync(PK_FULL, ok);
             int o = got + warp_excl_prefix(b);
-            if (ok && o < kk) {
+            const bool out = ok && o < kk;
+            const bool apx = out && (f & PK_APX);
+            double v = e < bl ? sm.bd[e] : 0.0;
+            if (__any_sync(PK_FULL, apx)) {
+                if (apx) v = exact_of(id);
+                const unsigned nb_ = __ballot_sync(PK_FULL, apx);
+            if (lane == 0) exact += __popc(nb_);
+            }
+            if (out) {
                 out_ids[o] = id;
-                out_d[o] = sm.bd[e];
+                out_d[o] = v;
             }
             got += __popc(b);
         }
         got = min(got, kk);
-        // warp-wide best evicted visited
-        double bd_ = ev_d;
-        unsigned bi_ = ev_i;
-#pragma unroll
-        for (int s = 16; s; s >>= 1) {
-            double od = __shfl_xor_sync(PK_FULL, bd_, s);
-            unsigned oi = __shfl_xor_sync(PK_FULL, bi_, s);
-            if (key_lt(od, oi, bd_, bi_)) { bd_ = od; bi_ = oi; }
-        }
-        if (got < kk && bi_ != 0xffffffffu && bi_ != self) {
+        // best evicted visited entry (warp-uniform, see merge)
+        const double bd_ = ev_d;
+        const unsigned bi_ = ev_i;
+        if (got < kk && bi_ != 0xffffffffu && (bi_ & PK_IDMASK) != self) {
             if (lane == 0) {
-                out_ids[got] = bi_;
-                out_d[got] = bd_;
+                out_ids[got] = bi_ & PK_IDMASK;
+                out_d[got] = (bi_ & PK_APX) ? exact_of(bi_ & PK_IDMASK) : bd_;
             }
             ++got;
         }

@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(128, 8) build_search_kernel(BuildArgs A) {
         wb.begin_counting(A.P.ubm ? A.P.ubm + ((size_t)blockIdx.x * wpb + wib) * A.P.uwords : nullptr, A.P.uwords);
         wb.seed(A.P, dist, false, uniq);
         wb.walk(A.P, dist);
+        if constexpr (has_screen<decltype(dist)>::value)
+            if (wb.lazy) wb.finalize_log(A.P, dist);
         un += wb.uniq;
         ev += wb.evals;
         expansions += wb.vl;
@@ -1146,6 +1148,10 @@ template <int MODE, int QV>
 int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
               int* adj, int* deg, long long* stats, int hash_bits, const Shard& SH, cudaStream_t st) {
     const bool u8 = MODE == MODE_EXACT_U8;
+    if ((long long)n > (long long)PK_IDMASK) {
+        set_error("too many points for the beam kernels (ids are 30-bit)");
+        return 2;
+    }
     const int H = choose_hash(L, hash_bits, n);
     const int cap = next_pow2(2 * L + 64 + R);
     const int vcap = cap - R;
@@ -1248,6 +1254,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s};
     A.P.screen = D.screen;
     A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
+    A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
     // counting mode (bench.py's untimed pass): exact distinct evaluations -> stats[4]
     unsigned* ubm = nullptr;
     if (stats && env_int("PK_COUNT_UNIQUE", 0) == 1) {

@@ -14,7 +14,11 @@
 
 #define PK_FULL 0xffffffffu
 #define PK_VIS 0x80000000u   // visited flag, stored in bit 31 of a beam id
-#define PK_IDMASK 0x7fffffffu
+#define PK_APX 0x40000000u   // lazy keys: the stored distance is an approximation (bit 30) ...
+#define PK_A32 0x20000000u   // ... from the fp32 screen (bit 29 set) or the float64 one (clear)
+#define PK_LAZYF 0x60000000u // both lazy-key flags
+#define PK_IDMASK 0x1fffffffu
+#define PK_IDAPX 0x7fffffffu // id + lazy-key flags (visit-log entries)
 
 namespace pk {
 
@@ -342,6 +346,33 @@ struct Seq64Screened : Seq64Member {
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, o);
         return acc;
     }
+    // Warp-cooperative float64 value of the squared distance (lazy keys): each
+    // lane accumulates its 4*QV coordinates with fma, then an xor butterfly
+    // (commutative adds: every lane ends with the same value).  Within
+    // (4*QV + 8) * 2^-53 relative of the exact sum, so within kLazyEps of the
+    // reference's sequential value (<= 2*dp roundings of 2^-53 each).
+    __device__ __forceinline__ double dscreen(const float* __restrict__ X, unsigned id) const {
+        const float4* a = reinterpret_cast<const float4*>(q);
+        const float4* r = reinterpret_cast<const float4*>(X + (size_t)id * dp);
+        const int nv = dp >> 2, lane = lane_id();
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < QV; ++j) {
+            const int f = lane + 32 * j;
+            if (f < nv) {
+                const float4 y = __ldg(a + f), x = __ldg(r + f);
+                const double d0 = (double)y.x - (double)x.x, d1 = (double)y.y - (double)x.y;
+                const double d2 = (double)y.z - (double)x.z, d3 = (double)y.w - (double)x.w;
+                acc = fma(d0, d0, acc);
+                acc = fma(d1, d1, acc);
+                acc = fma(d2, d2, acc);
+                acc = fma(d3, d3, acc);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, o);
+        return acc;
+    }
 };
 
 // distance policies whose values are exact integers below 2^32 (packed keys)
@@ -438,6 +469,34 @@ struct Fp32Pick {
         return s;
     }
 };
+
+// Lazy keys (beam searches on float data).  A beam entry stores one of
+//  * the fp32 warp-cooperative value a32 (Seq64Screened::screen; PK_APX|PK_A32):
+//    within (4*QV + 7) * 2^-24 <= 2.4e-6 relative of the exact sum for
+//    QV <= 8 when 1e-20 < a32 < 1e30 (no fp32 underflow / overflow), so the
+//    reference's sequential value D lies in [a (1 - kEps32), a (1 + kEps32)];
+//  * the float64 warp-cooperative value a64 (dscreen; PK_APX): both a64 and D
+//    are within 2*dp + 4*QV + 8 roundings of 2^-53 of the exact sum (< 2.4e-13
+//    for dp <= 1024), so D lies in [a (1 - kEps64), a (1 + kEps64)].  Every
+//    nonzero term is >= 2^-298 (the smallest fp32 difference, squared): no
+//    float64 underflow, and a64 == 0 means D == 0 exactly;
+//  * the exact value D (no flag).
+// Two keys whose intervals are disjoint are ordered by their stored values;
+// overlapping ones are refined one level at a time until they are not.
+constexpr double kEps32 = 4e-6;
+constexpr double kEps64 = 1e-12;
+__device__ __forceinline__ double key_eps(unsigned i) {
+    return (i & PK_APX) ? ((i & PK_A32) ? kEps32 : kEps64) : 0.0;
+}
+__device__ __forceinline__ double key_lo(double v, unsigned i) { return v * (1.0 - key_eps(i)); }
+__device__ __forceinline__ double key_hi(double v, unsigned i) { return v * (1.0 + key_eps(i)); }
+// is (va, ia) < (vb, ib) certain from the two intervals?
+__device__ __forceinline__ bool key_certain_lt(double va, unsigned ia, double vb, unsigned ib) {
+    if (!((ia | ib) & PK_APX)) return key_lt(va, ia & PK_IDMASK, vb, ib & PK_IDMASK);
+    return key_hi(va, ia) < key_lo(vb, ib);
+}
+// fp32 screen values usable as level-1 lazy keys
+__device__ __forceinline__ bool screen_usable(float s) { return s > 1e-20f && s < 1e30f; }
 
 // Verdict of "alpha2 * d <= k" from a screened d~ (fp32): 1 = true, 0 = false,
 // 2 = too close to call (the caller computes the exact float64 distance).

@@ -34,7 +34,11 @@ __global__ void __launch_bounds__(128, 8) beam_knn_kernel(SearchParams P, const 
         un += wb.uniq;
         long long* oi = out_ids + t * kk;
         double* od = out_d + t * kk;
-        int got = wb.emit(qi, kk, oi, od);
+        int got;
+        if constexpr (has_screen<decltype(dist)>::value)
+            got = wb.emit(qi, kk, oi, od, [&](unsigned id) { return dist.eval_one(P.X, (int)id); });
+        else
+            got = wb.emit(qi, kk, oi, od);
         for (int x = got + lane; x < kk; x += 32) {
             oi[x] = -1;
             od[x] = __longlong_as_double(0x7ff0000000000000LL);
@@ -518,6 +522,10 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
         set_error("beam width L must be >= k");
         return 2;
     }
+    if (n > (int64_t)PK_IDMASK) {
+        set_error("too many points for the beam kernels (ids are 30-bit)");
+        return 2;
+    }
     // Start points re-met as neighbours are simply re-evaluated (and dropped
     // by the key-equality check when already in the beam): cheaper than a
     // dependent bitmap load on every neighbour.
@@ -525,6 +533,7 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
     P.screen = env_int("PK_SCREEN", 1) == 1;
     P.n_points = n;
     P.prefetch = env_int("PK_PREFETCH", 1) == 1;
+    P.lazy = env_int("PK_LAZY", 1) == 1 && n < (int64_t)PK_IDMASK;
     int H = choose_hash((int)L, hash_bits, n);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);

@@ -268,6 +268,38 @@ def test_fp32_screened_beam_search_equals_float64(monkeypatch):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("case", ["c5", "dup128"])
+def test_lazy_keys_equal_eager(monkeypatch, case):
+    """Float data: beam searches holding fp32 screen values as lazy keys
+    (exact float64 only where an ordering decision or an output needs it)
+    build the same graph and return the same kNN rows, distances and labels
+    as the eager float64 searches (PK_LAZY=0)."""
+    if case == "c5":
+        data, _ = workloads.generate("C5", n=6_000, components=8)
+    else:
+        rng = np.random.default_rng(3)
+        hubs = rng.normal(size=(12, 128))
+        lab = rng.integers(0, 12, 5_000)
+        data = (hubs[lab] + 0.1 * rng.normal(size=(5_000, 128))).astype(np.float32)
+        data[:60] = hubs[lab[:60]]  # exact duplicates: zero distances and tied keys
+        data[60:90] = data[100:130]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PK_LAZY", flag)
+        p = pk.PointSet(data)
+        assert p.mode == _lib.MODE_SEQ64
+        res = pk.run_pipeline(p, pk.VamanaConfig(R=24, L_build=64, L=64, alpha=1.1, seed=0), k=16,
+                              density_kind="kth", center_policy=pk.ProductCenter(8), noise_policy=pk.NoisePolicy(0.0),
+                              doubling_params=pk.DoublingParams(initial_k=32, threshold=50))
+        st = res.state
+        g = pk.build_vamana(p, R=32, L_build=96, alpha=1.2, seed=1, query_beam=128)
+        nb = g.knn_all(40)
+        out[flag] = [st.neighbors.ids, st.neighbors.dists, st.rho, st.lam, st.delta, res.clustering.labels,
+                     g.graph.adjacency, nb.ids, nb.dists]
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
+
+
 def test_pointset_device_validation_reports_first_nonfinite():
     """With a GPU the PointSet check runs on the device (pk_scan_points); the
     error names the same first (point, dimension) as numpy's argwhere."""
