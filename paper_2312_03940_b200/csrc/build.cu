@@ -21,6 +21,7 @@
 #include "../../include/peakann_b200.h"
 #include "api.cuh"
 #include "beam.cuh"
+#include "tc_common.cuh"
 
 namespace pk {
 
@@ -811,9 +812,10 @@ __global__ void __launch_bounds__(BP_THREADS) build_prune_block_kernel(BuildArgs
         bp_sort(S.kd, S.ki, P);
         const int c = bp_unique(S, c0, p);
         int* out = A.new_ids + (size_t)t * R;
+        // the build always prunes (_kernels.py:370), even c <= R candidates
         int sel = c;
-        if (c <= R) {
-            for (int x = tid; x < c; x += BP_THREADS) out[x] = (int)S.ki2[x];
+        if (c <= 1) {
+            if (tid == 0 && c == 1) out[0] = (int)S.ki2[0];
         } else {
             sel = bp_prune(A.D.X8, S, c, A.alpha2, R, out, &pairs);
         }
@@ -911,6 +913,8 @@ __global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A, in
     }
     if (tid == 0 && A.stats && ev) atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 2), (unsigned long long)ev);
 }
+
+#include "prune_tc.cuh"
 
 // one thread, one full distance between two point ids (exact in every mode)
 template <int MODE>
@@ -1190,6 +1194,23 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rbk, BP_THREADS, bp_smem_bytes(kRevCap)));
         grid_rb = sm_count() * std::max(1, per_sm);
     }
+    // float data (SEQ64, dp <= 1024): block-per-item RobustPrune on the tensor cores
+    const int tcmode = env_int("PK_TC_PRUNE", 1);  // 1: build + reverse, 2: build only, 3: reverse only
+    const bool tcp = MODE == MODE_SEQ64 && D.dp <= 128 * QV && QV <= 8 && D.screen && tcmode >= 1 && tcmode <= 3;
+    const bool tcb = tcp && tcmode != 3, tcr = tcp && tcmode != 2;
+    auto tpk = prune_tc_build_kernel<QV>;
+    auto trk = prune_tc_reverse_kernel<MODE, QV>;
+    double* nrm64 = nullptr;
+    if (tcp) {
+        PK_CHECK(cudaFuncSetAttribute(tpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_SMEM));
+        PK_CHECK(cudaFuncSetAttribute(trk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_SMEM));
+        PK_CHECK(scratch(&nrm64, (size_t)n, st));
+        {
+            ProfScope _ps("norms64_kernel", st);
+            norms64_kernel<<<sm_count() * 8, 256, 0, st>>>(D.X, n, D.dp, nrm64);
+        }
+        PK_CHECK_LAUNCH("norms64_kernel");
+    }
     const int capB = 8192;
     const size_t big_bytes = (size_t)capB * 13 + 16;
     auto bigk = reverse_big_kernel<MODE, QV>;
@@ -1322,9 +1343,12 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                 sk<<<std::min(grid_s, (my_m + wpb_s - 1) / wpb_s), 32 * wpb_s, A.search_bytes * wpb_s, st>>>(A);
             }
             PK_CHECK_LAUNCH("build_search_kernel");
-            if (blockp) {
+            if (blockp || tcb) {
                 PK_CHECK(cudaMemsetAsync(nover, 0, sizeof(int), st));
-                {
+                if (tcb) {
+                    ProfScope _ps("prune_tc_build_kernel", st);
+                    tpk<<<std::min(sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, nrm64, over, nover);
+                } else {
                     ProfScope _ps("build_prune_block_kernel", st);
                     bpk<<<std::min(grid_bp, my_m), BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(A, over, nover);
                 }
@@ -1387,6 +1411,9 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                 ProfScope _ps("reverse_block_kernel", st);
                 rbk<<<grid_bp, BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(B, BP_CAP, midl, nmid, nullptr, nullptr);
             }
+        } else if (tcr) {
+            ProfScope _ps("prune_tc_reverse_kernel", st);
+            trk<<<std::min(sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, nrm64);
         } else {
             ProfScope _ps("reverse_kernel", st);
             rk<<<std::min(grid_r, (ubb + wpb_r - 1) / wpb_r), 32 * wpb_r, wbr * wpb_r, st>>>(B);
@@ -1430,7 +1457,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
-                    (void*)nmid, (void*)ubm, cub_tmp})
+                    (void*)nmid, (void*)ubm, (void*)nrm64, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

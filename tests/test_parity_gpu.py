@@ -300,6 +300,51 @@ def test_lazy_keys_equal_eager(monkeypatch, case):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("case", ["c5", "c4", "dup128"])
+def test_tensor_core_prune_equals_warp_prune(monkeypatch, case):
+    """Float data: RobustPrune decided from tcgen05 tf32 Gram tiles with a
+    rigorous error bound (uncertain pairs decided exactly) builds the same graph
+    as the warp-per-item screened prune (PK_TC_PRUNE=0)."""
+    if case == "c5":
+        data, _ = workloads.generate("C5", n=6_000, components=8)
+    elif case == "c4":
+        data, _ = workloads.generate("C4", n=8_000, components=40)
+    else:
+        rng = np.random.default_rng(5)
+        hubs = rng.normal(size=(10, 128)) * 3.0
+        lab = rng.integers(0, 10, 6_000)
+        data = (hubs[lab] + 0.2 * rng.normal(size=(6_000, 128))).astype(np.float32)
+        data[:50] = hubs[lab[:50]]
+        data[50:80] = data[200:230]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PK_TC_PRUNE", flag)
+        p = pk.PointSet(data)
+        g = pk.build_vamana(p, R=32, L_build=96, alpha=1.2, seed=2, query_beam=96)
+        out[flag] = (g.graph.adjacency.copy(), g.graph.degrees.copy())
+    assert np.array_equal(out["0"][1], out["1"][1])
+    assert np.array_equal(out["0"][0], out["1"][0])
+
+
+@pytest.mark.parametrize("kind", ["u8", "float"])
+def test_build_with_short_candidate_lists_matches_oracle(kind):
+    """L_build < R: many items have at most R candidates, and the build still
+    runs RobustPrune on them (_kernels.py:370) -- in the block kernels too."""
+    rng = np.random.default_rng(11)
+    if kind == "u8":
+        mu = rng.uniform(0, 255, (20, 128))
+        data = np.clip(np.round(mu[rng.integers(0, 20, 2_500)] + rng.normal(0, 20, (2_500, 128))), 0, 255)
+        data = data.astype(np.float32)
+    else:
+        data = (rng.normal(size=(2_500, 64)) + 3.0 * rng.normal(size=(12, 64))[rng.integers(0, 12, 2_500)])
+        data = data.astype(np.float32)
+    p = pk.PointSet(data)
+    g = pk.build_vamana(p, R=32, L_build=12, alpha=1.2, seed=4)
+    adj, deg, starts = oracle.build_vamana(data, R=32, L_build=12, alpha=1.2, seed=4)[:3]
+    assert np.array_equal(g.graph.degrees, deg)
+    assert np.array_equal(g.graph.adjacency, adj)
+
+
 def test_pointset_device_validation_reports_first_nonfinite():
     """With a GPU the PointSet check runs on the device (pk_scan_points); the
     error names the same first (point, dimension) as numpy's argwhere."""
