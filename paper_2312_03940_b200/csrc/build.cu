@@ -1347,7 +1347,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                 PK_CHECK(cudaMemsetAsync(nover, 0, sizeof(int), st));
                 if (tcb) {
                     ProfScope _ps("prune_tc_build_kernel", st);
-                    tpk<<<std::min(sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, nrm64, over, nover);
+                    tpk<<<std::min(2 * sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, nrm64, over, nover);
                 } else {
                     ProfScope _ps("build_prune_block_kernel", st);
                     bpk<<<std::min(grid_bp, my_m), BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(A, over, nover);
@@ -1413,7 +1413,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             }
         } else if (tcr) {
             ProfScope _ps("prune_tc_reverse_kernel", st);
-            trk<<<std::min(sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, nrm64);
+            trk<<<std::min(2 * sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, nrm64);
         } else {
             ProfScope _ps("reverse_kernel", st);
             rk<<<std::min(grid_r, (ubb + wpb_r - 1) / wpb_r), 32 * wpb_r, wbr * wpb_r, st>>>(B);

@@ -8,8 +8,9 @@
 //  * the Gram matrix G = C C^T of the candidate rows is one tcgen05 GEMM
 //    (kind::tf32, fp32 accumulators in TMEM): the rows stream through shared
 //    memory in 32-float K chunks (cp.async gathers into the 128-byte-swizzled
-//    K-major layout, 4 stages), tile 0 = rows 0-127 x columns 0-255 (TMEM
-//    columns 0-255), tile 1 = rows 128-255 x columns 128-255 (columns 256-383);
+//    K-major layout, 2 stages), pass 0 = rows 0-127 x columns 0-255, pass 1 =
+//    rows 128-255 x columns 128-255, each into the CTA's 256 TMEM columns (two
+//    CTAs per SM, so one item's staging overlaps the other's sort / greedy);
 //  * the epilogue (thread = TMEM lane = candidate row) forms
 //    d~ = |t|^2 + |u|^2 - 2 G~ (float64 norms precomputed once per build) and a
 //    rigorous bound E = 2 eg |t||u| + 1e-12 (|t|^2 + |u|^2) with
@@ -29,22 +30,26 @@
 // uses (BuildArgs, RevArgs, BPSmem, bp_sort, bp_unique, prune_by_selection).
 #pragma once
 
-constexpr int PT_CAP = 256;
+constexpr int PT_CAP = 512;   // unique candidates per item (bit rows in 128-row blocks)
+constexpr int PT_SORT = 512;  // candidates sorted per item
+constexpr int PT_WORDS = PT_CAP / 32;  // bit words per row
 constexpr int PT_THREADS = 128;
-constexpr int PT_STAGES = 4;
-constexpr int PT_STAGE_BYTES = PT_CAP * 128;  // 256 rows x 32 fp32
+constexpr int PT_STAGES = 2;  // two CTAs per SM (TMEM 2 x 256 columns, smem 2 x ~100 KB)
+constexpr int PT_STAGE_BYTES = 256 * 128;  // 256 row slots x 32 fp32
 constexpr size_t PT_SMEM = 1024 + (size_t)PT_STAGES * PT_STAGE_BYTES  // K-chunk stages
-                           + (size_t)PT_CAP * 8 * 4                    // kd, kd2, nrm, sq (f64)
-                           + (size_t)PT_CAP * 4 * 2                    // ki, ki2
-                           + (size_t)PT_CAP * 8 * 4 * 2                // kill, unc bit rows
+                           + (size_t)PT_SORT * 8 * 2 + (size_t)PT_CAP * 8 * 2  // kd, kd2, nrm, sq (f64)
+                           + (size_t)PT_SORT * 4 * 2                   // ki, ki2
+                           + (size_t)128 * PT_WORDS * 4 * 2            // kill, unc bit rows (one block)
+                           + (size_t)PT_CAP * 8                        // row pointers
                            + 256;                                      // barriers, scalars
 
 struct PTSmem {
-    unsigned char* stage;  // [PT_STAGES][PT_CAP][128 B], 1024-aligned
+    unsigned char* stage;  // [PT_STAGES][256][128 B], 1024-aligned
     double* nrm;           // [PT_CAP] |x|^2 of the sorted candidates
     double* sq;            // [PT_CAP] |x|
-    unsigned* kill;        // [PT_CAP][8]
-    unsigned* unc;         // [PT_CAP][8]
+    unsigned* kill;        // [128][PT_WORDS] bit rows of the current 128-candidate block
+    unsigned* unc;         // [128][PT_WORDS]
+    unsigned long long* rowp;  // [PT_CAP] global address of each sorted candidate row
     unsigned long long* bar;  // [PT_STAGES] MMAs of the stage's chunk done
     unsigned* tmem_slot;
     BPSmem S;              // kd, ki, kd2, ki2, scal (bp_sort / bp_unique)
@@ -56,14 +61,15 @@ __device__ __forceinline__ PTSmem carve_pt(unsigned char* raw) {
     P.stage = base;
     unsigned char* q = base + (size_t)PT_STAGES * PT_STAGE_BYTES;
     P.S.kd = reinterpret_cast<double*>(q);
-    P.S.kd2 = P.S.kd + PT_CAP;
-    P.nrm = P.S.kd2 + PT_CAP;
+    P.S.kd2 = P.S.kd + PT_SORT;
+    P.nrm = P.S.kd2 + PT_SORT;
     P.sq = P.nrm + PT_CAP;
     P.S.ki = reinterpret_cast<unsigned*>(P.sq + PT_CAP);
-    P.S.ki2 = P.S.ki + PT_CAP;
-    P.kill = P.S.ki2 + PT_CAP;
-    P.unc = P.kill + PT_CAP * 8;
-    P.bar = reinterpret_cast<unsigned long long*>(P.unc + PT_CAP * 8);
+    P.S.ki2 = P.S.ki + PT_SORT;
+    P.kill = P.S.ki2 + PT_SORT;
+    P.unc = P.kill + 128 * PT_WORDS;
+    P.rowp = reinterpret_cast<unsigned long long*>(P.unc + 128 * PT_WORDS);
+    P.bar = P.rowp + PT_CAP;
     P.tmem_slot = reinterpret_cast<unsigned*>(P.bar + PT_STAGES + 1);
     P.S.scal = reinterpret_cast<int*>(P.tmem_slot + 2);
     P.S.rows = nullptr;
@@ -120,16 +126,28 @@ __global__ void norms64_kernel(const float* __restrict__ X, long long n, int dp,
     }
 }
 
-// Copy K chunk kc (floats 32 kc .. 32 kc + 31) of the c sorted candidates into
-// stage buffer `st`: row r at r * 128 bytes, 16-byte piece j at (j ^ (r & 7)).
-__device__ __forceinline__ void pt_stage_chunk(const float* __restrict__ X, int dp, const unsigned* ki2, int c, int kc,
-                                               unsigned char* st) {
-    for (int e = threadIdx.x; e < c * 8; e += PT_THREADS) {
-        const int r = e >> 3, j = e & 7;
-        const int col = kc * 32 + j * 4;
-        unsigned char* dst = st + r * 128 + ((j ^ (r & 7)) << 4);
+// Copy K chunk kc (floats 32 kc .. 32 kc + 31) of the pass's rows into stage
+// buffer `st` (slot x at x * 128 bytes, 16-byte piece j at (j ^ (x & 7))):
+// A rows r0 .. r0 + na - 1 at slots 0 .., and, when the B block is separate
+// (b0 != r0), B rows b0 .. b0 + nb - 1 at slots 128 ..
+__device__ __forceinline__ void pt_stage_chunk(const float* __restrict__ X, int dp, const unsigned long long* rowp,
+                                               int r0, int na, int b0, int nb, int kc, unsigned char* st) {
+    const int col0 = kc * 32;
+    const int tot = (b0 == r0) ? nb : 128 + nb;
+    for (int e = threadIdx.x; e < tot * 8; e += PT_THREADS) {
+        const int x = e >> 3, j = e & 7;
+        int r;
+        if (b0 == r0) r = r0 + x;
+        else if (x < 128) {
+            if (x >= na) continue;
+            r = r0 + x;
+        } else {
+            r = b0 + x - 128;
+        }
+        const int col = col0 + j * 4;
+        unsigned char* dst = st + x * 128 + ((j ^ (x & 7)) << 4);
         if (col < dp) {
-            const float* src = X + (size_t)ki2[r] * dp + col;
+            const float* src = reinterpret_cast<const float*>(rowp[r]) + col;
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
         } else {
             *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -138,20 +156,23 @@ __device__ __forceinline__ void pt_stage_chunk(const float* __restrict__ X, int 
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-// Gram matrix of the c (<= 256) sorted candidates into TMEM (tile 0 at column
-// 0, tile 1 at column 256), then the occlusion / uncertain bit rows.
+// One Gram pass: rows r0 .. r0 + 127 (A) x columns b0 .. b0 + nb - 1 (B) of the
+// sorted candidates into TMEM columns 0 .. N - 1 (nb <= 256 when b0 == r0, else
+// <= 128), then the occlusion / uncertain bit words of rows r0 + tid for those
+// columns (pairs u > t only).
 template <int QV>
-__device__ void pt_gram_bits(const float* __restrict__ X, int dp, const PTSmem& P, PTPipe& pp, int c, double alpha2) {
+__device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& P, PTPipe& pp, int c, int r0, int b0,
+                             int nb, double alpha2) {
     const int tid = threadIdx.x;
     const int nk = (dp + 31) >> 5;
-    const int n0 = min(256, (c + 15) & ~15);
-    const bool two = c > 128;
-    const int n1 = two ? ((c - 128 + 15) & ~15) : 0;
-    const unsigned id0 = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(n0 >> 3) << 17) | ((128u >> 4) << 24);
-    const unsigned id1 = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(n1 >> 3) << 17) | ((128u >> 4) << 24);
+    const int na = min(128, c - r0);
+    const int ncol = (nb + 15) & ~15;
+    const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(ncol >> 3) << 17) | ((128u >> 4) << 24);
+    const unsigned long long* rowp = P.rowp;
+    const unsigned boff = (b0 == r0) ? 0u : 128u * 128u;  // B operand offset inside a stage
     // prologue: chunks 0 .. PT_STAGES - 2
     for (int k = 0; k < PT_STAGES - 1; ++k) {
-        if (k < nk) pt_stage_chunk(X, dp, P.S.ki2, c, k, P.stage + (size_t)k * PT_STAGE_BYTES);
+        if (k < nk) pt_stage_chunk(X, dp, rowp, r0, na, b0, nb, k, P.stage + (size_t)k * PT_STAGE_BYTES);
         else asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     for (int kc = 0; kc < nk; ++kc) {
@@ -162,7 +183,7 @@ __device__ void pt_gram_bits(const float* __restrict__ X, int dp, const PTSmem& 
             mbar_wait(P.bar + sn, (pp.phase >> sn) & 1u);
             pp.phase ^= 1u << sn;
         }
-        if (kn < nk) pt_stage_chunk(X, dp, P.S.ki2, c, kn, P.stage + (size_t)sn * PT_STAGE_BYTES);
+        if (kn < nk) pt_stage_chunk(X, dp, rowp, r0, na, b0, nb, kn, P.stage + (size_t)sn * PT_STAGE_BYTES);
         else asm volatile("cp.async.commit_group;\n" ::: "memory");
         asm volatile("cp.async.wait_group %0;\n" ::"n"(PT_STAGES - 1) : "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -171,17 +192,15 @@ __device__ void pt_gram_bits(const float* __restrict__ X, int dp, const PTSmem& 
             tc_fence_after();
             const int s = kc % PT_STAGES;
             unsigned char* sb = P.stage + (size_t)s * PT_STAGE_BYTES;
-            const unsigned long long d0 = umma_desc_sw128(sb);
-            const unsigned long long d1 = umma_desc_sw128(sb + 128 * 128);
+            const unsigned long long da = umma_desc_sw128(sb);
+            const unsigned long long db = umma_desc_sw128(sb + boff);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {  // 8 tf32 = 32 bytes per UMMA_K step
-                tc_mma_tf32(pp.tmem, d0 + 2ull * k, d0 + 2ull * k, id0, (kc | k) != 0);
-                if (two) tc_mma_tf32(pp.tmem + 256u, d1 + 2ull * k, d1 + 2ull * k, id1, (kc | k) != 0);
-            }
+            for (int k = 0; k < 4; ++k)  // 8 tf32 = 32 bytes per UMMA_K step
+                tc_mma_tf32(pp.tmem, da + 2ull * k, db + 2ull * k, idesc, (kc | k) != 0);
             tc_commit(P.bar + s);
         }
     }
-    // the last chunk's commit tracks every MMA of the item
+    // the last chunk's commit tracks every MMA of the pass
     {
         const int s = (nk - 1) % PT_STAGES;
         mbar_wait(P.bar + s, (pp.phase >> s) & 1u);
@@ -189,76 +208,80 @@ __device__ void pt_gram_bits(const float* __restrict__ X, int dp, const PTSmem& 
     }
     tc_fence_after();
 
-    // epilogue: thread tid = TMEM lane; tile 0 row t = tid, tile 1 row t = 128 + tid
+    // epilogue: thread tid = TMEM lane, candidate row t = r0 + tid
     const int warp = tid >> 5;
     const double eg = 0.001953125 + (double)(dp + 8) * 1.1920928955078125e-07;
-    for (int tile = 0; tile < (two ? 2 : 1); ++tile) {
-        const int t = tile * 128 + tid;
-        const int cbase = tile * 128;                  // first candidate column of the tile
-        const int ncol = tile ? n1 : n0;
-        const unsigned tbase = pp.tmem + ((unsigned)(warp * 32) << 16) + (tile ? 256u : 0u);
-        const bool live = t < c;
-        const double nt = live ? P.nrm[t] : 0.0, st = live ? P.sq[t] : 0.0;
-        // columns below this warp's first row hold only pairs u <= t: skip whole words
-        const int w0 = (cbase + 32 * warp - cbase) >> 5;  // word offset inside the tile
-        for (int wd = w0; wd * 32 < ncol; ++wd) {
-            unsigned kb = 0u, ub = 0u;
+    const int t = r0 + tid;
+    const unsigned tbase = pp.tmem + ((unsigned)(warp * 32) << 16);
+    const bool live = t < c;
+    const double nt = live ? P.nrm[t] : 0.0, st = live ? P.sq[t] : 0.0;
+    // in the diagonal block, columns below this warp's first row hold only pairs u <= t
+    for (int wd = (b0 == r0) ? warp : 0; wd * 32 < ncol; ++wd) {
+        unsigned kb = 0u, ub = 0u;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int col = wd * 32 + h * 16;
-                if (col >= ncol) break;
-                float g[16];
-                tmem_ld16(tbase + (unsigned)col, g);
+        for (int h = 0; h < 2; ++h) {
+            const int col = wd * 32 + h * 16;
+            if (col >= ncol) break;
+            float g[16];
+            tmem_ld16(tbase + (unsigned)col, g);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int u = cbase + col + i;
-                    if (live && u > t && u < c) {
-                        const double dt = nt + P.nrm[u] - 2.0 * (double)g[i];
-                        const double E = 2.0 * eg * st * P.sq[u] + 1e-12 * (nt + P.nrm[u]);
-                        const double K = P.S.kd2[u];
-                        const double hi = alpha2 * (dt + E) * (1.0 + 1e-12);
-                        const double lo = alpha2 * (dt - E) * (1.0 - 1e-12);
-                        const unsigned bit = 1u << (h * 16 + i);
-                        if (hi <= K) kb |= bit;
-                        else if (!(lo > K)) ub |= bit;
-                    }
+            for (int i = 0; i < 16; ++i) {
+                const int u = b0 + col + i;
+                if (live && u > t && u < c) {
+                    const double dt = nt + P.nrm[u] - 2.0 * (double)g[i];
+                    const double E = 2.0 * eg * st * P.sq[u] + 1e-12 * (nt + P.nrm[u]);
+                    const double K = P.S.kd2[u];
+                    const double hi = alpha2 * (dt + E) * (1.0 + 1e-12);
+                    const double lo = alpha2 * (dt - E) * (1.0 - 1e-12);
+                    const unsigned bit = 1u << (h * 16 + i);
+                    if (hi <= K) kb |= bit;
+                    else if (!(lo > K)) ub |= bit;
                 }
             }
-            if (live) {
-                const int word = (cbase >> 5) + wd;
-                P.kill[t * 8 + word] = kb;
-                P.unc[t * 8 + word] = ub;
-            }
+        }
+        if (live) {
+            const int word = (b0 >> 5) + wd;
+            P.kill[tid * PT_WORDS + word] = kb;
+            P.unc[tid * PT_WORDS + word] = ub;
         }
     }
     tc_fence_before();
     __syncthreads();
 }
 
-// Greedy picks over the bit rows (warp 0); uncertain pairs of a picked t are
-// decided exactly.  Returns sel (picks written to out[0, sel)).
+// Bit rows of candidates r0 .. r0 + 127 against every later candidate: the
+// diagonal block (columns r0 .. r0 + 255) then 128-column blocks up to c.
 template <int QV>
-__device__ int pt_greedy(const float* __restrict__ X, int dp, const PTSmem& P, int c, double alpha2, int R, int* out,
-                         long long* exact_pairs) {
+__device__ void pt_gram_rows(const float* __restrict__ X, int dp, const PTSmem& P, PTPipe& pp, int c, int r0,
+                             double alpha2) {
+    pt_gram_pass<QV>(X, dp, P, pp, c, r0, r0, min(256, c - r0), alpha2);
+    for (int b0 = r0 + 256; b0 < c; b0 += 128) pt_gram_pass<QV>(X, dp, P, pp, c, r0, b0, min(128, c - b0), alpha2);
+}
+
+// Greedy picks (warp 0) among the candidates of the current row block
+// [r0, r0 + 128) whose bit rows are in P.kill / P.unc; uncertain pairs of a
+// picked t are decided exactly.  `alive` (lane l: word l), `sel` persist across
+// blocks.  Returns true when the picks are complete (sel == R or no candidate
+// is left), false when the next alive candidate lies beyond this block.
+template <int QV>
+__device__ bool pt_greedy_block(const float* __restrict__ X, int dp, const PTSmem& P, int c, int r0, double alpha2,
+                                int R, int* out, unsigned& alive, int& sel, long long& nex) {
     const int lane = lane_id();
     const int nw = (c + 31) >> 5;
-    // lane l < nw holds alive word l
-    unsigned alive = 0u;
-    if (lane < nw) alive = (c - 32 * lane >= 32) ? 0xffffffffu : ((1u << (c - 32 * lane)) - 1u);
-    int sel = 0;
-    long long nex = 0;
     while (sel < R) {
         const unsigned nz = __ballot_sync(PK_FULL, alive != 0u);
-        if (!nz) break;
+        if (!nz) return true;
         const int wl = __ffs(nz) - 1;
         const int t = 32 * wl + __ffs(__shfl_sync(PK_FULL, alive, wl)) - 1;
+        if (t >= r0 + 128) return false;
         if (lane == wl) alive &= ~(1u << (t & 31));
         const unsigned tid_t = P.S.ki2[t];
         if (lane == 0) out[sel] = (int)tid_t;
         ++sel;
-        if (sel >= R) break;
-        unsigned kill = lane < nw ? P.kill[t * 8 + lane] : 0u;
-        unsigned unc = lane < nw ? (P.unc[t * 8 + lane] & alive) : 0u;
+        if (sel >= R) return true;
+        const int row = (t - r0) * PT_WORDS;
+        unsigned kill = lane < nw ? P.kill[row + lane] : 0u;
+        unsigned unc = lane < nw ? (P.unc[row + lane] & alive) : 0u;
         if (__any_sync(PK_FULL, unc != 0u)) {
             Fp32Pick<QV> pick;
             pick.load(X, dp, tid_t);
@@ -287,27 +310,85 @@ __device__ int pt_greedy(const float* __restrict__ X, int dp, const PTSmem& P, i
         }
         alive &= ~kill;
     }
-    if (lane == 0 && exact_pairs) *exact_pairs += nex;
-    return sel;
+    return true;
 }
 
-// one item: sorted unique candidates in P.S.kd2/ki2 (c > R) -> picks
+// drop `self` and repeated (dist, id) entries of the sorted kd/ki[0, c) (c <=
+// PT_SORT), keep order -> kd2/ki2; returns the count (block-wide)
+__device__ __forceinline__ int pt_unique(const BPSmem& S, int c, unsigned self) {
+    constexpr int E = PT_SORT / PT_THREADS;  // positions per thread
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    bool keep[E];
+    int mine = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = E * tid + e;
+        keep[e] = false;
+        if (i < c) {
+            const unsigned id = S.ki[i];
+            keep[e] = id != self && !(i > 0 && S.ki[i - 1] == id && S.kd[i - 1] == S.kd[i]);
+        }
+        mine += keep[e];
+    }
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(PK_FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) S.scal[wid] = incl;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < wid; ++w) base += S.scal[w];
+    const int total = S.scal[0] + S.scal[1] + S.scal[2] + S.scal[3];
+    int o = base + incl - mine;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        if (keep[e]) {
+            S.kd2[o] = S.kd[E * tid + e];
+            S.ki2[o] = S.ki[E * tid + e];
+            ++o;
+        }
+    __syncthreads();
+    return total;
+}
+
+// one item: sorted unique candidates in P.S.kd2/ki2 (c <= PT_CAP) -> picks.
+// Bit rows are computed one 128-candidate block at a time, only as far as the
+// greedy needs them (R picks usually come from the first block).
 template <int QV>
 __device__ int pt_prune(const float* __restrict__ X, int dp, const double* __restrict__ nrm64, const PTSmem& P,
                         PTPipe& pp, int c, double alpha2, int R, int* out, long long* exact_pairs) {
     for (int x = threadIdx.x; x < c; x += PT_THREADS) {
-        const double v = nrm64[P.S.ki2[x]];
+        const unsigned id = P.S.ki2[x];
+        const double v = nrm64[id];
         P.nrm[x] = v;
         P.sq[x] = sqrt(v);
+        P.rowp[x] = reinterpret_cast<unsigned long long>(X + (size_t)id * dp);
     }
     __syncthreads();
-    pt_gram_bits<QV>(X, dp, P, pp, c, alpha2);
-    if ((threadIdx.x >> 5) == 0) {
-        const int sel = pt_greedy<QV>(X, dp, P, c, alpha2, R, out, exact_pairs);
-        if (lane_id() == 0) P.S.scal[8] = sel;
+    const int lane = lane_id();
+    const int nw = (c + 31) >> 5;
+    unsigned alive = 0u;  // warp 0: lane l holds alive word l
+    if (lane < nw) alive = (c - 32 * lane >= 32) ? 0xffffffffu : ((1u << (c - 32 * lane)) - 1u);
+    int sel = 0;
+    long long nex = 0;
+    for (int r0 = 0; r0 < c; r0 += 128) {
+        pt_gram_rows<QV>(X, dp, P, pp, c, r0, alpha2);
+        if ((threadIdx.x >> 5) == 0) {
+            const bool done = pt_greedy_block<QV>(X, dp, P, c, r0, alpha2, R, out, alive, sel, nex);
+            if (lane == 0) {
+                P.S.scal[8] = sel;
+                P.S.scal[9] = done;
+            }
+        }
+        __syncthreads();
+        if (P.S.scal[9]) break;
     }
+    if (threadIdx.x == 0 && exact_pairs) *exact_pairs += nex;
+    const int r = P.S.scal[8];
     __syncthreads();
-    return P.S.scal[8];
+    return r;
 }
 
 __device__ __forceinline__ void pt_setup(const PTSmem& P, PTPipe& pp) {
@@ -317,7 +398,7 @@ __device__ __forceinline__ void pt_setup(const PTSmem& P, PTPipe& pp) {
     }
     if ((threadIdx.x >> 5) == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(P.tmem_slot)),
-                     "r"(512));
+                     "r"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -332,14 +413,14 @@ __device__ __forceinline__ void pt_teardown(const PTSmem& P, const PTPipe& pp) {
     __syncthreads();
     if ((threadIdx.x >> 5) == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(pp.tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(pp.tmem), "r"(256));
     }
 }
 
 // build phase 2 for float data: one block per inserted point (items with more
 // than PT_CAP candidates are queued for build_prune_kernel)
 template <int QV>
-__global__ void __launch_bounds__(PT_THREADS, 1) prune_tc_build_kernel(BuildArgs A, const double* __restrict__ nrm64,
+__global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs A, const double* __restrict__ nrm64,
                                                                       int* over, int* nover) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const PTSmem P = carve_pt(smem_raw);
@@ -355,7 +436,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) prune_tc_build_kernel(BuildArgs
         const int vl = A.vlen[t];
         const int nd = __ldg(A.P.deg + p);
         const int c0 = vl + nd;
-        if (c0 > PT_CAP) {
+        if (c0 > PT_SORT) {
             if (tid == 0) over[atomicAdd(nover, 1)] = t;
             continue;
         }
@@ -380,7 +461,12 @@ __global__ void __launch_bounds__(PT_THREADS, 1) prune_tc_build_kernel(BuildArgs
         }
         __syncthreads();
         bp_sort(P.S.kd, P.S.ki, Pw);
-        const int c = bp_unique(P.S, c0, p);
+        const int c = pt_unique(P.S, c0, p);
+        if (c > PT_CAP) {  // more unique candidates than one Gram holds: warp path
+            if (tid == 0) over[atomicAdd(nover, 1)] = t;
+            __syncthreads();
+            continue;
+        }
         int* out = A.new_ids + (size_t)t * R;
         // the build always prunes (_kernels.py:370), even c <= R candidates
         int sel = c;
@@ -402,7 +488,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) prune_tc_build_kernel(BuildArgs
 // reverse-edge re-prune for float data: one block per target vertex with at most
 // PT_CAP candidates (larger groups: reverse_big_kernel / the selection path)
 template <int MODE, int QV>
-__global__ void __launch_bounds__(PT_THREADS, 1) prune_tc_reverse_kernel(RevArgs A, const double* __restrict__ nrm64) {
+__global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_reverse_kernel(RevArgs A, const double* __restrict__ nrm64) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const PTSmem P = carve_pt(smem_raw);
     PTPipe pp;
@@ -451,7 +537,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) prune_tc_reverse_kernel(RevArgs
             }
             __syncthreads();
             bp_sort(P.S.kd, P.S.ki, Pw);
-            const int c = bp_unique(P.S, c0, u);
+            const int c = pt_unique(P.S, c0, u);
             if (tid == 0) ev += c0;
             if (c <= A.R) {
                 for (int x = tid; x < c; x += PT_THREADS) row[x] = (int)P.S.ki2[x];

@@ -300,7 +300,7 @@ def test_lazy_keys_equal_eager(monkeypatch, case):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("case", ["c5", "c4", "dup128"])
+@pytest.mark.parametrize("case", ["c5", "c4", "dup128", "wide"])
 def test_tensor_core_prune_equals_warp_prune(monkeypatch, case):
     """Float data: RobustPrune decided from tcgen05 tf32 Gram tiles with a
     rigorous error bound (uncertain pairs decided exactly) builds the same graph
@@ -309,6 +309,19 @@ def test_tensor_core_prune_equals_warp_prune(monkeypatch, case):
         data, _ = workloads.generate("C5", n=6_000, components=8)
     elif case == "c4":
         data, _ = workloads.generate("C4", n=8_000, components=40)
+    elif case == "wide":
+        # long candidate lists (up to ~400) and R = 160: several 128-row bit blocks
+        rng = np.random.default_rng(8)
+        data = (rng.normal(size=(5_000, 48)) + 2.0 * rng.normal(size=(6, 48))[rng.integers(0, 6, 5_000)])
+        data = data.astype(np.float32)
+        out = {}
+        for flag in ("0", "1"):
+            monkeypatch.setenv("PK_TC_PRUNE", flag)
+            g = pk.build_vamana(pk.PointSet(data), R=160, L_build=320, alpha=1.05, seed=3, query_beam=64)
+            out[flag] = (g.graph.adjacency.copy(), g.graph.degrees.copy())
+        assert np.array_equal(out["0"][1], out["1"][1])
+        assert np.array_equal(out["0"][0], out["1"][0])
+        return
     else:
         rng = np.random.default_rng(5)
         hubs = rng.normal(size=(10, 128)) * 3.0
