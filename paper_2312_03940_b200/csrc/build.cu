@@ -54,7 +54,7 @@ struct BuildArgs {
 // phase 1: one warp per inserted point searches the adjacency snapshot and
 // logs its visited set (_kernels.py:349-358)
 template <int MODE, int QV>
-__global__ void __launch_bounds__(128, 8) build_search_kernel(BuildArgs A) {
+__global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 6 : 8) : 8) build_search_kernel(BuildArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;

@@ -325,8 +325,17 @@ constexpr int MODE_EXACT_U8 = 2;
 template <int QV>
 struct Seq64Screened : Seq64Member {
     static constexpr int kQV = QV;
-    __device__ __forceinline__ float screen(const float* __restrict__ X, unsigned id) const {
+    float4 qr[QV];  // this lane's query slices (chunks lane + 32 j), held in registers
+    __device__ __forceinline__ void load_query() {
         const float4* a = reinterpret_cast<const float4*>(q);
+        const int nv = dp >> 2, lane = lane_id();
+#pragma unroll
+        for (int j = 0; j < QV; ++j) {
+            const int f = lane + 32 * j;
+            qr[j] = f < nv ? __ldg(a + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    __device__ __forceinline__ float screen(const float* __restrict__ X, unsigned id) const {
         const float4* r = reinterpret_cast<const float4*>(X + (size_t)id * dp);
         const int nv = dp >> 2, lane = lane_id();
         float acc = 0.f;
@@ -334,7 +343,7 @@ struct Seq64Screened : Seq64Member {
         for (int j = 0; j < QV; ++j) {
             const int f = lane + 32 * j;
             if (f < nv) {
-                const float4 y = __ldg(a + f), x = __ldg(r + f);
+                const float4 y = qr[j], x = __ldg(r + f);
                 const float d0 = y.x - x.x, d1 = y.y - x.y, d2 = y.z - x.z, d3 = y.w - x.w;
                 acc = fmaf(d0, d0, acc);
                 acc = fmaf(d1, d1, acc);
@@ -352,7 +361,6 @@ struct Seq64Screened : Seq64Member {
     // (4*QV + 8) * 2^-53 relative of the exact sum, so within kLazyEps of the
     // reference's sequential value (<= 2*dp roundings of 2^-53 each).
     __device__ __forceinline__ double dscreen(const float* __restrict__ X, unsigned id) const {
-        const float4* a = reinterpret_cast<const float4*>(q);
         const float4* r = reinterpret_cast<const float4*>(X + (size_t)id * dp);
         const int nv = dp >> 2, lane = lane_id();
         double acc = 0.0;
@@ -360,7 +368,7 @@ struct Seq64Screened : Seq64Member {
         for (int j = 0; j < QV; ++j) {
             const int f = lane + 32 * j;
             if (f < nv) {
-                const float4 y = __ldg(a + f), x = __ldg(r + f);
+                const float4 y = qr[j], x = __ldg(r + f);
                 const double d0 = (double)y.x - (double)x.x, d1 = (double)y.y - (double)x.y;
                 const double d2 = (double)y.z - (double)x.z, d3 = (double)y.w - (double)x.w;
                 acc = fma(d0, d0, acc);
@@ -403,7 +411,13 @@ struct DistFor;
 template <int QV>
 struct DistFor<MODE_SEQ64, QV> {
     using T = Seq64Screened<QV>;
-    __device__ static T make(const DataRef& D, unsigned id) { return T{{D.X + (size_t)id * D.dp, D.dp}}; }
+    __device__ static T make(const DataRef& D, unsigned id) {
+        T t;
+        t.q = D.X + (size_t)id * D.dp;
+        t.dp = D.dp;
+        t.load_query();
+        return t;
+    }
 };
 template <int QV>
 struct DistFor<MODE_EXACT32, QV> {

@@ -11,7 +11,7 @@ namespace pk {
 
 // ---- beam kNN of member queries (_kernels.py:230-262) --------------------------------
 template <int MODE, int QV>
-__global__ void __launch_bounds__(128, 8) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
+__global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 6 : 8) : 8) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
                                                        int L, int kk, int H, size_t warp_bytes,
                                                        long long* __restrict__ out_ids, double* __restrict__ out_d,
                                                        long long* __restrict__ counts, long long* evals_out) {
