@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tc-sample", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-hbm-sample", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
     return ap.parse_args()
 
 
@@ -188,6 +189,55 @@ def brute_tc_sample(n=131_072, k=16, reps=3):
             "screen_ms": scr_ms, "call_ms": e0.elapsed_time(e1) / reps,
             "rescore_ms": prof.get("tc_rescore_kernel", (0, 0.0))[1] / reps,
             "uncertified_rows": index.TC_STATS["uncertified"] // reps}
+
+
+def hbm_gather_sample(n=200_000, k=16, reps=2):
+    """Beam-search kNN at HBM scale (the gather-bound kernel):
+    knn_all over a C5-generator sample (d = 1024 float32, 820 MB >> the 126 MB
+    L2) on a graph built with C5's R = 64, L = 200.  One untimed counting pass
+    gives the distinct evaluations U and expansions X; bytes = (U - n s) 4 d +
+    X 4 R (fp32 rows, seeds excluded); time = beam_knn_kernel's CUDA-event time."""
+    import torch
+
+    import paper_2312_03940_b200 as pk
+    from paper_2312_03940_b200 import _lib, vamana, workloads
+
+    w = workloads.WORKLOADS["C5"]
+    data, _ = workloads.generate("C5", n=n, components=max(1, n // 1281))
+    p = pk.PointSet(data)
+    del data
+    g = pk.build_vamana(p, R=w.R, L_build=w.L, alpha=w.alpha, seed=0, query_beam=w.L)
+    q = torch.arange(n, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(3, dtype=torch.int64, device="cuda")
+    os.environ["PK_COUNT_UNIQUE"] = "1"
+    try:
+        vamana.beam_knn_raw(g.graph, q, w.L, k, cnt)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("PK_COUNT_UNIQUE", None)
+    evals, expansions, uniq = cnt.tolist()
+    _lib.prof_collect(reset=True)
+    _lib.prof_only(["beam_knn_kernel"])
+    _lib.prof_enable(True)
+    for _ in range(reps):
+        vamana.beam_knn_raw(g.graph, q, w.L, k)
+    torch.cuda.synchronize()
+    _lib.prof_enable(False)
+    prof = _lib.prof_collect(reset=True)
+    ms = prof["beam_knn_kernel"][1] / reps
+    s = int(np.ceil(np.sqrt(n)))
+    alg = (uniq - n * s) * 4 * w.d + expansions * 4 * w.R
+    hbm, _, kind = peaks()
+    ach = alg / (ms / 1e3) / 1e9
+    del g, p
+    torch.cuda.empty_cache()
+    return {"bound": "hbm", "kernel": "beam_knn_kernel", "achieved": ach, "peak": hbm, "unit": "GB/s",
+            "frac": ach / hbm, "traffic": None, "peak_source": kind,
+            "sample": f"knn_all (k={k}, L={w.L}) over a C5-generator sample n={n}, d={w.d} float32 "
+                      f"({n * w.d * 4 / 1e6:.0f} MB, larger than L2), graph R={w.R} L={w.L}",
+            "kernel_ms": ms, "queries_per_s": n / (ms / 1e3), "unique_evals_per_query": uniq / n,
+            "expansions_per_query": expansions / n, "algorithmic_bytes": alg,
+            "definition": "(unique evals - seeds) x 4d + expansions x 4R over all queries"}
 
 
 # ---------------------------------------------------------------------------- counting pass
@@ -397,6 +447,7 @@ def main_ours(args):
     pinned = torch.from_numpy(np.array(data, dtype=np.float32, copy=True)).pin_memory()
     host_view = pinned.numpy()
     e2e_ms = 0.0
+    e2e_steps_ms = []
     h2d = d2h = 0
     pk.run_pipeline(pk.PointSet(host_view), **kw, comm=comm)  # untimed e2e warm-up (pinned staging buffers)
     torch.cuda.synchronize()
@@ -412,6 +463,7 @@ def main_ours(args):
         torch.cuda.synchronize()
         barrier()
         e2e_ms += e0.elapsed_time(e1)
+        e2e_steps_ms.append(round(e0.elapsed_time(e1), 3))
         h2d = n * w.d * 4
         st = res.state
         d2h = sum(a.nbytes for a in (st.rho, st.lam, st.delta, st.neighbors.ids, st.neighbors.dists,
@@ -460,6 +512,12 @@ def main_ours(args):
             tc = brute_tc_sample()
         except Exception as e:  # noqa: BLE001 -- reported, never silently replaced
             tc = {"error": repr(e)}
+    hbm_s = None
+    if rank == 0 and not args.no_hbm_sample:
+        try:
+            hbm_s = hbm_gather_sample()
+        except Exception as e:  # noqa: BLE001 -- reported, never silently replaced
+            hbm_s = {"error": repr(e)}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -479,7 +537,8 @@ def main_ours(args):
             "vs_baseline": None, "dtype": {0: "f64", 1: "f32 (exact: integer data)", 2: "u8/int32 (exact: integer data)"}[p.mode],
             "data": f"synthetic ({name} generator, seed 0)",
             "config": workload_config(name, args.n, world),
-            "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "step_ms": e2e_steps_ms},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
                          "peak_source": peak_kind, "algorithmic_bytes_per_step": alg_bytes,
@@ -488,6 +547,7 @@ def main_ours(args):
                          "largest_kernel_overall": overall[0],
                          "largest_kernel_share": overall[1][1] / args.steps / ms_step},
             "roofline_tensor": tc,
+            "roofline_hbm_scale": hbm_s,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches / args.steps) * args.steps,
             "gpu_launches_per_step": launches / args.steps,
