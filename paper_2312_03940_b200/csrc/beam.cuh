@@ -73,6 +73,7 @@ struct SearchParams {
     long long n_points = 0;    // n (bitmap size in counting mode)
     int prefetch = 1;          // L1 prefetch of the next expansion's adjacency row
     int lazy = 1;              // float data: lazy keys (fp32 screen values until a decision needs the exact one)
+    int seed_only = 0;         // profiling aid (PK_SEED_ONLY): stop after seeding
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         wb.init(sm, L, nullptr, nullptr, 0, nullptr);
         wb.begin_counting(P.ubm ? P.ubm + ((size_t)blockIdx.x * wpb + wib) * P.uwords : nullptr, P.uwords);
         wb.seed(P, dist, false, uniq);
-        wb.walk(P, dist);
+        if (!P.seed_only) wb.walk(P, dist);
         un += wb.uniq;
         long long* oi = out_ids + t * kk;
         double* od = out_d + t * kk;
@@ -534,6 +534,7 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
     P.n_points = n;
     P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     P.lazy = env_int("PK_LAZY", 1) == 1 && n < (int64_t)PK_IDMASK;
+    P.seed_only = env_int("PK_SEED_ONLY", 0);
     int H = choose_hash((int)L, hash_bits, n);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);
