@@ -248,6 +248,12 @@ int pk_count_below(const float* x, int64_t n, int64_t dp, const uint32_t* x8, in
 int pk_resolve_short(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
                      const int64_t* rank, const int64_t* qids, int64_t m, int64_t kk, int64_t* lam,
                      double* delta, int64_t* unresolved, int64_t* n_unresolved, void* stream);
+/* pk_resolve_short with the dp scan already done (dp_id / dp_sqd = the exact
+ * nearest denser point of each row, e.g. from pk_dp_scan_tc): the count scan
+ * and the resolution only. */
+int pk_resolve_short_scanned(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                             const int64_t* qids, int64_t m, int64_t kk, const int64_t* dp_id, const double* dp_sqd,
+                             int64_t* lam, double* delta, int64_t* unresolved, int64_t* n_unresolved, void* stream);
 
 /* Scatter: lam[qids[i]] = src_id[i], delta[qids[i]] = sqrt(src_sqd[i])
  * (dependent.py:125-127). */

@@ -56,6 +56,7 @@ SIGNATURES = {
     "pk_dp_scan": [_P, _I, _I, _P, _I, _i, _P, _P, _I, _P, _P, _P],
     "pk_count_below": [_P, _I, _I, _P, _I, _i, _P, _I, _P, _P, _P, _P],
     "pk_resolve_short": [_P, _I, _I, _P, _I, _i, _P, _P, _I, _I, _P, _P, _P, _P, _P],
+    "pk_resolve_short_scanned": [_P, _I, _I, _P, _I, _i, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "pk_scatter_dependents": [_P, _I, _P, _P, _P, _P, _P],
     "pk_argmax_rank": [_P, _I, _P, _P],
     "pk_flag_noise": [_P, _I, _D, _P, _P, _P],

@@ -62,6 +62,37 @@ struct QueryTile<MODE_SEQ64> {
     }
 };
 
+// float32 screen of the count scan (SEQ64): per thread, sequential fma over
+// the coordinates -- within (dp + 3) 2^-24 relative of the exact sum (all
+// terms non-negative), widened to kCountEps below; pairs inside the band get
+// the exact float64 value (one_exact)
+__device__ __forceinline__ void dist32(const float* q, int dp, const float* __restrict__ X, int j, float* acc) {
+    const float* r = X + (size_t)j * dp;
+#pragma unroll
+    for (int a = 0; a < kScanQ; ++a) acc[a] = 0.f;
+    for (int t = 0; t < dp; t += 4) {
+        const float4 x = ldg4(r + t);
+#pragma unroll
+        for (int a = 0; a < kScanQ; ++a) {
+            const float4 qa = *reinterpret_cast<const float4*>(q + a * dp + t);
+            const float e0 = qa.x - x.x, e1 = qa.y - x.y, e2 = qa.z - x.z, e3 = qa.w - x.w;
+            acc[a] = fmaf(e0, e0, acc[a]);
+            acc[a] = fmaf(e1, e1, acc[a]);
+            acc[a] = fmaf(e2, e2, acc[a]);
+            acc[a] = fmaf(e3, e3, acc[a]);
+        }
+    }
+}
+__device__ __forceinline__ double one_exact(const float* q, int dp, const float* __restrict__ X, int j) {
+    const float* r = X + (size_t)j * dp;
+    double acc = 0.0;
+    for (int t = 0; t < dp; ++t) {
+        const double e = (double)q[t] - (double)__ldg(r + t);
+        acc = __dadd_rn(acc, __dmul_rn(e, e));
+    }
+    return acc;
+}
+
 template <>
 struct QueryTile<MODE_EXACT_U8> {
     const unsigned* q;  // smem, QT x dw words
@@ -141,6 +172,22 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs A) {
         if (OP == SCAN_DENSER) {
             rj = __ldg(A.rank + j);
             if (rj <= rmin) continue;
+        }
+        if constexpr (OP == SCAN_COUNT && MODE == MODE_SEQ64) {
+            float a32[kScanQ];
+            dist32(tile.q, tile.dp, A.D.X, j, a32);
+            const double eps = (double)(tile.dp + 8) * 1.1920928955078125e-07;
+#pragma unroll
+            for (int a = 0; a < kScanQ; ++a) {
+                if ((long long)j == qid[a] || a >= nq) continue;
+                const double v = (double)a32[a], T = kdd[a];
+                bool below;
+                if (v > 1e-30 && v < 1e30 && T > 1e-30 && v * (1.0 + eps) < T) below = true;
+                else if (v > 1e-30 && v < 1e30 && v * (1.0 - eps) > T) below = false;
+                else below = key_lt(one_exact(tile.q + a * tile.dp, tile.dp, A.D.X, j), (unsigned)j, T, (unsigned)kdi[a]);
+                cnt[a] += below;
+            }
+            continue;
         }
         double acc[kScanQ];
         tile.dist(A.D, j, acc);
@@ -302,6 +349,34 @@ extern "C" int pk_count_below(const float* x, int64_t n, int64_t dp, const uint3
     return dispatch_scan<SCAN_COUNT>(mode, A, st, &nc);
 }
 
+extern "C" int pk_resolve_short_scanned(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw,
+                                        int mode, const int64_t* qids, int64_t m, int64_t kk, const int64_t* dp_id,
+                                        const double* dp_sqd, int64_t* lam, double* delta, int64_t* unresolved,
+                                        int64_t* n_unresolved, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (m <= 0) {
+        PK_CHECK(cudaMemsetAsync(n_unresolved, 0, sizeof(int64_t), st));
+        return 0;
+    }
+    long long* cnt = nullptr;
+    unsigned char* fl = nullptr;
+    PK_CHECK(scratch(&cnt, (size_t)m, st));
+    PK_CHECK(scratch(&fl, (size_t)m, st));
+    int rc = pk_count_below(x, n, dp, x8, dw, mode, qids, m, dp_sqd, dp_id, reinterpret_cast<int64_t*>(cnt), stream);
+    if (rc) return rc;
+    {
+        ProfScope _ps("short_resolve_kernel", st);
+        short_resolve_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(
+            reinterpret_cast<const long long*>(qids), (int)m, reinterpret_cast<const long long*>(dp_id), dp_sqd, cnt,
+            kk, reinterpret_cast<long long*>(lam), delta, fl);
+    }
+    PK_CHECK_LAUNCH("short_resolve_kernel");
+    rc = compact_flagged(reinterpret_cast<const long long*>(qids), fl, m, reinterpret_cast<long long*>(unresolved),
+                         reinterpret_cast<long long*>(n_unresolved), st);
+    for (void* p : {(void*)cnt, (void*)fl}) release(p, st);
+    return rc;
+}
+
 extern "C" int pk_resolve_short(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
                                 const int64_t* rank, const int64_t* qids, int64_t m, int64_t kk, int64_t* lam,
                                 double* delta, int64_t* unresolved, int64_t* n_unresolved, void* stream) {
@@ -310,27 +385,15 @@ extern "C" int pk_resolve_short(const float* x, int64_t n, int64_t dp, const uin
         PK_CHECK(cudaMemsetAsync(n_unresolved, 0, sizeof(int64_t), st));
         return 0;
     }
-    long long *sid = nullptr, *cnt = nullptr;
+    int64_t* sid = nullptr;
     double* ssq = nullptr;
-    unsigned char* fl = nullptr;
     PK_CHECK(scratch(&sid, (size_t)m, st));
     PK_CHECK(scratch(&ssq, (size_t)m, st));
-    PK_CHECK(scratch(&cnt, (size_t)m, st));
-    PK_CHECK(scratch(&fl, (size_t)m, st));
-    int rc = pk_dp_scan(x, n, dp, x8, dw, mode, rank, qids, m, reinterpret_cast<int64_t*>(sid), ssq, stream);
+    int rc = pk_dp_scan(x, n, dp, x8, dw, mode, rank, qids, m, sid, ssq, stream);
     if (rc) return rc;
-    rc = pk_count_below(x, n, dp, x8, dw, mode, qids, m, ssq, reinterpret_cast<int64_t*>(sid),
-                        reinterpret_cast<int64_t*>(cnt), stream);
-    if (rc) return rc;
-    {
-        ProfScope _ps("short_resolve_kernel", st);
-        short_resolve_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(
-            reinterpret_cast<const long long*>(qids), (int)m, sid, ssq, cnt, kk, reinterpret_cast<long long*>(lam),
-            delta, fl);
-    }
-    PK_CHECK_LAUNCH("short_resolve_kernel");
-    rc = compact_flagged(reinterpret_cast<const long long*>(qids), fl, m, reinterpret_cast<long long*>(unresolved),
-                         reinterpret_cast<long long*>(n_unresolved), st);
-    for (void* p : {(void*)sid, (void*)ssq, (void*)cnt, (void*)fl}) release(p, st);
+    rc = pk_resolve_short_scanned(x, n, dp, x8, dw, mode, qids, m, kk, sid, ssq, lam, delta, unresolved, n_unresolved,
+                                  stream);
+    release(sid, st);
+    release(ssq, st);
     return rc;
 }

@@ -146,8 +146,16 @@ def _resolve_short(p: PointSet, rank_t, short_t, ms: int, kk: int, lam_t, delta_
 
     out = torch.empty(max(ms, 1), dtype=torch.int64, device=short_t.device)
     cnt = torch.zeros(1, dtype=torch.int64, device=short_t.device)
-    _lib.call("pk_resolve_short", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, rank_t, short_t, ms, kk, lam_t,
-              delta_t, out, cnt, _lib.stream())
+    if _dp_scan_on_tensor_cores(p, ms):
+        # the dp scan on the tensor cores (certificate + exact rescan), then the count scan
+        sid = torch.empty(ms, dtype=torch.int64, device=short_t.device)
+        ssq = torch.empty(ms, dtype=torch.float64, device=short_t.device)
+        _dp_scan_tc(p, rank_t, short_t, ms, sid, ssq)
+        _lib.call("pk_resolve_short_scanned", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, short_t, ms, kk, sid,
+                  ssq, lam_t, delta_t, out, cnt, _lib.stream())
+    else:
+        _lib.call("pk_resolve_short", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, rank_t, short_t, ms, kk,
+                  lam_t, delta_t, out, cnt, _lib.stream())
     c = int(cnt.item())
     return out[:c], c
 
@@ -218,6 +226,7 @@ def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: D
                 kq = min(kdep, n - 1)
                 if trace is not None:
                     trace.append((m, kq))
+                ms = 0
                 q = mine(todo)
                 if raw is not None:
                     r_ids, r_sqd, r_cnt = raw(q, kq)
@@ -230,6 +239,8 @@ def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: D
                 else:
                     r_ids, r_sqd = g.knn_batch_device(q, kq)
                     todo, m, _, _ = _resolve(rank_t, q, r_ids, sqrt_device(r_sqd), lam_t, delta_t, -1)
+                if trace is not None and ms:
+                    trace[-1] = trace[-1] + (ms,)  # rows the beam search left short (exact scans)
                 if comm is not None:
                     todo, m = regroup(todo)
                 if kq >= n - 1:

@@ -358,6 +358,29 @@ def test_build_with_short_candidate_lists_matches_oracle(kind):
     assert np.array_equal(g.graph.adjacency, adj)
 
 
+@pytest.mark.parametrize("d", [48, 384, 1024])
+def test_count_below_matches_exact_rows(d):
+    """pk_count_below (fp32-screened count scan, exact float64 inside the band)
+    == the position of the key in the exact brute-force row (oracle)."""
+    import torch
+
+    rng = np.random.default_rng(d)
+    n = 3_000
+    data = (rng.normal(size=(n, d)) + rng.normal(size=(8, d))[rng.integers(0, 8, n)]).astype(np.float32)
+    data[:20] = data[20:40]  # duplicates: zero distances and tied keys
+    p = pk.PointSet(data)
+    qids = np.sort(rng.choice(n, 40, replace=False)).astype(np.int64)
+    ids, sqd = oracle.brute_knn_batch(data, qids, n - 1)
+    pos = rng.integers(0, n - 1, qids.shape[0])
+    pos[:5] = 0
+    key_i = ids[np.arange(len(qids)), pos].astype(np.int64)
+    key_d = sqd[np.arange(len(qids)), pos]
+    cnt = torch.zeros(len(qids), dtype=torch.int64, device="cuda")
+    _lib.call("pk_count_below", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, _lib.to_dev(qids), len(qids),
+              _lib.to_dev(key_d), _lib.to_dev(key_i), cnt, _lib.stream())
+    assert np.array_equal(_lib.to_host(cnt), pos)
+
+
 def test_pointset_device_validation_reports_first_nonfinite():
     """With a GPU the PointSet check runs on the device (pk_scan_points); the
     error names the same first (point, dimension) as numpy's argwhere."""
