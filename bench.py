@@ -73,78 +73,113 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / clock-event (throttle) reasons sampled during the timed region
+    through NVML in a background thread (25 ms period).  NVML reads are cheap;
+    an nvidia-smi process in loop mode takes driver locks that stalled a timed
+    step.  Falls back to nvidia-smi when NVML is unavailable."""
 
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (host time, sm MHz, max MHz, reason bits)
         self.thread = None
+        self.proc = None
+        self.stop_flag = threading.Event()
+        self.source = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(self.gpu)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
 
     def start(self):
         if os.environ.get("PK_BENCH_NO_SMI") == "1":  # diagnosis only
             return
         try:
+            nv, h = self._nvml_handle()
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.source = "nvml"
+
+            def loop():
+                while not self.stop_flag.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.perf_counter(), float(sm), float(mx), int(rs)))
+                    except Exception:
+                        pass
+                    self.stop_flag.wait(0.025)
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            pass
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
         except Exception:
             self.proc = None
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread = threading.Thread(target=self._read_smi, daemon=True)
         self.thread.start()
 
-    def _read(self):
+    def _read_smi(self):
+        names = list(self.REASONS)
         for line in self.proc.stdout:
-            self.lines.append((time.perf_counter(), line.strip()))
-
-    def wait_first(self, n=2, timeout=3.0):
-        """Block until the sampler has produced n lines (its start-up holds driver
-        locks that would otherwise stall the first timed steps)."""
-        t = time.perf_counter()
-        while self.proc is not None and len(self.lines) < n and time.perf_counter() - t < timeout:
-            time.sleep(0.01)
-
-    def mark(self, t0, t1):
-        """The timed region's host-time window (samples inside it are preferred)."""
-        self.window = (t0, t1)
-
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        if self.thread:
-            self.thread.join(timeout=2)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        lines = self.lines
-        w = getattr(self, "window", None)
-        if w is not None:
-            inside = [x for x in lines if w[0] <= x[0] <= w[1]]
-            # short timed regions may fall between two 200 ms samples: keep the nearest
-            lines = inside or sorted(lines, key=lambda x: min(abs(x[0] - w[0]), abs(x[0] - w[1])))[:2]
-        for _, ln in lines:
-            parts = [x.strip() for x in ln.split(",")]
+            parts = [x.strip() for x in line.strip().split(",")]
             if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
+                bits = sum(self.REASONS[nm] for nm, v in zip(names, parts[5:9]) if v.lower() == "active")
+                self.samples.append((time.perf_counter(), float(parts[1]), float(parts[2]), bits))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
+
+    def wait_first(self, n=2, timeout=3.0):
+        """Block until the sampler has produced n samples."""
+        t = time.perf_counter()
+        while self.thread is not None and len(self.samples) < n and time.perf_counter() - t < timeout:
+            time.sleep(0.01)
+
+    def mark(self, t0, t1):
+        """The timed region's host-time window (samples inside it are used)."""
+        self.window = (t0, t1)
+
+    def stop(self):
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        self.stop_flag.set()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        self.thread.join(timeout=2)
+        samples = self.samples
+        w = getattr(self, "window", None)
+        if w is not None:
+            inside = [x for x in samples if w[0] <= x[0] <= w[1]]
+            samples = inside or sorted(samples, key=lambda x: min(abs(x[0] - w[0]), abs(x[0] - w[1])))[:2]
+        sm = [x[1] for x in samples]
+        mx = [x[2] for x in samples]
+        reasons = sorted(nm for nm, bit in self.REASONS.items() if any(x[3] & bit for x in samples))
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "source": self.source}
 
 
 # ---------------------------------------------------------------------------- tensor-core sample
@@ -340,7 +375,8 @@ def workload_config(name, n_override, n_gpus):
     return {"workload": f"{name}: n={n} d={w.d} Vamana R={w.R} L={w.L} alpha={w.alpha} {w.density} k={w.k} "
                         f"ProductCenter({w.n_centers}) doubling from {2 * w.k}, threshold 300",
             "n": n, "d": w.d, "R": w.R, "L": w.L, "k": w.k, "density": w.density,
-            "parallelism": par, "l2": "flushed (256 MiB write) before every timed step"}
+            "parallelism": par, "l2": "flushed (256 MiB write) before every timed step",
+            "host": "python gc.freeze() after the warm-up steps (start-up heap out of the collector)"}
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -389,6 +425,14 @@ def main_ours(args):
     for _ in range(args.warmup):
         run_pipeline_device(p, **kw, comm=comm)
     torch.cuda.synchronize()
+    # a serving process freezes its start-up heap: every object created so far
+    # (torch, numpy, the package) leaves the collector's generations, so a
+    # gen-2 collection inside a timed step scans only the step's own objects
+    # (unfrozen, full collections took 15-27 ms of a 37 ms step)
+    import gc
+
+    gc.collect()
+    gc.freeze()
 
     build_stats = torch.zeros(5, dtype=torch.int64, device="cuda")
     beam_stats = torch.zeros(3, dtype=torch.int64, device="cuda")
@@ -448,8 +492,14 @@ def main_ours(args):
     host_view = pinned.numpy()
     e2e_ms = 0.0
     e2e_steps_ms = []
+    e2e_stage_ms = []
     h2d = d2h = 0
-    pk.run_pipeline(pk.PointSet(host_view), **kw, comm=comm)  # untimed e2e warm-up (pinned staging buffers)
+    # untimed e2e warm-up: two calls with the first result still alive, as in the
+    # timed loop (each result's arrays live in a pinned staging block of torch's
+    # caching host allocator, so the loop alternates between two blocks)
+    r0 = pk.run_pipeline(pk.PointSet(host_view), **kw, comm=comm)
+    r1 = pk.run_pipeline(pk.PointSet(host_view), **kw, comm=comm)
+    del r0, r1
     torch.cuda.synchronize()
     for _ in range(args.e2e_steps):
         flush.fill_(1)
@@ -464,6 +514,7 @@ def main_ours(args):
         barrier()
         e2e_ms += e0.elapsed_time(e1)
         e2e_steps_ms.append(round(e0.elapsed_time(e1), 3))
+        e2e_stage_ms.append({k_: round(v * 1e3, 2) for k_, v in res.timings.items()})
         h2d = n * w.d * 4
         st = res.state
         d2h = sum(a.nbytes for a in (st.rho, st.lam, st.delta, st.neighbors.ids, st.neighbors.dists,
@@ -538,7 +589,7 @@ def main_ours(args):
             "data": f"synthetic ({name} generator, seed 0)",
             "config": workload_config(name, args.n, world),
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "step_ms": e2e_steps_ms},
+                    "step_ms": e2e_steps_ms, "step_stage_ms": e2e_stage_ms},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
                          "peak_source": peak_kind, "algorithmic_bytes_per_step": alg_bytes,
