@@ -49,7 +49,7 @@ TIMED_KERNELS = ("build_search_kernel", "beam_knn_kernel", "build_prune_block_ke
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
@@ -465,6 +465,8 @@ def main_ours(args):
         torch.cuda.synchronize()
         barrier()
         step_ms.append(e0.elapsed_time(e1))
+        if os.environ.get("PK_BENCH_TRACE") == "1":
+            print(f"timed step {len(step_ms) - 1}: host {time.perf_counter():.3f}", file=sys.stderr, flush=True)
         total_ms += step_ms[-1]
         for kk_, v in last["timings"].items():
             stage[kk_] += v

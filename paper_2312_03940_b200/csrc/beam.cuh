@@ -225,10 +225,10 @@ struct WarpBeam {
             }
             __syncwarp();
         }
-        int mev = evn;
+        if (__any_sync(PK_FULL, evn != 0x7fffffff)) {
+            int mev = evn;
 #pragma unroll
-        for (int s = 16; s; s >>= 1) mev = min(mev, __shfl_xor_sync(PK_FULL, mev, s));
-        if (mev != 0x7fffffff) {
+            for (int s = 16; s; s >>= 1) mev = min(mev, __shfl_xor_sync(PK_FULL, mev, s));
             const int src = __ffs(__ballot_sync(PK_FULL, evn == mev)) - 1;
             ev_d = __shfl_sync(PK_FULL, evd, src);
             ev_i = __shfl_sync(PK_FULL, evi, src);
