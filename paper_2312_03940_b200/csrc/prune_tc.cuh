@@ -13,9 +13,11 @@
 //    CTAs per SM, so one item's staging overlaps the other's sort / greedy);
 //  * the epilogue (thread = TMEM lane = candidate row) forms
 //    d~ = |t|^2 + |u|^2 - 2 G~ (float64 norms precomputed once per build) and a
-//    rigorous bound E = 2 eg |t||u| + 1e-12 (|t|^2 + |u|^2) with
-//    eg = 2^-9 + (dp + 8) 2^-23 (tf32 inputs keep >= 10 mantissa bits; fp32
-//    accumulation), then sets the occlusion bit where alpha^2 (d~ + E) <= d(p,u)
+//    rigorous bound E = 2 (eg |t||u| + ea (|t| + |u| + 1)) + 1e-12 (|t|^2 + |u|^2)
+//    with eg = 2^-9 + (dp + 8) 2^-23 (tf32 inputs keep >= 10 mantissa bits;
+//    fp32 accumulation) and ea = (dp + 8) 2^-126 (subnormals flushed to zero);
+//    a non-finite accumulator (overflow) is always "uncertain"; then sets the
+//    occlusion bit where alpha^2 (d~ + E) <= d(p,u)
 //    and an "uncertain" bit where neither that nor alpha^2 (d~ - E) > d(p,u)
 //    holds;
 //  * the greedy picks (warp 0) are bit arithmetic; an uncertain pair (t, u)
@@ -210,7 +212,11 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
 
     // epilogue: thread tid = TMEM lane, candidate row t = r0 + tid
     const int warp = tid >> 5;
+    // relative bound of the tf32 Gram (inputs keep >= 10 mantissa bits, fp32
+    // accumulation) and an absolute term for subnormal inputs / partial sums
+    // flushed to zero: <= (dp + 8) 2^-126 (|t| + |u| + 1)
     const double eg = 0.001953125 + (double)(dp + 8) * 1.1920928955078125e-07;
+    const double eabs = (double)(dp + 8) * 1.1754943508222875e-38;
     const int t = r0 + tid;
     const unsigned tbase = pp.tmem + ((unsigned)(warp * 32) << 16);
     const bool live = t < c;
@@ -228,12 +234,17 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
             for (int i = 0; i < 16; ++i) {
                 const int u = b0 + col + i;
                 if (live && u > t && u < c) {
+                    const unsigned bit = 1u << (h * 16 + i);
+                    if (!isfinite(g[i])) {  // fp32 accumulator overflow (huge coordinates): decide exactly
+                        ub |= bit;
+                        continue;
+                    }
                     const double dt = nt + P.nrm[u] - 2.0 * (double)g[i];
-                    const double E = 2.0 * eg * st * P.sq[u] + 1e-12 * (nt + P.nrm[u]);
+                    const double su = P.sq[u];
+                    const double E = 2.0 * (eg * st * su + eabs * (st + su + 1.0)) + 1e-12 * (nt + P.nrm[u]);
                     const double K = P.S.kd2[u];
                     const double hi = alpha2 * (dt + E) * (1.0 + 1e-12);
                     const double lo = alpha2 * (dt - E) * (1.0 - 1e-12);
-                    const unsigned bit = 1u << (h * 16 + i);
                     if (hi <= K) kb |= bit;
                     else if (!(lo > K)) ub |= bit;
                 }

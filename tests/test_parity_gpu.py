@@ -435,3 +435,42 @@ def test_device_contingency_equals_host():
     for f in ("rows", "cols", "counts", "row_sums", "col_sums"):
         assert np.array_equal(getattr(dev, f), getattr(host, f)), f
     assert pk.ari(a, b) == h_ari  # device path (n >= DEVICE_MIN)
+
+
+def _pipeline_vs_oracle(data, R, L, k, nc, alpha=1.2, threshold=50, density="kth", seed=0):
+    res = pk.run_pipeline(pk.PointSet(data), pk.VamanaConfig(R=R, L_build=L, L=L, alpha=alpha, seed=seed), k=k,
+                          density_kind=density, center_policy=pk.ProductCenter(nc), noise_policy=pk.NoisePolicy(0.0),
+                          doubling_params=pk.DoublingParams(initial_k=2 * k, threshold=threshold))
+    ref = oracle.pipeline(data, index="vamana", R=R, L_build=L, L=L, alpha=alpha, seed=seed, k=k, density_kind=density,
+                          center_policy=("product", nc), rho_min=0.0, initial_k=2 * k, threshold=threshold)
+    st = res.state
+    assert np.array_equal(st.neighbors.ids, ref["nbr_ids"])
+    assert np.array_equal(st.neighbors.dists, ref["nbr_dists"])
+    assert np.array_equal(st.rho, ref["rho"])
+    assert np.array_equal(st.lam, ref["lam"])
+    assert np.array_equal(st.delta, ref["delta"])
+    assert np.array_equal(res.clustering.labels, ref["labels"])
+
+
+@pytest.mark.parametrize("case", ["identical1024", "few_distinct256", "huge_scale", "tiny_scale", "d1", "n3"])
+def test_degenerate_float_data_matches_oracle(case):
+    """Float data the lazy keys / tensor-core prune / fp32 screens find hardest:
+    all points identical (every key tied, zero distances, cancellation in the
+    Gram epilogue), a handful of distinct rows, coordinates near the fp32 range
+    limits (screens overflow / underflow and fall back), d = 1, and n = 3."""
+    rng = np.random.default_rng(17)
+    if case == "identical1024":
+        data = np.tile(rng.normal(size=(1, 1024)).astype(np.float32), (400, 1))
+    elif case == "few_distinct256":
+        data = rng.normal(size=(5, 256)).astype(np.float32)[rng.integers(0, 5, 600)]
+    elif case == "huge_scale":
+        data = (rng.normal(size=(700, 300)) * 3e18).astype(np.float32)
+    elif case == "tiny_scale":
+        data = (rng.normal(size=(700, 300)) * 1e-19).astype(np.float32)
+    elif case == "d1":
+        data = rng.normal(size=(900, 1)).astype(np.float32)
+    else:
+        data = rng.normal(size=(3, 40)).astype(np.float32)
+    n = data.shape[0]
+    k = min(8, n - 1)
+    _pipeline_vs_oracle(data, R=16, L=max(24, k), k=k, nc=min(3, n))
