@@ -452,7 +452,8 @@ def _pipeline_vs_oracle(data, R, L, k, nc, alpha=1.2, threshold=50, density="kth
     assert np.array_equal(res.clustering.labels, ref["labels"])
 
 
-@pytest.mark.parametrize("case", ["identical1024", "few_distinct256", "huge_scale", "tiny_scale", "d1", "n3"])
+@pytest.mark.parametrize("case", ["identical1024", "few_distinct256", "huge_scale", "tiny_scale", "d1", "n3", "n2",
+                                  "identical_u8", "grid_u8_ties", "wide_beam"])
 def test_degenerate_float_data_matches_oracle(case):
     """Float data the lazy keys / tensor-core prune / fp32 screens find hardest:
     all points identical (every key tied, zero distances, cancellation in the
@@ -469,8 +470,29 @@ def test_degenerate_float_data_matches_oracle(case):
         data = (rng.normal(size=(700, 300)) * 1e-19).astype(np.float32)
     elif case == "d1":
         data = rng.normal(size=(900, 1)).astype(np.float32)
-    else:
+    elif case == "n3":
         data = rng.normal(size=(3, 40)).astype(np.float32)
+    elif case == "n2":
+        data = rng.normal(size=(2, 7)).astype(np.float32)
+    elif case == "identical_u8":
+        data = np.full((500, 128), 7.0, np.float32)
+    elif case == "grid_u8_ties":
+        # integer grid: many exactly equal distances (ties broken by id)
+        data = np.stack(np.meshgrid(np.arange(30), np.arange(30), indexing="ij"), -1).reshape(-1, 2)
+        data = np.concatenate([data, data[:100]]).astype(np.float32)
+    else:  # beam wider than n, every point a start
+        data = rng.normal(size=(120, 16)).astype(np.float32)
+        res = pk.run_pipeline(pk.PointSet(data), pk.VamanaConfig(R=8, L_build=200, L=200, alpha=1.0, seed=1,
+                                                                 num_starts=120), k=12, density_kind="sum",
+                              center_policy=pk.ProductCenter(4), noise_policy=pk.NoisePolicy(0.0),
+                              doubling_params=pk.DoublingParams(initial_k=24, threshold=5))
+        ref = oracle.pipeline(data, index="vamana", R=8, L_build=200, L=200, alpha=1.0, seed=1, num_starts=120, k=12,
+                              density_kind="sum", center_policy=("product", 4), rho_min=0.0, initial_k=24,
+                              threshold=5)
+        assert np.array_equal(res.state.neighbors.ids, ref["nbr_ids"])
+        assert np.array_equal(res.state.lam, ref["lam"])
+        assert np.array_equal(res.clustering.labels, ref["labels"])
+        return
     n = data.shape[0]
     k = min(8, n - 1)
     _pipeline_vs_oracle(data, R=16, L=max(24, k), k=k, nc=min(3, n))
