@@ -1199,11 +1199,14 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     const bool tcp = MODE == MODE_SEQ64 && D.dp <= 128 * QV && QV <= 8 && D.screen && tcmode >= 1 && tcmode <= 3;
     const bool tcb = tcp && tcmode != 3, tcr = tcp && tcmode != 2;
     auto tpk = prune_tc_build_kernel<QV>;
-    auto trk = prune_tc_reverse_kernel<MODE, QV>;
+    auto trk = prune_tc_reverse_kernel<MODE, QV, PT_CAP>;
+    auto trk2 = prune_tc_reverse_kernel<MODE, QV, PT_CAP_BIG>;
     double* nrm64 = nullptr;
     if (tcp) {
         PK_CHECK(cudaFuncSetAttribute(tpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_SMEM));
         PK_CHECK(cudaFuncSetAttribute(trk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_SMEM));
+        PK_CHECK(cudaFuncSetAttribute(trk2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)pt_smem_bytes(PT_CAP_BIG)));
         PK_CHECK(scratch(&nrm64, (size_t)n, st));
         {
             ProfScope _ps("norms64_kernel", st);
@@ -1412,8 +1415,16 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                 rbk<<<grid_bp, BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(B, BP_CAP, midl, nmid, nullptr, nullptr);
             }
         } else if (tcr) {
-            ProfScope _ps("prune_tc_reverse_kernel", st);
-            trk<<<std::min(2 * sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, nrm64);
+            PK_CHECK(cudaMemsetAsync(nmid, 0, sizeof(int), st));
+            {
+                ProfScope _ps("prune_tc_reverse_kernel", st);
+                trk<<<std::min(2 * sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, nrm64, nullptr, nullptr, midl, nmid);
+            }
+            PK_CHECK_LAUNCH("prune_tc_reverse_kernel");
+            {
+                ProfScope _ps("prune_tc_reverse_kernel", st);
+                trk2<<<sm_count(), PT_THREADS, pt_smem_bytes(PT_CAP_BIG), st>>>(B, nrm64, midl, nmid, nullptr, nullptr);
+            }
         } else {
             ProfScope _ps("reverse_kernel", st);
             rk<<<std::min(grid_r, (ubb + wpb_r - 1) / wpb_r), 32 * wpb_r, wbr * wpb_r, st>>>(B);

@@ -32,46 +32,53 @@
 // uses (BuildArgs, RevArgs, BPSmem, bp_sort, bp_unique, prune_by_selection).
 #pragma once
 
-constexpr int PT_CAP = 512;   // unique candidates per item (bit rows in 128-row blocks)
-constexpr int PT_SORT = 512;  // candidates sorted per item
-constexpr int PT_WORDS = PT_CAP / 32;  // bit words per row
+constexpr int PT_CAP = 512;   // candidates per item, two-CTA-per-SM kernels (bit rows in 128-row blocks)
+constexpr int PT_CAP_BIG = 1024;  // reverse groups of 513..1024 candidates: one CTA per SM
 constexpr int PT_THREADS = 128;
 constexpr int PT_STAGES = 2;  // two CTAs per SM (TMEM 2 x 256 columns, smem 2 x ~100 KB)
 constexpr int PT_STAGE_BYTES = 256 * 128;  // 256 row slots x 32 fp32
-constexpr size_t PT_SMEM = 1024 + (size_t)PT_STAGES * PT_STAGE_BYTES  // K-chunk stages
-                           + (size_t)PT_SORT * 8 * 2 + (size_t)PT_CAP * 8 * 2  // kd, kd2, nrm, sq (f64)
-                           + (size_t)PT_SORT * 4 * 2                   // ki, ki2
-                           + (size_t)128 * PT_WORDS * 4 * 2            // kill, unc bit rows (one block)
-                           + (size_t)PT_CAP * 8                        // row pointers
-                           + 256;                                      // barriers, scalars
+// shared memory of a kernel with room for `cap` candidates
+__host__ __device__ constexpr size_t pt_smem_bytes(int cap) {
+    return 1024 + (size_t)PT_STAGES * PT_STAGE_BYTES  // K-chunk stages
+           + (size_t)cap * 8 * 4                      // kd, kd2, nrm, sq (f64)
+           + (size_t)cap * 4 * 2                      // ki, ki2
+           + (size_t)128 * (cap / 32) * 4 * 2         // kill, unc bit rows (one 128-row block)
+           + (size_t)cap * 8                          // row pointers
+           + 256;                                     // barriers, scalars
+}
+constexpr size_t PT_SMEM = pt_smem_bytes(PT_CAP);
 
 struct PTSmem {
     unsigned char* stage;  // [PT_STAGES][256][128 B], 1024-aligned
     double* nrm;           // [PT_CAP] |x|^2 of the sorted candidates
     double* sq;            // [PT_CAP] |x|
-    unsigned* kill;        // [128][PT_WORDS] bit rows of the current 128-candidate block
-    unsigned* unc;         // [128][PT_WORDS]
+    unsigned* kill;        // [128][words] bit rows of the current 128-candidate block
+    unsigned* unc;         // [128][words]
+    int words;             // bit words per row (cap / 32)
     unsigned long long* rowp;  // [PT_CAP] global address of each sorted candidate row
     unsigned long long* bar;  // [PT_STAGES] MMAs of the stage's chunk done
     unsigned* tmem_slot;
     BPSmem S;              // kd, ki, kd2, ki2, scal (bp_sort / bp_unique)
 };
 
+template <int CAP>
 __device__ __forceinline__ PTSmem carve_pt(unsigned char* raw) {
+    constexpr int PT_SORT = CAP, PT_WORDS = CAP / 32;
     PTSmem P;
+    P.words = PT_WORDS;
     unsigned char* base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
     P.stage = base;
     unsigned char* q = base + (size_t)PT_STAGES * PT_STAGE_BYTES;
     P.S.kd = reinterpret_cast<double*>(q);
     P.S.kd2 = P.S.kd + PT_SORT;
     P.nrm = P.S.kd2 + PT_SORT;
-    P.sq = P.nrm + PT_CAP;
-    P.S.ki = reinterpret_cast<unsigned*>(P.sq + PT_CAP);
+    P.sq = P.nrm + CAP;
+    P.S.ki = reinterpret_cast<unsigned*>(P.sq + CAP);
     P.S.ki2 = P.S.ki + PT_SORT;
     P.kill = P.S.ki2 + PT_SORT;
     P.unc = P.kill + 128 * PT_WORDS;
     P.rowp = reinterpret_cast<unsigned long long*>(P.unc + 128 * PT_WORDS);
-    P.bar = P.rowp + PT_CAP;
+    P.bar = P.rowp + CAP;
     P.tmem_slot = reinterpret_cast<unsigned*>(P.bar + PT_STAGES + 1);
     P.S.scal = reinterpret_cast<int*>(P.tmem_slot + 2);
     P.S.rows = nullptr;
@@ -252,8 +259,8 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
         }
         if (live) {
             const int word = (b0 >> 5) + wd;
-            P.kill[tid * PT_WORDS + word] = kb;
-            P.unc[tid * PT_WORDS + word] = ub;
+            P.kill[tid * P.words + word] = kb;
+            P.unc[tid * P.words + word] = ub;
         }
     }
     tc_fence_before();
@@ -290,7 +297,7 @@ __device__ bool pt_greedy_block(const float* __restrict__ X, int dp, const PTSme
         if (lane == 0) out[sel] = (int)tid_t;
         ++sel;
         if (sel >= R) return true;
-        const int row = (t - r0) * PT_WORDS;
+        const int row = (t - r0) * P.words;
         unsigned kill = lane < nw ? P.kill[row + lane] : 0u;
         unsigned unc = lane < nw ? (P.unc[row + lane] & alive) : 0u;
         if (__any_sync(PK_FULL, unc != 0u)) {
@@ -325,9 +332,10 @@ __device__ bool pt_greedy_block(const float* __restrict__ X, int dp, const PTSme
 }
 
 // drop `self` and repeated (dist, id) entries of the sorted kd/ki[0, c) (c <=
-// PT_SORT), keep order -> kd2/ki2; returns the count (block-wide)
+// CAP), keep order -> kd2/ki2; returns the count (block-wide)
+template <int CAP>
 __device__ __forceinline__ int pt_unique(const BPSmem& S, int c, unsigned self) {
-    constexpr int E = PT_SORT / PT_THREADS;  // positions per thread
+    constexpr int E = CAP / PT_THREADS;  // positions per thread
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     bool keep[E];
     int mine = 0;
@@ -434,7 +442,7 @@ template <int QV>
 __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs A, const double* __restrict__ nrm64,
                                                                       int* over, int* nover) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const PTSmem P = carve_pt(smem_raw);
+    const PTSmem P = carve_pt<PT_CAP>(smem_raw);
     PTPipe pp;
     pt_setup(P, pp);
     const int tid = threadIdx.x;
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
         const int vl = A.vlen[t];
         const int nd = __ldg(A.P.deg + p);
         const int c0 = vl + nd;
-        if (c0 > PT_SORT) {
+        if (c0 > PT_CAP) {
             if (tid == 0) over[atomicAdd(nover, 1)] = t;
             continue;
         }
@@ -472,7 +480,7 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
         }
         __syncthreads();
         bp_sort(P.S.kd, P.S.ki, Pw);
-        const int c = pt_unique(P.S, c0, p);
+        const int c = pt_unique<PT_CAP>(P.S, c0, p);
         if (c > PT_CAP) {  // more unique candidates than one Gram holds: warp path
             if (tid == 0) over[atomicAdd(nover, 1)] = t;
             __syncthreads();
@@ -498,19 +506,25 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
 
 // reverse-edge re-prune for float data: one block per target vertex with at most
 // PT_CAP candidates (larger groups: reverse_big_kernel / the selection path)
-template <int MODE, int QV>
-__global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_reverse_kernel(RevArgs A, const double* __restrict__ nrm64) {
+// CAP = PT_CAP (two CTAs per SM) over every target: groups of PT_CAP + 1 ..
+// PT_CAP_BIG candidates are queued on (mid, nmid) for the CAP = PT_CAP_BIG
+// launch (one CTA per SM) over items = mid.
+template <int MODE, int QV, int CAP>
+__global__ void __launch_bounds__(PT_THREADS, CAP == PT_CAP ? 2 : 1)
+    prune_tc_reverse_kernel(RevArgs A, const double* __restrict__ nrm64, const int* items, const int* nitems,
+                            int* mid, int* nmid) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const PTSmem P = carve_pt(smem_raw);
+    const PTSmem P = carve_pt<CAP>(smem_raw);
     PTPipe pp;
     pt_setup(P, pp);
     const int tid = threadIdx.x, wid = tid >> 5;
     const MakeAt<MODE, QV> make{A.D};
     const int dp = A.dp;
     const float* X = A.X;
-    const int nt = *A.ntargets;
+    const int nt = items ? *nitems : *A.ntargets;
     long long ev = 0;
-    for (int s = blockIdx.x; s < nt; s += gridDim.x) {
+    for (int it = blockIdx.x; it < nt; it += gridDim.x) {
+        const int s = items ? items[it] : it;
         const unsigned u = (unsigned)A.targets[s];
         if (A.world > 1 && (int)(u % (unsigned)A.world) != A.rank) {
             if (tid == 0) A.cnt[u] = 0;
@@ -522,7 +536,11 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_reverse_kernel(RevArgs
         int* row = A.adj + (size_t)u * A.R;
         const int c0 = nd + size;
         int sel;
-        if (c0 > PT_CAP) {
+        if (c0 > CAP && mid && c0 <= PT_CAP_BIG) {
+            if (tid == 0) mid[atomicAdd(nmid, 1)] = s;
+            continue;
+        }
+        if (c0 > CAP) {
             if (c0 <= A.capB) {
                 if (tid == 0) A.biglist[atomicAdd(A.nbig, 1)] = s;
                 continue;
@@ -548,7 +566,7 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_reverse_kernel(RevArgs
             }
             __syncthreads();
             bp_sort(P.S.kd, P.S.ki, Pw);
-            const int c = pt_unique(P.S, c0, u);
+            const int c = pt_unique<CAP>(P.S, c0, u);
             if (tid == 0) ev += c0;
             if (c <= A.R) {
                 for (int x = tid; x < c; x += PT_THREADS) row[x] = (int)P.S.ki2[x];

@@ -12,12 +12,15 @@ import paper_2312_03940_b200 as pk  # noqa: E402
 from paper_2312_03940_b200 import _lib, vamana, workloads  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 300_000
-w = workloads.WORKLOADS["C5"]
-data, _ = workloads.generate("C5", n=n, components=max(1, n // 1281))
+cfg = sys.argv[2] if len(sys.argv) > 2 else "C5"
+w = workloads.WORKLOADS[cfg]
+data, _ = workloads.generate(cfg, n=n, components=max(1, int(round(w.components * n / w.n))))
 p = pk.PointSet(data)
 g = pk.build_vamana(p, R=w.R, L_build=w.L, alpha=w.alpha, seed=0, query_beam=w.L)
 rng = np.random.default_rng(0)
-for m, k in [(3000, 32), (1000, 256), (800, 512), (700, 1024), (700, 2048)]:
+plan = [(3000, 32), (1000, 256), (800, 512), (700, 1024), (700, 2048)] if cfg != "C3" else \
+    [(30000, 64), (15000, 128), (7600, 256), (3800, 512), (1900, 1024), (970, 2048), (466, 4096)]
+for m, k in plan:
     q = torch.from_numpy(np.sort(rng.choice(n, m, replace=False))).cuda()
     for rep in range(2):
         _lib.prof_collect(reset=True)
