@@ -345,11 +345,21 @@ template <int MODE, int QV>
 int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, int kk, int H,
                     long long* out_ids, double* out_d, long long* counts, long long* evals, cudaStream_t st) {
     size_t wb = align16(beam_smem_bytes(L, H));
-    int wpb = 4;
-    while (wpb > 1 && wb * wpb > (size_t)max_smem_optin()) wpb >>= 1;
-    if (wb * wpb > (size_t)max_smem_optin()) {
+    if (wb > (size_t)max_smem_optin()) {
         set_error("beam width too large for shared memory");
         return 2;
+    }
+    // warps per block: the most resident warps per SM (wide beams: a block of 2
+    // x 64 KB leaves a third warp's worth of the SM's shared memory unused)
+    const size_t sm_bytes = (size_t)max_smem_optin() + 1024;  // per-SM capacity (one block's reserve)
+    int wpb = 1, best = 0;
+    for (int w = 4; w >= 1; w >>= 1) {
+        if (wb * w > (size_t)max_smem_optin()) continue;
+        const int resident = w * (int)std::min<size_t>(32 / w, sm_bytes / (wb * w + 1024));
+        if (resident > best) {
+            best = resident;
+            wpb = w;
+        }
     }
     auto kern = beam_knn_kernel<MODE, QV>;
     PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wb * wpb)));
