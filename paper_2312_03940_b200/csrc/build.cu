@@ -522,7 +522,8 @@ __global__ void __launch_bounds__(128) reverse_kernel(RevArgs A) {
 // per row; the greedy pass is then bit arithmetic (alive &= ~kill[t]).  The
 // picks are identical to the sequential algorithm: the kill decision for (t, u)
 // depends only on the pair and on t being picked.
-constexpr int BP_CAP = 256;      // candidates per item (more -> warp path / big-group path)
+constexpr int BP_CAP = 256;      // candidates per build item (more -> warp path)
+constexpr int BP_CAP_MAX = 512;  // reverse groups: third launch with room for 512 (more -> reverse_big_kernel)
 constexpr int BP_THREADS = 128;
 
 struct BPSmem {
@@ -532,13 +533,17 @@ struct BPSmem {
     unsigned* ki;
     double* kd2;      // [BP_CAP] de-duplicated, sorted
     unsigned* ki2;
-    unsigned* kill;   // [BP_CAP][8] occlusion bits: bit u of row t = t occludes u
+    unsigned* kill;   // [cap][words] occlusion bits: bit u of row t = t occludes u
     int* scal;        // [16] block scalars
+    int words;        // bit words per row: 8 (cap <= 256) or cap / 32
 };
+
+__host__ __device__ constexpr int bp_words(int cap) { return cap > 256 ? cap / 32 : 8; }
 
 // shared memory of one item with room for `cap` (<= BP_CAP) candidates
 __host__ __device__ constexpr size_t bp_smem_bytes(int cap) {
-    return (size_t)cap * 32 * 4 + cap * 4 + cap * 8 * 2 + cap * 4 * 2 + cap * 32 + 16 * 4 + 16;
+    return (size_t)cap * 32 * 4 + cap * 4 + cap * 8 * 2 + cap * 4 * 2 + (size_t)cap * bp_words(cap) * 4 + 16 * 4 +
+           16;
 }
 
 __device__ __forceinline__ BPSmem carve_bp(unsigned char* base, int cap) {
@@ -550,7 +555,8 @@ __device__ __forceinline__ BPSmem carve_bp(unsigned char* base, int cap) {
     S.ki = S.nrm + cap;
     S.ki2 = S.ki + cap;
     S.kill = S.ki2 + cap;
-    S.scal = reinterpret_cast<int*>(S.kill + cap * 8);
+    S.words = bp_words(cap);
+    S.scal = reinterpret_cast<int*>(S.kill + (size_t)cap * S.words);
     return S;
 }
 
@@ -601,18 +607,19 @@ __device__ __forceinline__ void bp_sort(double* kd, unsigned* ki, int P) {
 // drop `self` and repeated (dist, id) entries, keep order -> kd2/ki2; returns the count
 __device__ __forceinline__ int bp_unique(const BPSmem& S, int c, unsigned self) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    // thread tid owns positions 2 tid and 2 tid + 1 (c <= 256)
-    bool keep[2];
+    // thread tid owns positions 4 tid .. 4 tid + 3 (c <= 512)
+    bool keep[4];
+    int mine = 0;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const int i = 2 * tid + e;
+    for (int e = 0; e < 4; ++e) {
+        const int i = 4 * tid + e;
         keep[e] = false;
         if (i < c) {
             const unsigned id = S.ki[i];
             keep[e] = id != self && !(i > 0 && S.ki[i - 1] == id && S.kd[i - 1] == S.kd[i]);
         }
+        mine += keep[e];
     }
-    const int mine = (int)keep[0] + (int)keep[1];
     int incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -626,10 +633,10 @@ __device__ __forceinline__ int bp_unique(const BPSmem& S, int c, unsigned self) 
     const int total = S.scal[0] + S.scal[1] + S.scal[2] + S.scal[3];
     int o = base + incl - mine;
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
+    for (int e = 0; e < 4; ++e)
         if (keep[e]) {
-            S.kd2[o] = S.kd[2 * tid + e];
-            S.ki2[o] = S.ki[2 * tid + e];
+            S.kd2[o] = S.kd[4 * tid + e];
+            S.ki2[o] = S.ki[4 * tid + e];
             ++o;
         }
     __syncthreads();
@@ -659,7 +666,7 @@ __device__ int bp_prune(const unsigned* __restrict__ X8, const BPSmem& S, int c,
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
-    for (int e = tid; e < c * 8; e += BP_THREADS) S.kill[e] = 0u;
+    for (int e = tid; e < c * S.words; e += BP_THREADS) S.kill[e] = 0u;
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     for (int x = tid; x < c; x += BP_THREADS) {
@@ -715,7 +722,7 @@ __device__ int bp_prune(const unsigned* __restrict__ X8, const BPSmem& S, int c,
                 const unsigned e0 = lane < 8 ? b00 : b10, e1 = lane < 8 ? b01 : b11;
                 const unsigned byte = bp_spread4((e0 >> (4 * r)) & 15u) | (bp_spread4((e1 >> (4 * r)) & 15u) << 1);
                 const int t = 16 * i + lane;
-                if (t < c) reinterpret_cast<unsigned char*>(S.kill)[t * 32 + j] = (unsigned char)byte;
+                if (t < c) reinterpret_cast<unsigned char*>(S.kill)[t * S.words * 4 + j] = (unsigned char)byte;
             }
         }
     }
@@ -732,7 +739,7 @@ __device__ int bp_prune(const unsigned* __restrict__ X8, const BPSmem& S, int c,
             const int left = c - 32 * w;
             const unsigned valid = left >= 32 ? 0xffffffffu : (1u << left) - 1u;
             unsigned alive = valid & ~__shfl_sync(PK_FULL, acc, w);
-            const unsigned kw = x < c ? S.kill[x * 8 + w] : 0u;
+            const unsigned kw = x < c ? S.kill[x * S.words + w] : 0u;
             const int sel0 = sel;
             unsigned picked = 0u;
             while (alive && sel < R) {
@@ -746,7 +753,7 @@ __device__ int bp_prune(const unsigned* __restrict__ X8, const BPSmem& S, int c,
             if (mine) out[sel0 + __popc(picked & ((1u << lane) - 1u))] = (int)S.ki2[x];
             if (sel < R) {
                 for (int v = w + 1; v < nw; ++v) {
-                    const unsigned r = __reduce_or_sync(PK_FULL, mine ? S.kill[x * 8 + v] : 0u);
+                    const unsigned r = __reduce_or_sync(PK_FULL, mine ? S.kill[x * S.words + v] : 0u);
                     if (lane == v) acc |= r;
                 }
             }
@@ -830,8 +837,9 @@ __global__ void __launch_bounds__(BP_THREADS) build_prune_block_kernel(BuildArgs
 // reverse-edge re-prune for u8 rows (d = 128): one block per target vertex
 // (groups above BP_CAP go to reverse_big_kernel / the selection path as in
 // reverse_kernel)
-// cap = candidate room of this launch: groups with cap < c0 <= BP_CAP are queued
-// on (mid, nmid) for a second launch with cap = BP_CAP over items = mid.
+// cap = candidate room of this launch: groups with cap < c0 <= BP_CAP_MAX are
+// queued on (mid, nmid) for the next launch (cap 128 -> 256 -> 512, each over
+// the previous one's queue; the last launch passes mid = null).
 template <int MODE, int QV>
 __global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A, int cap, const int* items,
                                                                    const int* nitems, int* mid, int* nmid) {
@@ -854,11 +862,11 @@ __global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A, in
         int* row = A.adj + (size_t)u * A.R;
         const int c0 = nd + size;
         int sel;
-        if (c0 > cap && c0 <= BP_CAP) {
+        if (c0 > cap && c0 <= BP_CAP_MAX && mid) {
             if (tid == 0) mid[atomicAdd(nmid, 1)] = s;
             continue;
         }
-        if (c0 > BP_CAP) {
+        if (c0 > BP_CAP_MAX) {
             if (c0 <= A.capB) {
                 if (tid == 0) A.biglist[atomicAdd(A.nbig, 1)] = s;
                 continue;
@@ -1187,7 +1195,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     if (blockp) {
         const int bytes = (int)bp_smem_bytes(BP_CAP);
         PK_CHECK(cudaFuncSetAttribute(bpk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        PK_CHECK(cudaFuncSetAttribute(rbk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        PK_CHECK(cudaFuncSetAttribute(rbk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)bp_smem_bytes(BP_CAP_MAX)));
         int per_sm = 0;
         PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bpk, BP_THREADS, bytes));
         grid_bp = sm_count() * std::max(1, per_sm);
@@ -1249,9 +1258,11 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     int *over = nullptr, *nover = nullptr;
     PK_CHECK(scratch(&over, (size_t)mb, st));
     PK_CHECK(scratch(&nover, 1, st));
-    int *midl = nullptr, *nmid = nullptr;
+    int *midl = nullptr, *nmid = nullptr, *midl2 = nullptr, *nmid2 = nullptr;
     PK_CHECK(scratch(&midl, (size_t)ub, st));
     PK_CHECK(scratch(&nmid, 1, st));
+    PK_CHECK(scratch(&midl2, (size_t)ub, st));
+    PK_CHECK(scratch(&nmid2, 1, st));
     PK_CHECK(scratch(&cnt, (size_t)n, st));
     PK_CHECK(scratch(&tslot, (size_t)n, st));
     PK_CHECK(scratch(&targets, (size_t)ub, st));
@@ -1410,9 +1421,16 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                                                                                        midl, nmid);
             }
             PK_CHECK_LAUNCH("reverse_block_kernel");
+            PK_CHECK(cudaMemsetAsync(nmid2, 0, sizeof(int), st));
             {
                 ProfScope _ps("reverse_block_kernel", st);
-                rbk<<<grid_bp, BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(B, BP_CAP, midl, nmid, nullptr, nullptr);
+                rbk<<<grid_bp, BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(B, BP_CAP, midl, nmid, midl2, nmid2);
+            }
+            PK_CHECK_LAUNCH("reverse_block_kernel");
+            {
+                ProfScope _ps("reverse_block_kernel", st);
+                rbk<<<2 * sm_count(), BP_THREADS, bp_smem_bytes(BP_CAP_MAX), st>>>(B, BP_CAP_MAX, midl2, nmid2,
+                                                                                   nullptr, nullptr);
             }
         } else if (tcr) {
             PK_CHECK(cudaMemsetAsync(nmid, 0, sizeof(int), st));
@@ -1468,7 +1486,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
-                    (void*)nmid, (void*)ubm, (void*)nrm64, cub_tmp})
+                    (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {
