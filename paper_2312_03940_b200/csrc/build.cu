@@ -604,6 +604,55 @@ __device__ __forceinline__ void bp_sort(double* kd, unsigned* ki, int P) {
         }
 }
 
+// Reverse groups: kd/ki[0, nd) is the target's current row -- every adjacency
+// row is kept (dist, id)-sorted (the build's picks and the re-prunes come out in
+// key order) -- and kd/ki[nd, c0) are this batch's few new sources.  Sort the
+// sources alone (bitonic over a small power of two), then merge the two sorted
+// runs (each element's place = its index + its rank in the other run; equal
+// keys are identical entries, row first).  Replaces the full bitonic sort of c0
+// keys; kd/ki hold the sorted c0 keys afterwards.
+__device__ __forceinline__ void bp_sort_row_plus_adds(const BPSmem& S, int nd, int c0) {
+    const int tid = threadIdx.x;
+    const int sz = c0 - nd;
+    const int P2 = next_pow2_dev(sz < 2 ? 2 : sz);
+    for (int x = c0 + tid; x < nd + P2; x += BP_THREADS) {
+        S.kd[x] = __longlong_as_double(0x7ff0000000000000LL);
+        S.ki[x] = 0xffffffffu;
+    }
+    __syncthreads();
+    if (sz > 1) bp_sort(S.kd + nd, S.ki + nd, P2);
+    for (int x = tid; x < c0; x += BP_THREADS) {
+        const double d = S.kd[x];
+        const unsigned i = S.ki[x];
+        int pos;
+        if (x < nd) {  // row entry: + number of sources strictly below it
+            int lo = 0, hi = sz;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (key_lt(S.kd[nd + mid], S.ki[nd + mid], d, i)) lo = mid + 1;
+                else hi = mid;
+            }
+            pos = x + lo;
+        } else {  // source: + number of row entries not above it
+            int lo = 0, hi = nd;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (!key_lt(d, i, S.kd[mid], S.ki[mid])) lo = mid + 1;
+                else hi = mid;
+            }
+            pos = x - nd + lo;
+        }
+        S.kd2[pos] = d;
+        S.ki2[pos] = i;
+    }
+    __syncthreads();
+    for (int x = tid; x < c0; x += BP_THREADS) {
+        S.kd[x] = S.kd2[x];
+        S.ki[x] = S.ki2[x];
+    }
+    __syncthreads();
+}
+
 // drop `self` and repeated (dist, id) entries, keep order -> kd2/ki2; returns the count
 __device__ __forceinline__ int bp_unique(const BPSmem& S, int c, unsigned self) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -896,13 +945,18 @@ __global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A, in
                 S.ki[x] = id;
                 S.kd[x] = (double)bp_dist_global(q, nq, A.D.X8 + (size_t)id * 32);
             }
-            const int P = next_pow2_dev(c0 < 2 ? 2 : c0);
-            for (int x = c0 + tid; x < P; x += BP_THREADS) {
-                S.kd[x] = __longlong_as_double(0x7ff0000000000000LL);
-                S.ki[x] = 0xffffffffu;
+            if (c0 - nd <= 64 && nd + 64 <= cap) {
+                __syncthreads();
+                bp_sort_row_plus_adds(S, nd, c0);
+            } else {
+                const int P = next_pow2_dev(c0 < 2 ? 2 : c0);
+                for (int x = c0 + tid; x < P; x += BP_THREADS) {
+                    S.kd[x] = __longlong_as_double(0x7ff0000000000000LL);
+                    S.ki[x] = 0xffffffffu;
+                }
+                __syncthreads();
+                bp_sort(S.kd, S.ki, P);
             }
-            __syncthreads();
-            bp_sort(S.kd, S.ki, P);
             const int c = bp_unique(S, c0, u);
             if (tid == 0) ev += c0;
             if (c <= A.R) {
