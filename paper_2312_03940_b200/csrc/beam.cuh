@@ -127,6 +127,19 @@ struct WarpBeam {
         __syncwarp();
     }
 
+    // Exact integer modes store the packed key (dist << 32 | id) in the bd slot
+    // (one 64-bit compare per ordering decision instead of a float64 compare and
+    // an id compare); dist_of() turns a stored slot back into the distance.
+    __device__ __forceinline__ static double dist_of(double slot) {
+        if constexpr (int_keys<Dist>::value)
+            return (double)(unsigned)((unsigned long long)__double_as_longlong(slot) >> 32);
+        else
+            return slot;
+    }
+    __device__ __forceinline__ static unsigned long long kbits(double slot) {
+        return (unsigned long long)__double_as_longlong(slot);
+    }
+
     // Merge the candidates held by lanes with `valid` into the beam.
     // CheckDups: equal keys inside the batch are possible (duplicate start ids
     // in a user start list) -- keep the lowest lane.  Graph neighbours of one
@@ -139,18 +152,35 @@ struct WarpBeam {
         const unsigned cid = cidf & PK_IDMASK;  // cidf may carry PK_APX (stored with the entry)
         int pos = 0;
         bool keep = valid;
-        // a full beam rejects anything not better than its worst entry
-        if (keep && bl == L && !key_lt(cd, cid, bd[L - 1], bi[L - 1] & PK_IDMASK)) keep = false;
-        if (!__any_sync(PK_FULL, keep)) return;
-        if (keep) {
-            int lo = 0, hi = bl;
-            while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (key_lt(bd[mid], bi[mid] & PK_IDMASK, cd, cid)) lo = mid + 1;
-                else hi = mid;
+        // exact modes: distances are integers < 2^32, (dist, id) packs into one u64
+        const unsigned long long mk = int_keys<Dist>::value ? ((unsigned long long)(unsigned)cd << 32) | cid : 0ull;
+        if constexpr (int_keys<Dist>::value) {
+            if (keep && bl == L && !(mk < kbits(bd[L - 1]))) keep = false;
+            if (!__any_sync(PK_FULL, keep)) return;
+            if (keep) {
+                int lo = 0, hi = bl;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (kbits(bd[mid]) < mk) lo = mid + 1;
+                    else hi = mid;
+                }
+                pos = lo;
+                if (pos < bl && kbits(bd[pos]) == mk) keep = false;
             }
-            pos = lo;
-            if (pos < bl && bd[pos] == cd && (bi[pos] & PK_IDMASK) == cid) keep = false;
+        } else {
+            // a full beam rejects anything not better than its worst entry
+            if (keep && bl == L && !key_lt(cd, cid, bd[L - 1], bi[L - 1] & PK_IDMASK)) keep = false;
+            if (!__any_sync(PK_FULL, keep)) return;
+            if (keep) {
+                int lo = 0, hi = bl;
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (key_lt(bd[mid], bi[mid] & PK_IDMASK, cd, cid)) lo = mid + 1;
+                    else hi = mid;
+                }
+                pos = lo;
+                if (pos < bl && bd[pos] == cd && (bi[pos] & PK_IDMASK) == cid) keep = false;
+            }
         }
         unsigned fb = __ballot_sync(PK_FULL, keep);
         if (!fb) return;
@@ -167,8 +197,6 @@ struct WarpBeam {
         }
         int rank = 0;
         if constexpr (int_keys<Dist>::value) {
-            // exact modes: distances are integers < 2^32, (dist, id) packs into one u64
-            const unsigned long long mk = ((unsigned long long)(unsigned)cd << 32) | cid;
             for (unsigned b = fb; b; b &= b - 1) {
                 const unsigned long long kj = __shfl_sync(PK_FULL, mk, __ffs(b) - 1);
                 rank += kj < mk;
@@ -235,7 +263,7 @@ struct WarpBeam {
         }
         const int np = pos + rank;
         if (keep && np < L) {
-            bd[np] = cd;
+            bd[np] = int_keys<Dist>::value ? __longlong_as_double((long long)mk) : cd;
             bi[np] = cidf;
         }
         int mn = (keep && np < L) ? np : 0x7fffffff;
@@ -514,7 +542,7 @@ struct WarpBeam {
             if (pos < 0) break;
             const unsigned pf = sm.bi[pos] & PK_IDAPX;
             const unsigned p = pf & PK_IDMASK;
-            const double pd = sm.bd[pos];
+            const double pd = dist_of(sm.bd[pos]);
             __syncwarp();
             if (lane == 0) {
                 sm.bi[pos] = pf | PK_VIS;
@@ -589,7 +617,7 @@ struct WarpBeam {
                     const int at = vl + __popc(run & ((1u << lane) - 1u));
                     if (at < vcap) {
                         vlog_i[at] = iv & PK_IDAPX;
-                        vlog_d[at] = sm.bd[e];
+                        vlog_d[at] = dist_of(sm.bd[e]);
                     } else {
                         atomicOr(err, ERR_VISIT_OVERFLOW);
                     }
@@ -670,7 +698,7 @@ struct WarpBeam {
             int o = got + warp_excl_prefix(b);
             const bool out = ok && o < kk;
             const bool apx = out && (f & PK_APX);
-            double v = e < bl ? sm.bd[e] : 0.0;
+            double v = e < bl ? dist_of(sm.bd[e]) : 0.0;
             if (__any_sync(PK_FULL, apx)) {
                 if (apx) v = exact_of(id);
                 const unsigned nb_ = __ballot_sync(PK_FULL, apx);
@@ -689,7 +717,7 @@ struct WarpBeam {
         if (got < kk && bi_ != 0xffffffffu && (bi_ & PK_IDMASK) != self) {
             if (lane == 0) {
                 out_ids[got] = bi_ & PK_IDMASK;
-                out_d[got] = (bi_ & PK_APX) ? exact_of(bi_ & PK_IDMASK) : bd_;
+                out_d[got] = (bi_ & PK_APX) ? exact_of(bi_ & PK_IDMASK) : dist_of(bd_);
             }
             ++got;
         }
