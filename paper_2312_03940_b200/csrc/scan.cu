@@ -165,7 +165,48 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs A) {
     }
     const int chunk = kScanThreads * kScanPPT;
     const int j0 = blockIdx.y * chunk;
+    if constexpr (OP == SCAN_COUNT && MODE == MODE_EXACT_U8) {
+        // register-blocked count scan on packed u8 rows: each thread carries its
+        // kScanPPT points through the words together, so every staged query word
+        // is read once per kScanPPT points (exact integer distances, any order)
+        const int dw = A.D.dw;
+        int js[kScanPPT];
+        const unsigned* rp[kScanPPT];
+        unsigned acc[kScanPPT][kScanQ];
+#pragma unroll
+        for (int p = 0; p < kScanPPT; ++p) {
+            js[p] = j0 + threadIdx.x + p * kScanThreads;
+            rp[p] = A.D.X8 + (size_t)min(js[p], A.n - 1) * dw;
+#pragma unroll
+            for (int a = 0; a < kScanQ; ++a) acc[p][a] = 0u;
+        }
+        const unsigned* qw = tile.q;
+        for (int w = 0; w < dw; ++w) {
+            unsigned x[kScanPPT];
+#pragma unroll
+            for (int p = 0; p < kScanPPT; ++p) x[p] = __ldg(rp[p] + w);
+#pragma unroll
+            for (int a = 0; a < kScanQ; ++a) {
+                const unsigned qa = qw[a * dw + w];
+#pragma unroll
+                for (int p = 0; p < kScanPPT; ++p) {
+                    const unsigned v = __vabsdiffu4(qa, x[p]);
+                    acc[p][a] = __dp4a(v, v, acc[p][a]);
+                }
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < kScanPPT; ++p) {
+            if (js[p] >= A.n) continue;
+#pragma unroll
+            for (int a = 0; a < kScanQ; ++a)
+                if (a < nq && (long long)js[p] != qid[a] &&
+                    key_lt((double)acc[p][a], (unsigned)js[p], kdd[a], (unsigned)kdi[a]))
+                    ++cnt[a];
+        }
+    }
     for (int jj = threadIdx.x; jj < chunk; jj += kScanThreads) {
+        if constexpr (OP == SCAN_COUNT && MODE == MODE_EXACT_U8) break;
         const int j = j0 + jj;
         if (j >= A.n) break;
         long long rj = 0;

@@ -358,17 +358,24 @@ def test_build_with_short_candidate_lists_matches_oracle(kind):
     assert np.array_equal(g.graph.adjacency, adj)
 
 
-@pytest.mark.parametrize("d", [48, 384, 1024])
+@pytest.mark.parametrize("d", [48, 384, 1024, "u8"])
 def test_count_below_matches_exact_rows(d):
-    """pk_count_below (fp32-screened count scan, exact float64 inside the band)
-    == the position of the key in the exact brute-force row (oracle)."""
+    """pk_count_below (float data: fp32-screened count scan, exact float64 inside
+    the band; u8 rows: register-blocked exact integer scan) == the position of
+    the key in the exact brute-force row (oracle)."""
     import torch
 
-    rng = np.random.default_rng(d)
+    rng = np.random.default_rng(7 if d == "u8" else d)
     n = 3_000
-    data = (rng.normal(size=(n, d)) + rng.normal(size=(8, d))[rng.integers(0, 8, n)]).astype(np.float32)
+    if d == "u8":
+        mu = rng.uniform(0, 255, (8, 128))
+        data = np.clip(np.round(mu[rng.integers(0, 8, n)] + rng.normal(0, 20, (n, 128))), 0, 255).astype(np.float32)
+    else:
+        data = (rng.normal(size=(n, d)) + rng.normal(size=(8, d))[rng.integers(0, 8, n)]).astype(np.float32)
     data[:20] = data[20:40]  # duplicates: zero distances and tied keys
     p = pk.PointSet(data)
+    if d == "u8":
+        assert p.mode == _lib.MODE_EXACT_U8
     qids = np.sort(rng.choice(n, 40, replace=False)).astype(np.int64)
     ids, sqd = oracle.brute_knn_batch(data, qids, n - 1)
     pos = rng.integers(0, n - 1, qids.shape[0])
