@@ -372,6 +372,125 @@ extern "C" int pk_dp_scan(const float* x, int64_t n, int64_t dp, const uint32_t*
     return 0;
 }
 
+// ---- u8 rows of d = 128 (32 words): count scan on the integer tensor cores ----------------
+// Exact u8 x u8 -> s32 mma.sync tiles (m16n8k32): a block holds 64 queries (4
+// warps x 16 rows, A fragments in registers) and streams 64-point tiles of the
+// packed rows through shared memory (cp.async, double-buffered, 16-byte chunks
+// XOR-swizzled by row); every accumulator becomes the exact integer distance
+// |q|^2 + |x|^2 - 2 q.x and is compared with the row's key.
+constexpr int CU_Q = 64, CU_P = 64;
+
+__device__ __forceinline__ int cu_swz(int r, int w) { return r * 32 + (w ^ ((r & 7) << 2)); }
+
+__device__ __forceinline__ void cu_mma(const unsigned (&a)[4], unsigned b0, unsigned b1, int (&d)[4]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void cu_stage(const unsigned* __restrict__ X8, int n, int p0, unsigned* dst) {
+    for (int e = threadIdx.x; e < CU_P * 8; e += 128) {
+        const int r = e >> 3, ch = e & 7;
+        const int j = min(p0 + r, n - 1);
+        const unsigned d = (unsigned)__cvta_generic_to_shared(dst + r * 32 + ((ch ^ (r & 7)) << 2));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(X8 + (size_t)j * 32 + ch * 4)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(128) count_u8_tc_kernel(const unsigned* __restrict__ X8, int n,
+                                                         const long long* __restrict__ qids, int m,
+                                                         const double* __restrict__ key_d,
+                                                         const long long* __restrict__ key_i, int tiles_per_block,
+                                                         long long* __restrict__ count) {
+    __shared__ __align__(16) unsigned qs[CU_Q * 32];
+    __shared__ __align__(16) unsigned ps[2][CU_P * 32];
+    __shared__ unsigned pn[2][CU_P];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, tig = lane & 3;
+    const int q0 = blockIdx.x * CU_Q;
+    for (int e = tid; e < CU_Q * 8; e += 128) {
+        const int r = e >> 3, ch = e & 7;
+        const long long qi = qids[min(q0 + r, m - 1)];
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(X8 + (size_t)qi * 32 + ch * 4));
+        *reinterpret_cast<uint4*>(qs + r * 32 + ((ch ^ (r & 7)) << 2)) = v;
+    }
+    const int t0 = blockIdx.y * tiles_per_block;
+    const int ntile = (n + CU_P - 1) / CU_P;
+    const int t1 = min(ntile, t0 + tiles_per_block);
+    if (t0 < t1) cu_stage(X8, n, t0 * CU_P, ps[0]);
+    __syncthreads();
+    // this warp's 16 query rows: A fragments, norms, keys
+    const int ra = warp * 16 + g, rb = ra + 8;
+    unsigned a[4][4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+        a[ks][0] = qs[cu_swz(ra, ks * 8 + tig)];
+        a[ks][1] = qs[cu_swz(rb, ks * 8 + tig)];
+        a[ks][2] = qs[cu_swz(ra, ks * 8 + 4 + tig)];
+        a[ks][3] = qs[cu_swz(rb, ks * 8 + 4 + tig)];
+    }
+    unsigned na = 0u, nb = 0u;
+    for (int w = 0; w < 32; ++w) {
+        const unsigned x = qs[cu_swz(ra, w)], y = qs[cu_swz(rb, w)];
+        na = __dp4a(x, x, na);
+        nb = __dp4a(y, y, nb);
+    }
+    const bool va = q0 + ra < m, vb = q0 + rb < m;
+    const long long sa = va ? qids[q0 + ra] : -1, sb = vb ? qids[q0 + rb] : -1;
+    const double ka = va ? key_d[q0 + ra] : -1.0, kb = vb ? key_d[q0 + rb] : -1.0;
+    const unsigned ia = va ? (unsigned)key_i[q0 + ra] : 0u, ib = vb ? (unsigned)key_i[q0 + rb] : 0u;
+    int ca = 0, cb = 0;
+    for (int t = t0; t < t1; ++t) {
+        const int buf = (t - t0) & 1;
+        if (t + 1 < t1) cu_stage(X8, n, (t + 1) * CU_P, ps[buf ^ 1]);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncthreads();
+        const unsigned* P = ps[buf];
+        if (tid < CU_P) {
+            unsigned s0 = 0u;
+            for (int w = 0; w < 32; ++w) {
+                const unsigned x = P[cu_swz(tid, w)];
+                s0 = __dp4a(x, x, s0);
+            }
+            pn[buf][tid] = s0;
+        }
+        __syncthreads();
+        const int pbase = t * CU_P;
+#pragma unroll
+        for (int nt = 0; nt < CU_P / 8; ++nt) {
+            int d[4] = {0, 0, 0, 0};
+            const int col = nt * 8 + g;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+                cu_mma(a[ks], P[cu_swz(col, ks * 8 + tig)], P[cu_swz(col, ks * 8 + 4 + tig)], d);
+            const int c0 = nt * 8 + 2 * tig;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = pbase + c0 + h;
+                if (j >= n) continue;
+                const unsigned pj = pn[buf][c0 + h];
+                const double da = (double)(na + pj - 2u * (unsigned)d[h]);
+                const double db = (double)(nb + pj - 2u * (unsigned)d[2 + h]);
+                if (va && (long long)j != sa && key_lt(da, (unsigned)j, ka, ia)) ++ca;
+                if (vb && (long long)j != sb && key_lt(db, (unsigned)j, kb, ib)) ++cb;
+            }
+        }
+        __syncthreads();
+    }
+    ca += __shfl_xor_sync(PK_FULL, ca, 1);
+    ca += __shfl_xor_sync(PK_FULL, ca, 2);
+    cb += __shfl_xor_sync(PK_FULL, cb, 1);
+    cb += __shfl_xor_sync(PK_FULL, cb, 2);
+    if (tig == 0) {
+        if (va && ca) atomicAdd(reinterpret_cast<unsigned long long*>(count + q0 + ra), (unsigned long long)ca);
+        if (vb && cb) atomicAdd(reinterpret_cast<unsigned long long*>(count + q0 + rb), (unsigned long long)cb);
+    }
+}
+
 extern "C" int pk_count_below(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
                               const int64_t* qids, int64_t m, const double* key_d, const int64_t* key_i,
                               int64_t* out_count, void* stream) {
@@ -386,6 +505,22 @@ extern "C" int pk_count_below(const float* x, int64_t n, int64_t dp, const uint3
     A.key_i = reinterpret_cast<const long long*>(key_i);
     A.count = reinterpret_cast<long long*>(out_count);
     PK_CHECK(cudaMemsetAsync(out_count, 0, sizeof(int64_t) * (size_t)m, st));
+    if (mode == MODE_EXACT_U8 && dw == 32 && x8 && env_int("PK_U8_TC_SCAN", 1) == 1) {
+        const int qt = (int)((m + CU_Q - 1) / CU_Q);
+        const int ntile = (int)((n + CU_P - 1) / CU_P);
+        // enough blocks for ~4 waves of 148 SMs x 8 blocks
+        int splits = std::max(1, std::min(ntile, (sm_count() * 32 + qt - 1) / qt));
+        const int per = (ntile + splits - 1) / splits;
+        splits = (ntile + per - 1) / per;
+        {
+            ProfScope _ps("count_u8_tc_kernel", st);
+            count_u8_tc_kernel<<<dim3(qt, splits), 128, 0, st>>>(
+                x8, (int)n, reinterpret_cast<const long long*>(qids), (int)m, key_d,
+                reinterpret_cast<const long long*>(key_i), per, reinterpret_cast<long long*>(out_count));
+        }
+        PK_CHECK_LAUNCH("count_u8_tc_kernel");
+        return 0;
+    }
     int nc = 0;
     return dispatch_scan<SCAN_COUNT>(mode, A, st, &nc);
 }
