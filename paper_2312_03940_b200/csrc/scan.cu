@@ -340,6 +340,9 @@ extern int compact_flagged(const long long* in, const unsigned char* flags, long
 
 using namespace pk;
 
+int dp_scan_u8_tc(const uint32_t* x8, int64_t n, const int64_t* rank, const int64_t* qids, int64_t m, int64_t* out_id,
+                  double* out_sqd, cudaStream_t st);
+
 extern "C" int pk_dp_scan(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
                           const int64_t* rank, const int64_t* qids, int64_t m, int64_t* out_id, double* out_sqd,
                           void* stream) {
@@ -349,6 +352,8 @@ extern "C" int pk_dp_scan(const float* x, int64_t n, int64_t dp, const uint32_t*
         set_error("u8 mode needs the packed rows");
         return 2;
     }
+    if (mode == MODE_EXACT_U8 && dw == 32 && n < (1ll << 30) && env_int("PK_U8_TC_SCAN", 1) == 1)
+        return dp_scan_u8_tc(x8, n, rank, qids, m, out_id, out_sqd, as_stream(stream));
     ScanArgs A{};
     A.D = DataRef{x, (int)dp, x8, (int)dw};
     A.n = (int)n;
@@ -400,14 +405,21 @@ __device__ __forceinline__ void cu_stage(const unsigned* __restrict__ X8, int n,
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-__global__ void __launch_bounds__(128) count_u8_tc_kernel(const unsigned* __restrict__ X8, int n,
-                                                         const long long* __restrict__ qids, int m,
-                                                         const double* __restrict__ key_d,
-                                                         const long long* __restrict__ key_i, int tiles_per_block,
-                                                         long long* __restrict__ count) {
+// OP = SCAN_COUNT: count[q] += #{j != q : (d, j) < key}; OP = SCAN_DENSER:
+// best[q] = min over j with rank[j] > rank[q] of the packed key (d << 32 | j)
+// (exact integer distances < 2^32, ids < 2^30: the u64 order is the (d, id) order).
+template <int OP>
+__global__ void __launch_bounds__(128) u8_tc_scan_kernel(const unsigned* __restrict__ X8, int n,
+                                                        const long long* __restrict__ qids, int m,
+                                                        const double* __restrict__ key_d,
+                                                        const long long* __restrict__ key_i,
+                                                        const long long* __restrict__ rank, int tiles_per_block,
+                                                        long long* __restrict__ count,
+                                                        unsigned long long* __restrict__ best) {
     __shared__ __align__(16) unsigned qs[CU_Q * 32];
     __shared__ __align__(16) unsigned ps[2][CU_P * 32];
     __shared__ unsigned pn[2][CU_P];
+    __shared__ long long pr[2][CU_P];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, tig = lane & 3;
     const int q0 = blockIdx.x * CU_Q;
@@ -440,9 +452,20 @@ __global__ void __launch_bounds__(128) count_u8_tc_kernel(const unsigned* __rest
     }
     const bool va = q0 + ra < m, vb = q0 + rb < m;
     const long long sa = va ? qids[q0 + ra] : -1, sb = vb ? qids[q0 + rb] : -1;
-    const double ka = va ? key_d[q0 + ra] : -1.0, kb = vb ? key_d[q0 + rb] : -1.0;
-    const unsigned ia = va ? (unsigned)key_i[q0 + ra] : 0u, ib = vb ? (unsigned)key_i[q0 + rb] : 0u;
+    double ka = -1.0, kb = -1.0;
+    unsigned ia = 0u, ib = 0u;
+    long long rka = 0x7fffffffffffffffLL, rkb = 0x7fffffffffffffffLL;
+    if constexpr (OP == SCAN_COUNT) {
+        ka = va ? key_d[q0 + ra] : -1.0;
+        kb = vb ? key_d[q0 + rb] : -1.0;
+        ia = va ? (unsigned)key_i[q0 + ra] : 0u;
+        ib = vb ? (unsigned)key_i[q0 + rb] : 0u;
+    } else {
+        if (va) rka = rank[sa];
+        if (vb) rkb = rank[sb];
+    }
     int ca = 0, cb = 0;
+    unsigned long long ba = ~0ull, bb = ~0ull;
     for (int t = t0; t < t1; ++t) {
         const int buf = (t - t0) & 1;
         if (t + 1 < t1) cu_stage(X8, n, (t + 1) * CU_P, ps[buf ^ 1]);
@@ -457,6 +480,10 @@ __global__ void __launch_bounds__(128) count_u8_tc_kernel(const unsigned* __rest
                 s0 = __dp4a(x, x, s0);
             }
             pn[buf][tid] = s0;
+            if constexpr (OP == SCAN_DENSER) {
+                const int j = t * CU_P + tid;
+                pr[buf][tid] = j < n ? rank[j] : -1;
+            }
         }
         __syncthreads();
         const int pbase = t * CU_P;
@@ -473,22 +500,84 @@ __global__ void __launch_bounds__(128) count_u8_tc_kernel(const unsigned* __rest
                 const int j = pbase + c0 + h;
                 if (j >= n) continue;
                 const unsigned pj = pn[buf][c0 + h];
-                const double da = (double)(na + pj - 2u * (unsigned)d[h]);
-                const double db = (double)(nb + pj - 2u * (unsigned)d[2 + h]);
-                if (va && (long long)j != sa && key_lt(da, (unsigned)j, ka, ia)) ++ca;
-                if (vb && (long long)j != sb && key_lt(db, (unsigned)j, kb, ib)) ++cb;
+                const unsigned ua = na + pj - 2u * (unsigned)d[h], ub = nb + pj - 2u * (unsigned)d[2 + h];
+                if constexpr (OP == SCAN_COUNT) {
+                    if (va && (long long)j != sa && key_lt((double)ua, (unsigned)j, ka, ia)) ++ca;
+                    if (vb && (long long)j != sb && key_lt((double)ub, (unsigned)j, kb, ib)) ++cb;
+                } else {
+                    const long long rj = pr[buf][c0 + h];
+                    const unsigned long long pa = ((unsigned long long)ua << 32) | (unsigned)j;
+                    const unsigned long long pb = ((unsigned long long)ub << 32) | (unsigned)j;
+                    if (rj > rka && pa < ba) ba = pa;
+                    if (rj > rkb && pb < bb) bb = pb;
+                }
             }
         }
         __syncthreads();
     }
-    ca += __shfl_xor_sync(PK_FULL, ca, 1);
-    ca += __shfl_xor_sync(PK_FULL, ca, 2);
-    cb += __shfl_xor_sync(PK_FULL, cb, 1);
-    cb += __shfl_xor_sync(PK_FULL, cb, 2);
-    if (tig == 0) {
-        if (va && ca) atomicAdd(reinterpret_cast<unsigned long long*>(count + q0 + ra), (unsigned long long)ca);
-        if (vb && cb) atomicAdd(reinterpret_cast<unsigned long long*>(count + q0 + rb), (unsigned long long)cb);
+    if constexpr (OP == SCAN_COUNT) {
+        ca += __shfl_xor_sync(PK_FULL, ca, 1);
+        ca += __shfl_xor_sync(PK_FULL, ca, 2);
+        cb += __shfl_xor_sync(PK_FULL, cb, 1);
+        cb += __shfl_xor_sync(PK_FULL, cb, 2);
+        if (tig == 0) {
+            if (va && ca) atomicAdd(reinterpret_cast<unsigned long long*>(count + q0 + ra), (unsigned long long)ca);
+            if (vb && cb) atomicAdd(reinterpret_cast<unsigned long long*>(count + q0 + rb), (unsigned long long)cb);
+        }
+    } else {
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+            ba = min(ba, __shfl_xor_sync(PK_FULL, ba, o));
+            bb = min(bb, __shfl_xor_sync(PK_FULL, bb, o));
+        }
+        if (tig == 0) {
+            if (va && ba != ~0ull) atomicMin(best + q0 + ra, ba);
+            if (vb && bb != ~0ull) atomicMin(best + q0 + rb, bb);
+        }
     }
+}
+
+__global__ void u8_tc_best_kernel(const unsigned long long* best, int m, long long* out_id, double* out_d) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const unsigned long long b = best[t];
+    out_id[t] = b == ~0ull ? -1 : (long long)(b & 0xffffffffull);
+    out_d[t] = b == ~0ull ? __longlong_as_double(0x7ff0000000000000LL) : (double)(unsigned)(b >> 32);
+}
+
+// grid: one block per 64 queries x point splits (~32 blocks per SM overall)
+template <int OP>
+int launch_u8_tc_scan(const unsigned* x8, int64_t n, const int64_t* qids, int64_t m, const double* key_d,
+                      const int64_t* key_i, const int64_t* rank, long long* count, unsigned long long* best,
+                      cudaStream_t st) {
+    const int qt = (int)((m + CU_Q - 1) / CU_Q);
+    const int ntile = (int)((n + CU_P - 1) / CU_P);
+    int splits = std::max(1, std::min(ntile, (sm_count() * 32 + qt - 1) / qt));
+    const int per = (ntile + splits - 1) / splits;
+    splits = (ntile + per - 1) / per;
+    ProfScope _ps(OP == SCAN_COUNT ? "count_u8_tc_kernel" : "denser_u8_tc_kernel", st);
+    u8_tc_scan_kernel<OP><<<dim3(qt, splits), 128, 0, st>>>(
+        x8, (int)n, reinterpret_cast<const long long*>(qids), (int)m, key_d, reinterpret_cast<const long long*>(key_i),
+        reinterpret_cast<const long long*>(rank), per, count, best);
+    PK_CHECK_LAUNCH("u8_tc_scan_kernel");
+    return 0;
+}
+
+int dp_scan_u8_tc(const uint32_t* x8, int64_t n, const int64_t* rank, const int64_t* qids, int64_t m, int64_t* out_id,
+                  double* out_sqd, cudaStream_t st) {
+    unsigned long long* best = nullptr;
+    PK_CHECK(scratch(&best, (size_t)m, st));
+    PK_CHECK(cudaMemsetAsync(best, 0xff, sizeof(unsigned long long) * (size_t)m, st));
+    int rc = launch_u8_tc_scan<SCAN_DENSER>(x8, n, qids, m, nullptr, nullptr, rank, nullptr, best, st);
+    if (rc) return rc;
+    {
+        ProfScope _ps("u8_tc_best_kernel", st);
+        u8_tc_best_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(best, (int)m, reinterpret_cast<long long*>(out_id),
+                                                                    out_sqd);
+    }
+    PK_CHECK_LAUNCH("u8_tc_best_kernel");
+    release(best, st);
+    return 0;
 }
 
 extern "C" int pk_count_below(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
@@ -505,22 +594,9 @@ extern "C" int pk_count_below(const float* x, int64_t n, int64_t dp, const uint3
     A.key_i = reinterpret_cast<const long long*>(key_i);
     A.count = reinterpret_cast<long long*>(out_count);
     PK_CHECK(cudaMemsetAsync(out_count, 0, sizeof(int64_t) * (size_t)m, st));
-    if (mode == MODE_EXACT_U8 && dw == 32 && x8 && env_int("PK_U8_TC_SCAN", 1) == 1) {
-        const int qt = (int)((m + CU_Q - 1) / CU_Q);
-        const int ntile = (int)((n + CU_P - 1) / CU_P);
-        // enough blocks for ~4 waves of 148 SMs x 8 blocks
-        int splits = std::max(1, std::min(ntile, (sm_count() * 32 + qt - 1) / qt));
-        const int per = (ntile + splits - 1) / splits;
-        splits = (ntile + per - 1) / per;
-        {
-            ProfScope _ps("count_u8_tc_kernel", st);
-            count_u8_tc_kernel<<<dim3(qt, splits), 128, 0, st>>>(
-                x8, (int)n, reinterpret_cast<const long long*>(qids), (int)m, key_d,
-                reinterpret_cast<const long long*>(key_i), per, reinterpret_cast<long long*>(out_count));
-        }
-        PK_CHECK_LAUNCH("count_u8_tc_kernel");
-        return 0;
-    }
+    if (mode == MODE_EXACT_U8 && dw == 32 && x8 && env_int("PK_U8_TC_SCAN", 1) == 1)
+        return launch_u8_tc_scan<SCAN_COUNT>(x8, n, qids, m, key_d, key_i, nullptr,
+                                             reinterpret_cast<long long*>(out_count), nullptr, st);
     int nc = 0;
     return dispatch_scan<SCAN_COUNT>(mode, A, st, &nc);
 }

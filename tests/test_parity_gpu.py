@@ -426,6 +426,33 @@ def test_tensor_core_dp_scan_equals_exact_scan(case):
     assert torch.equal(s0, s1)
 
 
+def test_u8_tensor_core_dp_scan_equals_cuda_core_scan(monkeypatch):
+    """u8 rows (d = 128): the integer tensor-core nearest-denser scan (packed
+    (d, id) keys, atomicMin) == the CUDA-core scan, with density ties and
+    duplicate points."""
+    rng = np.random.default_rng(4)
+    mu = rng.uniform(0, 255, (6, 128))
+    data = np.clip(np.round(mu[rng.integers(0, 6, 5_000)] + rng.normal(0, 20, (5_000, 128))), 0, 255)
+    data[:30] = data[30:60]
+    p = pk.PointSet(data.astype(np.float32))
+    assert p.mode == _lib.MODE_EXACT_U8
+    from paper_2312_03940_b200 import density
+
+    rho = torch.from_numpy(rng.integers(0, 40, p.n).astype(np.float64)).cuda()
+    rank = density.rank_order_device(rho)
+    q = torch.from_numpy(np.sort(rng.choice(p.n, 900, replace=False)).astype(np.int64)).cuda()
+    m = q.shape[0]
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PK_U8_TC_SCAN", flag)
+        i = torch.empty(m, dtype=torch.int64, device="cuda")
+        d = torch.empty(m, dtype=torch.float64, device="cuda")
+        _lib.call("pk_dp_scan", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, rank, q, m, i, d, _lib.stream())
+        out.append((i, d))
+    assert torch.equal(out[0][0], out[1][0])
+    assert torch.equal(out[0][1], out[1][1])
+
+
 def test_device_contingency_equals_host():
     from paper_2312_03940_b200 import metrics
 
