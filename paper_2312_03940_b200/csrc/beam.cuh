@@ -74,6 +74,7 @@ struct SearchParams {
     int prefetch = 1;          // L1 prefetch of the next expansion's adjacency row
     int lazy = 1;              // float data: lazy keys (fp32 screen values until a decision needs the exact one)
     int seed_only = 0;         // profiling aid (PK_SEED_ONLY): stop after seeding
+    int seed_select = 1;       // exact integer modes: seed by selection instead of merges (PK_SEED_SELECT)
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -501,6 +502,15 @@ struct WarpBeam {
     __device__ void seed(const SearchParams& P, const D& dist, bool hash_starts, bool unique) {
         const int lane = lane_id();
         if constexpr (has_screen<D>::value) lazy = P.screen && P.lazy && P.dp <= 128 * D::kQV;
+        if constexpr (int_keys<D>::value) {
+            // needs: L a power of two >= 128 (the 1 KB histogram lives in bd), the
+            // s u32 distances fit the seen table
+            if (unique && !hash_starts && P.s > 32 && P.seed_select && L >= 128 && (L & (L - 1)) == 0 &&
+                2 * P.s <= (int)sm.hmask + 1) {
+                seed_select(P, dist);
+                return;
+            }
+        }
         for (int b = 0; b < P.s; b += 32) {
             const int cnt = min(32, P.s - b);
             unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
@@ -519,6 +529,125 @@ struct WarpBeam {
             if (unique) merge<false>(dd, id, lane < cnt);
             else merge<true>(dd, id, lane < cnt);
         }
+    }
+
+    // Seeding by selection (exact integer modes, strictly increasing start list):
+    // the beam after merging every start is the sorted top-min(L, s) of their
+    // keys (dist, id); id order = start-list order, so the keys are (dist,
+    // index).  Distances go to the (still empty) seen table as u32 scratch, a
+    // radix select on dist (4 passes of 8 bits, histogram in the bd area) finds
+    // the L-th key, the selected entries are packed into bd and sorted (warp
+    // bitonic over L), and the seen table is cleared again.  Replaces ceil(s/32)
+    // merges of a growing beam.
+    template <class D>
+    __device__ void seed_select(const SearchParams& P, const D& dist) {
+        const int lane = lane_id();
+        const int s = P.s;
+        unsigned* dsc = reinterpret_cast<unsigned*>(sm.hash);  // [s] seed distances
+        unsigned* bins = reinterpret_cast<unsigned*>(sm.bd);   // [256] histogram
+        for (int b = 0; b < s; b += 32) {
+            const int cnt = min(32, s - b);
+            const unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
+            count_unique(id, cnt);
+            const double dd = dist.eval(P.X, (int)id, cnt);
+            if (lane == 0) evals += cnt;
+            if (lane < cnt) dsc[b + lane] = (unsigned)dd;
+        }
+        __syncwarp();
+        const int take = min(L, s);
+        // radix select: the take-th smallest distance T, and how many entries
+        // with distance == T are taken (the lowest indices)
+        unsigned prefix = 0u;
+        int need = take;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int x = lane; x < 256; x += 32) bins[x] = 0u;
+            __syncwarp();
+            for (int x = lane; x < s; x += 32) {
+                const unsigned v = dsc[x];
+                if (shift == 24 || (v >> (shift + 8)) == prefix) atomicAdd(bins + ((v >> shift) & 255u), 1u);
+            }
+            __syncwarp();
+            // lane l owns bins 8l .. 8l + 7
+            unsigned c[8], tot = 0u;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                c[i] = bins[8 * lane + i];
+                tot += c[i];
+            }
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned v = __shfl_up_sync(PK_FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const unsigned excl = incl - tot;
+            // the bin where the cumulative count reaches `need`
+            const bool here = excl < (unsigned)need && incl >= (unsigned)need;
+            const unsigned hb = __ballot_sync(PK_FULL, here);
+            const int src = __ffs(hb) - 1;
+            int bin = 0;
+            unsigned before = 0u;
+            if (lane == src) {
+                unsigned acc = excl;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (acc + c[i] >= (unsigned)need) {
+                        bin = 8 * lane + i;
+                        break;
+                    }
+                    acc += c[i];
+                }
+                before = acc;
+            }
+            bin = __shfl_sync(PK_FULL, bin, src);
+            before = __shfl_sync(PK_FULL, before, src);
+            need -= (int)before;
+            prefix = (prefix << 8) | (unsigned)bin;
+            __syncwarp();
+        }
+        const unsigned T = prefix;  // the take-th smallest distance; `need` entries equal to T are taken
+        // collect in index order: every d < T, the first `need` with d == T
+        unsigned long long* bk = reinterpret_cast<unsigned long long*>(sm.bd);
+        int got = 0, eq = 0;
+        for (int b = 0; b < s; b += 32) {
+            const int x = b + lane;
+            const unsigned v = x < s ? dsc[x] : 0xffffffffu;
+            const bool isq = x < s && v == T;
+            const unsigned qb = __ballot_sync(PK_FULL, isq);
+            const bool sel = x < s && (v < T || (isq && eq + __popc(qb & ((1u << lane) - 1u)) < need));
+            const unsigned sb = __ballot_sync(PK_FULL, sel);
+            if (sel) {
+                const unsigned id = (unsigned)P.starts[x];
+                bk[got + __popc(sb & ((1u << lane) - 1u))] = ((unsigned long long)v << 32) | id;
+            }
+            got += __popc(sb);
+            eq += __popc(qb);
+        }
+        __syncwarp();
+        // pad to L (a power of two) and sort the packed keys
+        for (int x = take + lane; x < L; x += 32) bk[x] = ~0ull;
+        __syncwarp();
+        for (int k = 2; k <= L; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < L; i += 32) {
+                    const int x = i ^ j;
+                    if (x > i) {
+                        const unsigned long long a = bk[i], b = bk[x];
+                        if ((b < a) == ((i & k) == 0)) {
+                            bk[i] = b;
+                            bk[x] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        for (int x = lane; x < take; x += 32) sm.bi[x] = (unsigned)(bk[x] & 0xffffffffull);
+        bl = take;
+        cursor = 0;
+        // the seen table was scratch: empty it again
+        unsigned* h32 = reinterpret_cast<unsigned*>(sm.hash);
+        for (unsigned h = lane_id(); h <= sm.hmask / 2; h += 32) h32[h] = 0xffffffffu;
+        __syncwarp();
     }
 
     // First unvisited beam position at or after the cursor, -1 if none.

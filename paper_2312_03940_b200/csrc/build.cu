@@ -1344,6 +1344,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.P.screen = D.screen;
     A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
+    A.P.seed_select = env_int("PK_SEED_SELECT", 1);
     // counting mode (bench.py's untimed pass): exact distinct evaluations -> stats[4]
     unsigned* ubm = nullptr;
     if (stats && env_int("PK_COUNT_UNIQUE", 0) == 1) {

@@ -545,6 +545,7 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
     P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     P.lazy = env_int("PK_LAZY", 1) == 1 && n < (int64_t)PK_IDMASK;
     P.seed_only = env_int("PK_SEED_ONLY", 0);
+    P.seed_select = env_int("PK_SEED_SELECT", 1);
     int H = choose_hash((int)L, hash_bits, n);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);
