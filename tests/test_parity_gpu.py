@@ -530,3 +530,25 @@ def test_degenerate_float_data_matches_oracle(case):
     n = data.shape[0]
     k = min(8, n - 1)
     _pipeline_vs_oracle(data, R=16, L=max(24, k), k=k, nc=min(3, n))
+
+
+@pytest.mark.parametrize("mode", [None, "exact32"])
+def test_wide_beam_integer_modes_match_oracle(mode):
+    """Integer data with L = 128 (seeding by selection, packed beam keys) in the
+    u8 and the exact-fp32 policies: graph, kNN rows and labels == the oracle."""
+    rng = np.random.default_rng(21)
+    mu = rng.uniform(0, 255, (12, 64))
+    data = np.clip(np.round(mu[rng.integers(0, 12, 3_000)] + rng.normal(0, 25, (3_000, 64))), 0, 255)
+    data = data.astype(np.float32)
+    data[:20] = data[20:40]
+    p = points(data, mode)
+    assert p.mode == (_lib.MODE_EXACT32 if mode == "exact32" else _lib.MODE_EXACT_U8)
+    g = pk.build_vamana(p, R=24, L_build=128, alpha=1.2, seed=5, query_beam=128)
+    adj, deg, _ = oracle.build_vamana(data, R=24, L_build=128, alpha=1.2, seed=5)
+    assert np.array_equal(g.graph.degrees, deg)
+    assert np.array_equal(g.graph.adjacency, adj)
+    nb = g.knn_all(20)
+    ids, sqd = oracle.GraphIndexOracle(data, adj, deg, g.graph.start_points, 128).knn_batch(
+        np.arange(3_000, dtype=np.int64), 20)
+    assert np.array_equal(nb.ids, ids)
+    assert np.array_equal(nb.dists, sqd)
