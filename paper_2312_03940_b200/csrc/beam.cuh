@@ -502,6 +502,12 @@ struct WarpBeam {
     __device__ void seed(const SearchParams& P, const D& dist, bool hash_starts, bool unique) {
         const int lane = lane_id();
         if constexpr (has_screen<D>::value) lazy = P.screen && P.lazy && P.dp <= 128 * D::kQV;
+        if constexpr (has_screen<D>::value) {
+            if (lazy && unique && !hash_starts && P.s > 64 && P.seed_select && L >= 128 &&
+                2 * P.s <= (int)sm.hmask + 1) {
+                if (seed_select_lazy(P, dist)) return;
+            }
+        }
         if constexpr (int_keys<D>::value) {
             // needs: L a power of two >= 128 (the 1 KB histogram lives in bd), the
             // s u32 distances fit the seen table
@@ -531,6 +537,134 @@ struct WarpBeam {
         }
     }
 
+    // The take-th smallest of vals[0, s) (u32, in shared memory) by a radix
+    // select, 4 passes of 8 bits with a 256-bin histogram in `bins`; on return
+    // `need` = how many entries equal to the result belong to the take smallest.
+    __device__ unsigned radix_kth(const unsigned* vals, int s, int take, unsigned* bins, int& need) {
+        const int lane = lane_id();
+        unsigned prefix = 0u;
+        need = take;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int x = lane; x < 256; x += 32) bins[x] = 0u;
+            __syncwarp();
+            for (int x = lane; x < s; x += 32) {
+                const unsigned v = vals[x];
+                if (shift == 24 || (v >> (shift + 8)) == prefix) atomicAdd(bins + ((v >> shift) & 255u), 1u);
+            }
+            __syncwarp();
+            // lane l owns bins 8l .. 8l + 7
+            unsigned c[8], tot = 0u;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                c[i] = bins[8 * lane + i];
+                tot += c[i];
+            }
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned v = __shfl_up_sync(PK_FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const unsigned excl = incl - tot;
+            const bool here = excl < (unsigned)need && incl >= (unsigned)need;
+            const int src = __ffs(__ballot_sync(PK_FULL, here)) - 1;
+            int bin = 0;
+            unsigned before = 0u;
+            if (lane == src) {
+                unsigned acc = excl;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (acc + c[i] >= (unsigned)need) {
+                        bin = 8 * lane + i;
+                        break;
+                    }
+                    acc += c[i];
+                }
+                before = acc;
+            }
+            bin = __shfl_sync(PK_FULL, bin, src);
+            before = __shfl_sync(PK_FULL, before, src);
+            need -= (int)before;
+            prefix = (prefix << 8) | (unsigned)bin;
+            __syncwarp();
+        }
+        return prefix;
+    }
+
+    // Seeding by selection for lazy keys (float data, strictly increasing start
+    // list): every start's fp32 screen value a goes to the (still empty) seen
+    // table, the take-th smallest value T is found by a radix select, and only
+    // the starts with a (1 - eps) <= T (1 + eps) -- every other start is
+    // certainly above the take-th key -- are inserted (resolve + merge, 32 at a
+    // time).  Top-L is associative, so the beam equals the one after inserting
+    // all starts.  Returns false (nothing changed) if a screen value is unusable.
+    template <class D>
+    __device__ bool seed_select_lazy(const SearchParams& P, const D& dist) {
+        const int lane = lane_id();
+        const int s = P.s;
+        unsigned* asc = reinterpret_cast<unsigned*>(sm.hash);  // [s] fp32 screen values (bits)
+        unsigned* bins = reinterpret_cast<unsigned*>(sm.bd);   // [256] histogram (L >= 128)
+        bool bad = false;
+        for (int b = 0; b < s; b += 32) {
+            const int cnt = min(32, s - b);
+            const unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
+            float mine = 0.f;
+            for (int j = 0; j < cnt; j += 2) {
+                const int j1 = j + 1 < cnt ? j + 1 : j;
+                const float s0 = dist.screen(P.X, __shfl_sync(PK_FULL, id, j));
+                const float s1 = dist.screen(P.X, __shfl_sync(PK_FULL, id, j1));
+                if (lane == j) mine = s0;
+                if (lane == j1) mine = s1;
+            }
+            if (lane < cnt) {
+                bad |= !screen_usable(mine);
+                asc[b + lane] = __float_as_uint(mine);
+            }
+        }
+        const bool any_bad = __any_sync(PK_FULL, bad);
+        if (!any_bad) {
+            for (int b = 0; b < s; b += 32) count_unique(lane < min(32, s - b) ? (unsigned)P.starts[b + lane] : 0u,
+                                                         min(32, s - b));
+            if (lane == 0) evals += s;
+            __syncwarp();
+            const int take = min(L, s);
+            int need = 0;
+            const unsigned T = radix_kth(asc, s, take, bins, need);
+            const double thr = (double)__uint_as_float(T) * (1.0 + kEps32) / (1.0 - kEps32);
+            // candidates in index order, staged in cbuf (start-list positions):
+            // each chunk appends <= 32, full groups of 32 are inserted at once
+            int nc = 0;
+            auto insert = [&](int cnt) {
+                __syncwarp();
+                const unsigned xi = lane < cnt ? sm.cbuf[lane] : 0u;
+                unsigned cidf = lane < cnt ? ((unsigned)P.starts[xi] | PK_APX | PK_A32) : 0u;
+                double v = lane < cnt ? (double)__uint_as_float(asc[xi]) : 0.0;
+                bool valid = lane < cnt;
+                const unsigned rest = lane + cnt < nc ? sm.cbuf[lane + cnt] : 0u;
+                __syncwarp();
+                if (lane + cnt < nc) sm.cbuf[lane] = rest;
+                nc -= cnt;
+                __syncwarp();
+                resolve(P, dist, v, cidf, valid);
+                merge<false>(v, cidf, valid);
+            };
+            for (int b = 0; b < s; b += 32) {
+                const int x = b + lane;
+                const bool cand = x < s && (double)__uint_as_float(asc[x]) <= thr;
+                const unsigned cb = __ballot_sync(PK_FULL, cand);
+                if (cand) sm.cbuf[nc + __popc(cb & ((1u << lane) - 1u))] = (unsigned)x;
+                nc += __popc(cb);
+                if (nc >= 32) insert(32);
+            }
+            if (nc > 0) insert(nc);
+        }
+        // the seen table was scratch: empty it again
+        unsigned* h32 = reinterpret_cast<unsigned*>(sm.hash);
+        for (unsigned h = lane_id(); h <= sm.hmask / 2; h += 32) h32[h] = 0xffffffffu;
+        __syncwarp();
+        return !any_bad;
+    }
+
     // Seeding by selection (exact integer modes, strictly increasing start list):
     // the beam after merging every start is the sorted top-min(L, s) of their
     // keys (dist, id); id order = start-list order, so the keys are (dist,
@@ -555,57 +689,8 @@ struct WarpBeam {
         }
         __syncwarp();
         const int take = min(L, s);
-        // radix select: the take-th smallest distance T, and how many entries
-        // with distance == T are taken (the lowest indices)
-        unsigned prefix = 0u;
         int need = take;
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            for (int x = lane; x < 256; x += 32) bins[x] = 0u;
-            __syncwarp();
-            for (int x = lane; x < s; x += 32) {
-                const unsigned v = dsc[x];
-                if (shift == 24 || (v >> (shift + 8)) == prefix) atomicAdd(bins + ((v >> shift) & 255u), 1u);
-            }
-            __syncwarp();
-            // lane l owns bins 8l .. 8l + 7
-            unsigned c[8], tot = 0u;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                c[i] = bins[8 * lane + i];
-                tot += c[i];
-            }
-            unsigned incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned v = __shfl_up_sync(PK_FULL, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const unsigned excl = incl - tot;
-            // the bin where the cumulative count reaches `need`
-            const bool here = excl < (unsigned)need && incl >= (unsigned)need;
-            const unsigned hb = __ballot_sync(PK_FULL, here);
-            const int src = __ffs(hb) - 1;
-            int bin = 0;
-            unsigned before = 0u;
-            if (lane == src) {
-                unsigned acc = excl;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if (acc + c[i] >= (unsigned)need) {
-                        bin = 8 * lane + i;
-                        break;
-                    }
-                    acc += c[i];
-                }
-                before = acc;
-            }
-            bin = __shfl_sync(PK_FULL, bin, src);
-            before = __shfl_sync(PK_FULL, before, src);
-            need -= (int)before;
-            prefix = (prefix << 8) | (unsigned)bin;
-            __syncwarp();
-        }
-        const unsigned T = prefix;  // the take-th smallest distance; `need` entries equal to T are taken
+        const unsigned T = radix_kth(dsc, s, take, bins, need);  // `need` entries equal to T are taken
         // collect in index order: every d < T, the first `need` with d == T
         unsigned long long* bk = reinterpret_cast<unsigned long long*>(sm.bd);
         int got = 0, eq = 0;
