@@ -395,10 +395,17 @@ def main_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PK_BENCH_BACKEND=gloo PK_BENCH_DEVICE=0: functional check of the multi-rank
+    # path with every rank on one device (not a measurement)
+    local = int(os.environ.get("PK_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     comm = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         comm = Comm()
 
     name = args.config
