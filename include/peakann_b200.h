@@ -81,6 +81,14 @@ int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64
                 int64_t L, int64_t k, int64_t* out_ids, double* out_sqd, int64_t* out_counts,
                 int brute_fallback, int64_t* out_evals, int hash_bits, void* stream);
 
+/* pk_beam_knn starting each member query from its beam saved by
+ * pk_build_vamana_seeds (L must equal the build's L, same start list). */
+int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                       const int32_t* adj, int64_t R, const int32_t* deg, const int32_t* starts, int64_t s,
+                       const int64_t* qids, int64_t m, int64_t L, int64_t k, int64_t* out_ids, double* out_sqd,
+                       int64_t* out_counts, int brute_fallback, int64_t* out_evals, int hash_bits,
+                       const double* seed_bd, const uint32_t* seed_bi, const int32_t* seed_bl, void* stream);
+
 /* One search from an explicit start list for a member query (qid >= 0) or a
  * float64 query vector (qid < 0, qvec = dp doubles, zero padded).  Replaces
  * _kernels.beam_search_single (_kernels.py:215-227) as used by beam_search /
@@ -127,6 +135,16 @@ int pk_build_vamana(const float* x, int64_t n, int64_t dp, const uint32_t* x8, i
                     int64_t R, int64_t L, double alpha,
                     const int32_t* starts, int64_t s, const int32_t* order, int32_t* adj_out,
                     int32_t* deg_out, int64_t* stats, int hash_bits, void* stream);
+
+/* pk_build_vamana that also saves, per inserted point p, the beam its search
+ * starts from (after seeding with the start list): seed_bd / seed_bi are
+ * [n][L] (the beam's key slots and id words), seed_bl [n] the lengths.  A later
+ * pk_beam_knn_seeded of member queries with the same L and start list starts
+ * from these beams instead of seeding again (same inputs, same seeded beam). */
+int pk_build_vamana_seeds(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode, int64_t R,
+                          int64_t L, double alpha, const int32_t* starts, int64_t s, const int32_t* order,
+                          int32_t* adj_out, int32_t* deg_out, int64_t* stats, int hash_bits, double* seed_bd,
+                          uint32_t* seed_bi, int32_t* seed_bl, void* stream);
 
 /* Sharded build: one process per GPU, every rank holds the full point set
  * and ends with the full graph (identical on every rank and to

@@ -35,12 +35,15 @@ SIGNATURES = {
     "pk_check_exact32": [_P, _I, _I, _I, _P, _P],
     "pk_pack_u8": [_P, _I, _I, _I, _P, _I, _P],
     "pk_beam_knn": [_P, _I, _I, _P, _I, _i, _P, _I, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _i, _P, _i, _P],
+    "pk_beam_knn_seeded": [_P, _I, _I, _P, _I, _i, _P, _I, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _i, _P, _i,
+                           _P, _P, _P, _P],
     "pk_beam_search_single": [_P, _I, _I, _P, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P],
     "pk_brute_knn": [_P, _I, _I, _P, _I, _I, _P, _P, _P],
     "pk_brute_knn_vector": [_P, _I, _I, _P, _I, _P, _P, _P],
     "pk_brute_knn_tc": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P],
     "pk_dp_scan_tc": [_P, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P],
     "pk_build_vamana": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P],
+    "pk_build_vamana_seeds": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _P, _P, _P, _P],
     "pk_build_vamana_sharded": [_P, _I, _I, _P, _I, _i, _I, _I, _D, _P, _I, _P, _P, _P, _P, _i, _i, _i, _I,
                                 EXCHANGE_FN, _P, _P, _P, _P, _P, _P, _P],
     "pk_pcg64_permutation": [_P, _i, ctypes.c_uint32, _I, _P, _P],

@@ -75,6 +75,14 @@ struct SearchParams {
     int lazy = 1;              // float data: lazy keys (fp32 screen values until a decision needs the exact one)
     int seed_only = 0;         // profiling aid (PK_SEED_ONLY): stop after seeding
     int seed_select = 1;       // exact integer modes: seed by selection instead of merges (PK_SEED_SELECT)
+    // seeded beams per point id ([n][L] slots, [n] lengths): the build saves the
+    // beam each inserted point starts its search from; a later search of the same
+    // member query with the same L and start list starts from it instead of
+    // seeding again (same start list + same L = same seeded beam)
+    double* seed_bd = nullptr;
+    unsigned* seed_bi = nullptr;
+    int* seed_bl = nullptr;
+    int seed_save = 0, seed_load = 0;
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -732,6 +740,28 @@ struct WarpBeam {
         // the seen table was scratch: empty it again
         unsigned* h32 = reinterpret_cast<unsigned*>(sm.hash);
         for (unsigned h = lane_id(); h <= sm.hmask / 2; h += 32) h32[h] = 0xffffffffu;
+        __syncwarp();
+    }
+
+    // seeded-beam cache (SearchParams::seed_*): save after seed(), load instead of it
+    __device__ void save_seed(const SearchParams& P, unsigned q) {
+        const size_t o = (size_t)q * L;
+        for (int x = lane_id(); x < bl; x += 32) {
+            P.seed_bd[o + x] = sm.bd[x];
+            P.seed_bi[o + x] = sm.bi[x];
+        }
+        if (lane_id() == 0) P.seed_bl[q] = bl;
+    }
+    template <class D>
+    __device__ void load_seed(const SearchParams& P, const D&, unsigned q) {
+        if constexpr (has_screen<D>::value) lazy = P.screen && P.lazy && P.dp <= 128 * D::kQV;
+        const size_t o = (size_t)q * L;
+        bl = P.seed_bl[q];
+        for (int x = lane_id(); x < bl; x += 32) {
+            sm.bd[x] = P.seed_bd[o + x];
+            sm.bi[x] = P.seed_bi[o + x];
+        }
+        cursor = 0;
         __syncwarp();
     }
 

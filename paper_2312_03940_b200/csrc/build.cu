@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         wb.init(sm, A.L, A.vlog_i + (size_t)t * A.vcap, A.vlog_d + (size_t)t * A.vcap, A.vcap, A.err);
         wb.begin_counting(A.P.ubm ? A.P.ubm + ((size_t)blockIdx.x * wpb + wib) * A.P.uwords : nullptr, A.P.uwords);
         wb.seed(A.P, dist, false, uniq);
+        if (A.P.seed_save) wb.save_seed(A.P, p);
         wb.walk(A.P, dist);
         if constexpr (has_screen<decltype(dist)>::value)
             if (wb.lazy) wb.finalize_log(A.P, dist);
@@ -300,13 +301,17 @@ struct RevArgs {
     int rank, world;  // sharded build: this rank re-prunes the targets u % world == rank
 };
 
-// multi-GPU build context (pk_build_vamana_sharded)
+// build context: multi-GPU split (pk_build_vamana_sharded) and the optional
+// seeded-beam cache (pk_build_vamana_seeds; single-GPU builds only)
 struct Shard {
     int rank = 0, world = 1;
     long long min_shard = 0;
     pk_exchange_fn fn = nullptr;
     void* ctx = nullptr;
     int *xids = nullptr, *xlen = nullptr, *xsend = nullptr, *xrecv = nullptr, *xcnt = nullptr;
+    double* seed_bd = nullptr;
+    unsigned* seed_bi = nullptr;
+    int* seed_bl = nullptr;
 };
 
 // rows of the targets this rank re-pruned -> [u, deg, row[R]] records
@@ -1345,6 +1350,12 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
     A.P.seed_select = env_int("PK_SEED_SELECT", 1);
+    if (SH.seed_bd && SH.seed_bi && SH.seed_bl && SH.world == 1) {
+        A.P.seed_bd = SH.seed_bd;
+        A.P.seed_bi = SH.seed_bi;
+        A.P.seed_bl = SH.seed_bl;
+        A.P.seed_save = 1;
+    }
     // counting mode (bench.py's untimed pass): exact distinct evaluations -> stats[4]
     unsigned* ubm = nullptr;
     if (stats && env_int("PK_COUNT_UNIQUE", 0) == 1) {
@@ -1599,6 +1610,19 @@ extern "C" int pk_build_vamana(const float* x, int64_t n, int64_t dp, const uint
                                int hash_bits, void* stream) {
     return build_entry(x, n, dp, x8, dw, mode, R, L, alpha, starts, s, order, adj_out, deg_out, stats, hash_bits,
                        Shard{}, stream);
+}
+
+extern "C" int pk_build_vamana_seeds(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                                     int64_t R, int64_t L, double alpha, const int32_t* starts, int64_t s,
+                                     const int32_t* order, int32_t* adj_out, int32_t* deg_out, int64_t* stats,
+                                     int hash_bits, double* seed_bd, uint32_t* seed_bi, int32_t* seed_bl,
+                                     void* stream) {
+    Shard sh;
+    sh.seed_bd = seed_bd;
+    sh.seed_bi = reinterpret_cast<unsigned*>(seed_bi);
+    sh.seed_bl = reinterpret_cast<int*>(seed_bl);
+    return build_entry(x, n, dp, x8, dw, mode, R, L, alpha, starts, s, order, adj_out, deg_out, stats, hash_bits, sh,
+                       stream);
 }
 
 extern "C" int pk_build_vamana_sharded(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw,

@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, L, nullptr, nullptr, 0, nullptr);
         wb.begin_counting(P.ubm ? P.ubm + ((size_t)blockIdx.x * wpb + wib) * P.uwords : nullptr, P.uwords);
-        wb.seed(P, dist, false, uniq);
+        if (P.seed_load) wb.load_seed(P, dist, qi);
+        else wb.seed(P, dist, false, uniq);
         if (!P.seed_only) wb.walk(P, dist);
         un += wb.uniq;
         long long* oi = out_ids + t * kk;
@@ -517,11 +518,28 @@ extern "C" int pk_pack_u8(const float* x, int64_t n, int64_t dp, int64_t d, uint
     return 0;
 }
 
+extern "C" int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                                  const int32_t* adj, int64_t R, const int32_t* deg, const int32_t* starts, int64_t s,
+                                  const int64_t* qids, int64_t m, int64_t L, int64_t k, int64_t* out_ids,
+                                  double* out_sqd, int64_t* out_counts, int brute_fallback, int64_t* out_evals,
+                                  int hash_bits, const double* seed_bd, const uint32_t* seed_bi, const int32_t* seed_bl,
+                                  void* stream);
+
 extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
                            const int32_t* adj, int64_t R,
                            const int32_t* deg, const int32_t* starts, int64_t s, const int64_t* qids, int64_t m,
                            int64_t L, int64_t k, int64_t* out_ids, double* out_sqd, int64_t* out_counts,
                            int brute_fallback, int64_t* out_evals, int hash_bits, void* stream) {
+    return pk_beam_knn_seeded(x, n, dp, x8, dw, mode, adj, R, deg, starts, s, qids, m, L, k, out_ids, out_sqd,
+                              out_counts, brute_fallback, out_evals, hash_bits, nullptr, nullptr, nullptr, stream);
+}
+
+extern "C" int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
+                                  const int32_t* adj, int64_t R, const int32_t* deg, const int32_t* starts, int64_t s,
+                                  const int64_t* qids, int64_t m, int64_t L, int64_t k, int64_t* out_ids,
+                                  double* out_sqd, int64_t* out_counts, int brute_fallback, int64_t* out_evals,
+                                  int hash_bits, const double* seed_bd, const uint32_t* seed_bi, const int32_t* seed_bl,
+                                  void* stream) {
     cudaStream_t st = as_stream(stream);
     int64_t kk = k < n - 1 ? k : n - 1;
     if (kk <= 0 || m <= 0) {
@@ -546,6 +564,14 @@ extern "C" int pk_beam_knn(const float* x, int64_t n, int64_t dp, const uint32_t
     P.lazy = env_int("PK_LAZY", 1) == 1 && n < (int64_t)PK_IDMASK;
     P.seed_only = env_int("PK_SEED_ONLY", 0);
     P.seed_select = env_int("PK_SEED_SELECT", 1);
+    // the counting pass (bench.py) must evaluate the seeds: no cached beams there
+    if (seed_bd && seed_bi && seed_bl && !(out_evals && env_int("PK_COUNT_UNIQUE", 0) == 1) &&
+        env_int("PK_SEED_CACHE", 1) == 1) {
+        P.seed_bd = const_cast<double*>(seed_bd);
+        P.seed_bi = const_cast<unsigned*>(reinterpret_cast<const unsigned*>(seed_bi));
+        P.seed_bl = const_cast<int*>(seed_bl);
+        P.seed_load = 1;
+    }
     int H = choose_hash((int)L, hash_bits, n);
     const long long* q = reinterpret_cast<const long long*>(qids);
     long long* oi = reinterpret_cast<long long*>(out_ids);

@@ -253,8 +253,10 @@ MIN_SHARD_BATCH = 2048
 
 
 def build_graph_device(p: PointSet, R: int, L_build: int, alpha: float, starts: np.ndarray, order: np.ndarray,
-                       stats=None, order_t=None, starts_t=None, comm=None):
-    """Run pk_build_vamana (or pk_build_vamana_sharded over `comm`); returns (adj_t, deg_t)."""
+                       stats=None, order_t=None, starts_t=None, comm=None, seed_cache=False):
+    """Run pk_build_vamana (or pk_build_vamana_sharded over `comm`); returns
+    (adj_t, deg_t), plus the seeded-beam cache (seed slots, id words, lengths,
+    L) with seed_cache=True on a single GPU (pk_build_vamana_seeds)."""
     import torch
 
     dev = _lib.device()
@@ -265,6 +267,13 @@ def build_graph_device(p: PointSet, R: int, L_build: int, alpha: float, starts: 
     if stats is None:
         stats = STATS["build"]
     if comm is None or comm.world == 1:
+        if seed_cache:
+            sbd = torch.empty((p.n, L_build), dtype=torch.float64, device=dev)
+            sbi = torch.empty((p.n, L_build), dtype=torch.int32, device=dev)
+            sbl = torch.empty(p.n, dtype=torch.int32, device=dev)
+            _lib.call("pk_build_vamana_seeds", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, R, L_build,
+                      float(alpha), st, st.shape[0], od, adj, deg, stats, 0, sbd, sbi, sbl, _lib.stream())
+            return adj, deg, (sbd, sbi, sbl, int(L_build))
         _lib.call("pk_build_vamana", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, R, L_build, float(alpha), st,
                   st.shape[0], od, adj, deg, stats, 0, _lib.stream())
         return adj, deg
@@ -302,9 +311,24 @@ def build_vamana(
     if alpha < 1.0:
         raise ValueError(f"alpha must be >= 1, got {alpha}")
     starts, order = sample_starts(p.n, num_starts, seed, medoid_start, p)
-    adj, deg = build_graph_device(p, R, L_build, alpha, starts, order, comm=comm)
-    graph = GraphIndex.on_device(p, adj, deg, R, starts, float(alpha))
-    return VamanaIndex(graph, query_beam if query_beam is not None else L_build)
+    qb = query_beam if query_beam is not None else L_build
+    single = comm is None or comm.world == 1
+    # the seeded beams of the build are reused by member queries with L == L_build
+    res = build_graph_device(p, R, L_build, alpha, starts, order, comm=comm, seed_cache=single and qb == L_build)
+    graph = GraphIndex.on_device(p, res[0], res[1], R, starts, float(alpha))
+    if len(res) == 3:
+        graph._seed_cache = res[2]
+        graph._seed_src = graph.start_points
+    return VamanaIndex(graph, qb)
+
+
+def _seed_cache(g: "GraphIndex", L: int):
+    """The build's seeded beams when they apply to a search with beam width L
+    from the graph's current start list, else None."""
+    c = getattr(g, "_seed_cache", None)
+    if c is None or c[3] != L or getattr(g, "_seed_src", None) is not g.start_points:
+        return None
+    return c
 
 
 def beam_knn_raw(g: GraphIndex, qids_t, L: int, k: int, evals=None, hash_bits: int = 0):
@@ -321,8 +345,14 @@ def beam_knn_raw(g: GraphIndex, qids_t, L: int, k: int, evals=None, hash_bits: i
     sqd = torch.empty((m, kk), dtype=torch.float64, device=dev)
     counts = torch.zeros(m, dtype=torch.int64, device=dev)
     if kk > 0 and m > 0:
-        _lib.call("pk_beam_knn", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, adj, g.R, deg, st, st.shape[0], qids_t, m, L, k, ids,
-                  sqd, counts, 0, evals, hash_bits, _lib.stream())
+        c = _seed_cache(g, L)
+        if c is not None:
+            _lib.call("pk_beam_knn_seeded", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, adj, g.R, deg, st,
+                      st.shape[0], qids_t, m, L, k, ids, sqd, counts, 0, evals, hash_bits, c[0], c[1], c[2],
+                      _lib.stream())
+        else:
+            _lib.call("pk_beam_knn", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, adj, g.R, deg, st, st.shape[0],
+                      qids_t, m, L, k, ids, sqd, counts, 0, evals, hash_bits, _lib.stream())
     return ids, sqd, counts
 
 
@@ -342,8 +372,13 @@ def beam_knn_device(g: GraphIndex, qids_t, k: int, L: int, evals=None):
     sqd = torch.empty((m, kk), dtype=torch.float64, device=dev)
     counts = torch.empty(m, dtype=torch.int64, device=dev)
     if kk > 0 and m > 0:
-        _lib.call("pk_beam_knn", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, adj, g.R, deg, st, st.shape[0], qids_t, m, L, k, ids,
-                  sqd, counts, 1, evals, 0, _lib.stream())
+        c = _seed_cache(g, L)
+        if c is not None:
+            _lib.call("pk_beam_knn_seeded", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, adj, g.R, deg, st,
+                      st.shape[0], qids_t, m, L, k, ids, sqd, counts, 1, evals, 0, c[0], c[1], c[2], _lib.stream())
+        else:
+            _lib.call("pk_beam_knn", p.device(), p.n, p.dp, p.packed(), p.dw, p.mode, adj, g.R, deg, st, st.shape[0],
+                      qids_t, m, L, k, ids, sqd, counts, 1, evals, 0, _lib.stream())
     return ids, sqd
 
 

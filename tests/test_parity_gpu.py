@@ -552,3 +552,25 @@ def test_wide_beam_integer_modes_match_oracle(mode):
         np.arange(3_000, dtype=np.int64), 20)
     assert np.array_equal(nb.ids, ids)
     assert np.array_equal(nb.dists, sqd)
+
+
+@pytest.mark.parametrize("case", ["u8", "float"])
+def test_seeded_beam_cache_equals_fresh_seeding(monkeypatch, case):
+    """Member queries with L == L_build start from the beams the build saved
+    (pk_build_vamana_seeds / pk_beam_knn_seeded): same kNN rows, densities,
+    dependent points and labels as seeding afresh (PK_SEED_CACHE=0)."""
+    if case == "u8":
+        data, _ = workloads.generate("C2", n=20_000, components=20)
+    else:
+        data, _ = workloads.generate("C5", n=6_000, components=8)
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PK_SEED_CACHE", flag)
+        res = pk.run_pipeline(pk.PointSet(data), pk.VamanaConfig(R=32, L_build=128, L=128, alpha=1.1, seed=3), k=16,
+                              density_kind="kth", center_policy=pk.ProductCenter(10),
+                              noise_policy=pk.NoisePolicy(0.0), doubling_params=pk.DoublingParams(initial_k=32,
+                                                                                                 threshold=40))
+        st = res.state
+        out[flag] = [st.neighbors.ids, st.neighbors.dists, st.rho, st.lam, st.delta, res.clustering.labels]
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
