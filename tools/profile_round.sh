@@ -3,7 +3,7 @@
 # of the top kernels (each command already ran clean without ncu).
 set -x
 mkdir -p gpurun_out/prof
-timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/prof/bench.json 2> gpurun_out/prof/bench.err
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/prof/bench.json 2> gpurun_out/prof/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_c2.csv python tools/profile_step.py C2 > gpurun_out/prof/launch.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:beam_knn -s 2 -c 1 -o gpurun_out/prof/beam_c2 python tools/profile_step.py C2 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:build_search -s 33 -c 1 -o gpurun_out/prof/bsearch_c2 python tools/profile_step.py C2 > /dev/null 2>&1
