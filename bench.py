@@ -428,9 +428,11 @@ def main_ours(args):
     # start-up does not land in the timed steps; samples are filtered to the window
     clocks = ClockSampler(local)
     clocks.start()
-    # warm-up (untimed)
+    # warm-up (untimed), holding the previous result alive as the timed loop does
+    # (so the caching allocator already has room for two results' tensors)
+    last = None
     for _ in range(args.warmup):
-        run_pipeline_device(p, **kw, comm=comm)
+        last = run_pipeline_device(p, **kw, comm=comm)
     torch.cuda.synchronize()
     # a serving process freezes its start-up heap: every object created so far
     # (torch, numpy, the package) leaves the collector's generations, so a
