@@ -139,27 +139,53 @@ __global__ void norms64_kernel(const float* __restrict__ X, long long n, int dp,
 // buffer `st` (slot x at x * 128 bytes, 16-byte piece j at (j ^ (x & 7))):
 // A rows r0 .. r0 + na - 1 at slots 0 .., and, when the B block is separate
 // (b0 != r0), B rows b0 .. b0 + nb - 1 at slots 128 ..
-__device__ __forceinline__ void pt_stage_chunk(const float* __restrict__ X, int dp, const unsigned long long* rowp,
-                                               int r0, int na, int b0, int nb, int kc, unsigned char* st) {
-    const int col0 = kc * 32;
+// Per-thread staging plan of one Gram pass: thread tid always copies 16-byte
+// piece j = tid & 7 of slots x = (tid >> 3) + 16 i (i < 16): the source row
+// pointer (already offset by the piece) and the swizzled destination offset
+// are computed once per pass, so a K chunk costs one add + one cp.async per
+// piece.  Slot x holds A row r0 + x (x < na) and, when the B block is separate
+// (b0 != r0), B row b0 + x - 128 at x >= 128; with b0 == r0 slot x is row r0 + x.
+struct PTStagePlan {
+    const float* src[16];
+    unsigned dst[16];
+    unsigned live;  // bit i: slot (tid >> 3) + 16 i is copied
+    int j;
+};
+
+__device__ __forceinline__ void pt_stage_plan(const unsigned long long* rowp, int r0, int na, int b0, int nb,
+                                              PTStagePlan& pl) {
+    const int tid = threadIdx.x;
+    pl.j = tid & 7;
+    pl.live = 0u;
     const int tot = (b0 == r0) ? nb : 128 + nb;
-    for (int e = threadIdx.x; e < tot * 8; e += PT_THREADS) {
-        const int x = e >> 3, j = e & 7;
-        int r;
-        if (b0 == r0) r = r0 + x;
-        else if (x < 128) {
-            if (x >= na) continue;
-            r = r0 + x;
-        } else {
-            r = b0 + x - 128;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int x = (tid >> 3) + 16 * i;
+        int r = -1;
+        if (x < tot) {
+            if (b0 == r0) r = r0 + x;
+            else if (x < 128) r = x < na ? r0 + x : -1;
+            else r = b0 + x - 128;
         }
-        const int col = col0 + j * 4;
-        unsigned char* dst = st + x * 128 + ((j ^ (x & 7)) << 4);
-        if (col < dp) {
-            const float* src = reinterpret_cast<const float*>(rowp[r]) + col;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+        pl.src[i] = r >= 0 ? reinterpret_cast<const float*>(rowp[r]) + pl.j * 4 : nullptr;
+        pl.dst[i] = (unsigned)(x * 128 + ((pl.j ^ (x & 7)) << 4));
+        if (r >= 0) pl.live |= 1u << i;
+    }
+}
+
+// Copy K chunk kc (floats 32 kc .. 32 kc + 31) of the planned slots into stage
+// buffer `st` (row slot x at x * 128 bytes, 16-byte piece j at (j ^ (x & 7))).
+__device__ __forceinline__ void pt_stage_chunk(int dp, const PTStagePlan& pl, int kc, unsigned char* st) {
+    const bool in = kc * 32 + pl.j * 4 < dp;
+    const unsigned sbase = smem_u32(st);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        if (!((pl.live >> i) & 1u)) continue;
+        if (in) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + pl.dst[i]), "l"(pl.src[i] + kc * 32)
+                         : "memory");
         } else {
-            *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(st + pl.dst[i]) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -177,11 +203,12 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
     const int na = min(128, c - r0);
     const int ncol = (nb + 15) & ~15;
     const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(ncol >> 3) << 17) | ((128u >> 4) << 24);
-    const unsigned long long* rowp = P.rowp;
+    PTStagePlan pl;
+    pt_stage_plan(P.rowp, r0, na, b0, nb, pl);
     const unsigned boff = (b0 == r0) ? 0u : 128u * 128u;  // B operand offset inside a stage
     // prologue: chunks 0 .. PT_STAGES - 2
     for (int k = 0; k < PT_STAGES - 1; ++k) {
-        if (k < nk) pt_stage_chunk(X, dp, rowp, r0, na, b0, nb, k, P.stage + (size_t)k * PT_STAGE_BYTES);
+        if (k < nk) pt_stage_chunk(dp, pl, k, P.stage + (size_t)k * PT_STAGE_BYTES);
         else asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     for (int kc = 0; kc < nk; ++kc) {
@@ -192,7 +219,7 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
             mbar_wait(P.bar + sn, (pp.phase >> sn) & 1u);
             pp.phase ^= 1u << sn;
         }
-        if (kn < nk) pt_stage_chunk(X, dp, rowp, r0, na, b0, nb, kn, P.stage + (size_t)sn * PT_STAGE_BYTES);
+        if (kn < nk) pt_stage_chunk(dp, pl, kn, P.stage + (size_t)sn * PT_STAGE_BYTES);
         else asm volatile("cp.async.commit_group;\n" ::: "memory");
         asm volatile("cp.async.wait_group %0;\n" ::"n"(PT_STAGES - 1) : "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
