@@ -45,6 +45,8 @@ struct BuildArgs {
     int* vlen;         // [m]
     int* new_ids;      // [m * R]
     int* new_len;      // [m]
+    double* new_d;     // [m * R] distances of the out-lists' entries (NaN = unknown), or null
+    const double* adjd;  // [n * R] distances of the adjacency rows' entries (NaN = unknown), or null
     unsigned* err;
     long long* stats;  // [4]
     const int* items;  // optional: batch indices to process (overflow of the block prune), count *nitems
@@ -227,6 +229,8 @@ __global__ void __launch_bounds__(128) build_prune_kernel(BuildArgs A) {
         int* out = A.new_ids + (size_t)t * R;
         int sel = prune_candidates<MODE, QV>(A.D, C, c, A.alpha2, R, staged, out, &ev_prune);
         for (int x = sel + lane; x < R; x += 32) out[x] = -1;
+        if (A.new_d)
+            for (int x = lane; x < R; x += 32) A.new_d[(size_t)t * R + x] = __longlong_as_double(0x7ff8000000000000LL);
         if (lane == 0) A.new_len[t] = sel;
         __syncwarp();
     }
@@ -236,7 +240,8 @@ __global__ void __launch_bounds__(128) build_prune_kernel(BuildArgs A) {
 
 // write staged rows, count reverse edges, register targets (warp per point)
 __global__ void commit_kernel(const int* bids, int m, int R, const int* new_ids, const int* new_len, int* adj,
-                              int* deg, int* cnt, int* tslot, int* targets, int* ntargets) {
+                              int* deg, int* cnt, int* tslot, int* targets, int* ntargets, const double* new_d,
+                              double* adjd) {
     const int lane = lane_id();
     const int wpb = blockDim.x >> 5;
     for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < m; t += gridDim.x * wpb) {
@@ -245,6 +250,7 @@ __global__ void commit_kernel(const int* bids, int m, int R, const int* new_ids,
         for (int x = lane; x < R; x += 32) {
             int u = new_ids[(size_t)t * R + x];
             adj[(size_t)p * R + x] = u;
+            if (adjd) adjd[(size_t)p * R + x] = new_d[(size_t)t * R + x];
             if (x < len) {
                 if (atomicAdd(cnt + u, 1) == 0) {
                     int s = atomicAdd(ntargets, 1);
@@ -263,7 +269,8 @@ __global__ void sizes_kernel(const int* targets, const int* ntargets, const int*
 }
 
 __global__ void scatter_kernel(const int* bids, int m, int R, const int* new_ids, const int* new_len,
-                               const int* tslot, const int* offs, int* fill, int* adds) {
+                               const int* tslot, const int* offs, int* fill, int* adds, const double* new_d,
+                               double* addd) {
     for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < (long long)m * R;
          x += (long long)gridDim.x * blockDim.x) {
         int t = (int)(x / R), e = (int)(x % R);
@@ -272,6 +279,7 @@ __global__ void scatter_kernel(const int* bids, int m, int R, const int* new_ids
         int s = tslot[u];
         int pos = offs[s] + atomicAdd(fill + s, 1);
         adds[pos] = bids[t];
+        if (addd) addd[pos] = new_d[x];  // d(p, u) == d(u, p) bit for bit
     }
 }
 
@@ -299,6 +307,8 @@ struct RevArgs {
     int* biglist;   // groups with cap < candidates <= capB
     int* nbig;
     int rank, world;  // sharded build: this rank re-prunes the targets u % world == rank
+    double* adjd;        // [n * R] row-entry distances (NaN = unknown), or null
+    const double* addd;  // [E] distances of the batch's new sources to their targets, or null
 };
 
 // build context: multi-GPU split (pk_build_vamana_sharded) and the optional
@@ -1088,6 +1098,8 @@ __global__ void __launch_bounds__(kBigThreads) reverse_big_kernel(RevArgs A) {
         }
         __syncthreads();
         for (int x = sel + tid; x < A.R; x += kBigThreads) row[x] = -1;
+        if (A.adjd)
+            for (int x = tid; x < A.R; x += kBigThreads) A.adjd[(size_t)u * A.R + x] = __longlong_as_double(0x7ff8000000000000LL);
         if (tid == 0) {
             A.deg[u] = sel;
             A.cnt[u] = 0;
@@ -1305,6 +1317,16 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     PK_CHECK(scratch(&vlog_d, (size_t)mb * vcap, st));
     PK_CHECK(scratch(&vlen, (size_t)mb, st));
     const bool multi = SH.world > 1;
+    // float data on the tensor-core prune path, one GPU: adjacency rows carry the
+    // exact distances of their entries (NaN = unknown) so re-prunes need none
+    const bool dcache = tcb && tcr && !multi && env_int("PK_ROW_DIST", 1) == 1;
+    double *adjd = nullptr, *new_d = nullptr, *addd = nullptr;
+    if (dcache) {
+        PK_CHECK(scratch(&adjd, (size_t)n * R, st));
+        PK_CHECK(scratch(&new_d, (size_t)E, st));
+        PK_CHECK(scratch(&addd, (size_t)E, st));
+        PK_CHECK(cudaMemsetAsync(adjd, 0xff, sizeof(double) * (size_t)n * R, st));  // all NaN
+    }
     if (multi) {
         new_ids = SH.xids;
         new_len = SH.xlen;
@@ -1379,6 +1401,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.stats = stats;
     A.items = nullptr;
     A.nitems = nullptr;
+    A.new_d = new_d;
+    A.adjd = adjd;
 
     RevArgs B;
     B.X = D.X;
@@ -1405,6 +1429,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     B.nbig = nbig;
     B.rank = 0;
     B.world = 1;
+    B.adjd = adjd;
+    B.addd = addd;
 
     for (int lo = 0, batch = 1; lo < n; lo += batch, batch *= 2) {
         const int m = std::min(batch, n - lo);
@@ -1461,7 +1487,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         {
             ProfScope _ps("commit_kernel", st);
             commit_kernel<<<grid_for((long long)m * 32, 256), 256, 0, st>>>(order + lo, m, R, new_ids, new_len, adj, deg,
-                                                                             cnt, tslot, targets, ntargets);
+                                                                             cnt, tslot, targets, ntargets, new_d, adjd);
         }
         PK_CHECK_LAUNCH("commit_kernel");
         {
@@ -1476,7 +1502,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         {
             ProfScope _ps("scatter_kernel", st);
             scatter_kernel<<<grid_for((long long)m * R, 256), 256, 0, st>>>(order + lo, m, R, new_ids, new_len, tslot,
-                                                                             offs, fill, adds);
+                                                                             offs, fill, adds, new_d, addd);
         }
         PK_CHECK_LAUNCH("scatter_kernel");
         if (blockp) {
@@ -1552,7 +1578,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
-                    (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, cub_tmp})
+                    (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)adjd, (void*)new_d,
+                    (void*)addd, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

@@ -310,7 +310,7 @@ __device__ void pt_gram_rows(const float* __restrict__ X, int dp, const PTSmem& 
 // is left), false when the next alive candidate lies beyond this block.
 template <int QV>
 __device__ bool pt_greedy_block(const float* __restrict__ X, int dp, const PTSmem& P, int c, int r0, double alpha2,
-                                int R, int* out, unsigned& alive, int& sel, long long& nex) {
+                                int R, int* out, double* out_d, unsigned& alive, int& sel, long long& nex) {
     const int lane = lane_id();
     const int nw = (c + 31) >> 5;
     while (sel < R) {
@@ -321,7 +321,10 @@ __device__ bool pt_greedy_block(const float* __restrict__ X, int dp, const PTSme
         if (t >= r0 + 128) return false;
         if (lane == wl) alive &= ~(1u << (t & 31));
         const unsigned tid_t = P.S.ki2[t];
-        if (lane == 0) out[sel] = (int)tid_t;
+        if (lane == 0) {
+            out[sel] = (int)tid_t;
+            if (out_d) out_d[sel] = P.S.kd2[t];
+        }
         ++sel;
         if (sel >= R) return true;
         const int row = (t - r0) * P.words;
@@ -404,7 +407,7 @@ __device__ __forceinline__ int pt_unique(const BPSmem& S, int c, unsigned self) 
 // greedy needs them (R picks usually come from the first block).
 template <int QV>
 __device__ int pt_prune(const float* __restrict__ X, int dp, const double* __restrict__ nrm64, const PTSmem& P,
-                        PTPipe& pp, int c, double alpha2, int R, int* out, long long* exact_pairs) {
+                        PTPipe& pp, int c, double alpha2, int R, int* out, double* out_d, long long* exact_pairs) {
     for (int x = threadIdx.x; x < c; x += PT_THREADS) {
         const unsigned id = P.S.ki2[x];
         const double v = nrm64[id];
@@ -422,7 +425,7 @@ __device__ int pt_prune(const float* __restrict__ X, int dp, const double* __res
     for (int r0 = 0; r0 < c; r0 += 128) {
         pt_gram_rows<QV>(X, dp, P, pp, c, r0, alpha2);
         if ((threadIdx.x >> 5) == 0) {
-            const bool done = pt_greedy_block<QV>(X, dp, P, c, r0, alpha2, R, out, alive, sel, nex);
+            const bool done = pt_greedy_block<QV>(X, dp, P, c, r0, alpha2, R, out, out_d, alive, sel, nex);
             if (lane == 0) {
                 P.S.scal[8] = sel;
                 P.S.scal[9] = done;
@@ -497,7 +500,8 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
             } else {
                 const unsigned id = (unsigned)__ldg(row + x - vl);
                 P.S.ki[x] = id;
-                P.S.kd[x] = dq.eval_one(X, (int)id);
+                const double cd = A.adjd ? A.adjd[(size_t)p * R + x - vl] : 0.0;
+                P.S.kd[x] = (A.adjd && !isnan(cd)) ? cd : dq.eval_one(X, (int)id);
             }
         }
         const int Pw = next_pow2_dev(c0 < 2 ? 2 : c0);
@@ -514,15 +518,22 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
             continue;
         }
         int* out = A.new_ids + (size_t)t * R;
+        double* out_d = A.new_d ? A.new_d + (size_t)t * R : nullptr;
         // the build always prunes (_kernels.py:370), even c <= R candidates
         int sel = c;
         if (c <= 1) {
-            if (tid == 0 && c == 1) out[0] = (int)P.S.ki2[0];
+            if (tid == 0 && c == 1) {
+                out[0] = (int)P.S.ki2[0];
+                if (out_d) out_d[0] = P.S.kd2[0];
+            }
         } else {
-            sel = pt_prune<QV>(X, dp, nrm64, P, pp, c, A.alpha2, R, out, &exact_pairs);
+            sel = pt_prune<QV>(X, dp, nrm64, P, pp, c, A.alpha2, R, out, out_d, &exact_pairs);
             if (tid == 0) pairs += (long long)c * (c - 1) / 2;
         }
-        for (int x = sel + tid; x < R; x += PT_THREADS) out[x] = -1;
+        for (int x = sel + tid; x < R; x += PT_THREADS) {
+            out[x] = -1;
+            if (out_d) out_d[x] = __longlong_as_double(0x7ff8000000000000LL);
+        }
         if (tid == 0) A.new_len[t] = sel;
         __syncthreads();
     }
@@ -579,12 +590,20 @@ __global__ void __launch_bounds__(PT_THREADS, CAP == PT_CAP ? 2 : 1)
             }
             __syncthreads();
             sel = P.S.scal[9];
+            if (A.adjd)
+                for (int x = tid; x < A.R; x += PT_THREADS) A.adjd[(size_t)u * A.R + x] = __longlong_as_double(0x7ff8000000000000LL);
         } else {
             const Seq64Member du{X + (size_t)u * dp, dp};
             for (int x = tid; x < c0; x += PT_THREADS) {
                 const unsigned id = x < nd ? (unsigned)row[x] : (unsigned)A.adds[off + x - nd];
                 P.S.ki[x] = id;
-                P.S.kd[x] = du.eval_one(X, (int)id);
+                double cd = 0.0;
+                bool known = false;
+                if (A.adjd) {  // row entries and new sources carry their exact distances (NaN = unknown)
+                    cd = x < nd ? A.adjd[(size_t)u * A.R + x] : A.addd[off + x - nd];
+                    known = !isnan(cd);
+                }
+                P.S.kd[x] = known ? cd : du.eval_one(X, (int)id);
             }
             const int Pw = next_pow2_dev(c0 < 2 ? 2 : c0);
             for (int x = c0 + tid; x < Pw; x += PT_THREADS) {
@@ -595,14 +614,20 @@ __global__ void __launch_bounds__(PT_THREADS, CAP == PT_CAP ? 2 : 1)
             bp_sort(P.S.kd, P.S.ki, Pw);
             const int c = pt_unique<CAP>(P.S, c0, u);
             if (tid == 0) ev += c0;
+            double* rowd = A.adjd ? A.adjd + (size_t)u * A.R : nullptr;
             if (c <= A.R) {
-                for (int x = tid; x < c; x += PT_THREADS) row[x] = (int)P.S.ki2[x];
+                for (int x = tid; x < c; x += PT_THREADS) {
+                    row[x] = (int)P.S.ki2[x];
+                    if (rowd) rowd[x] = P.S.kd2[x];
+                }
                 sel = c;
             } else {
                 long long ex = 0;
-                sel = pt_prune<QV>(X, dp, nrm64, P, pp, c, A.alpha2, A.R, row, &ex);
+                sel = pt_prune<QV>(X, dp, nrm64, P, pp, c, A.alpha2, A.R, row, rowd, &ex);
                 if (tid == 0) ev += ex;
             }
+            if (rowd)
+                for (int x = sel + tid; x < A.R; x += PT_THREADS) rowd[x] = __longlong_as_double(0x7ff8000000000000LL);
         }
         for (int x = sel + tid; x < A.R; x += PT_THREADS) row[x] = -1;
         if (tid == 0) {
