@@ -83,6 +83,14 @@ struct SearchParams {
     unsigned* seed_bi = nullptr;
     int* seed_bl = nullptr;
     int seed_save = 0, seed_load = 0;
+    // tensor-core screens of every point against every start (tc_seed_dump):
+    // [n][seed_ld] fp32 with |value - d| <= seed_eps |x| |start|_max + rounding
+    const float* seed_tc = nullptr;
+    long long seed_ld = 0;
+    const float* seed_qn = nullptr;     // [n] |x|^2
+    const float* seed_smax2 = nullptr;  // max |start|^2 (device scalar)
+    float seed_eps = 0.f;               // relative fp16/fp32 term
+    float seed_abs = 0.f;               // fp16 subnormal term, per unit of |x| + |start|_max
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -612,21 +620,51 @@ struct WarpBeam {
         const int s = P.s;
         unsigned* asc = reinterpret_cast<unsigned*>(sm.hash);  // [s] fp32 screen values (bits)
         unsigned* bins = reinterpret_cast<unsigned*>(sm.bd);   // [256] histogram (L >= 128)
+        // tensor-core pre-screen: only starts whose low bound is not above the
+        // take-th high bound can be among the take nearest; the rest get no fp32 screen
+        const float* drow = nullptr;
+        float ebase = 0.f, T_hi = 0.f;
+        if (P.seed_tc) {
+            const unsigned q = (unsigned)((dist.q - P.X) / P.dp);
+            drow = P.seed_tc + (size_t)q * P.seed_ld;
+            const float qn = P.seed_qn[q], sm2 = *P.seed_smax2;
+            ebase = P.seed_eps * sqrtf(qn) * sqrtf(sm2) + P.seed_abs * (sqrtf(qn) + sqrtf(sm2)) +
+                    1e-6f * (qn + sm2);
+            for (int x = lane; x < s; x += 32) {
+                const float v = drow[x];
+                const float hi = v + ebase + 1e-5f * fabsf(v);
+                // non-finite (fp16 overflow): no bound, the start stays a candidate
+                asc[x] = isfinite(hi) ? __float_as_uint(fmaxf(hi, 0.f)) : 0x7f800000u;
+            }
+            __syncwarp();
+            int need_hi = 0;
+            T_hi = __uint_as_float(radix_kth(asc, s, min(L, s), bins, need_hi));
+        }
         bool bad = false;
         for (int b = 0; b < s; b += 32) {
             const int cnt = min(32, s - b);
             const unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
-            float mine = 0.f;
-            for (int j = 0; j < cnt; j += 2) {
-                const int j1 = j + 1 < cnt ? j + 1 : j;
+            bool want = lane < cnt;
+            if (drow && want) {
+                const float v = drow[b + lane];
+                want = !(v - ebase - 1e-5f * fabsf(v) > T_hi) || !isfinite(v);
+            }
+            unsigned wm = __ballot_sync(PK_FULL, want);
+            float mine = __uint_as_float(0x7f800000u);
+            while (wm) {
+                const int j = __ffs(wm) - 1;
+                wm &= wm - 1u;
+                const int j1 = wm ? __ffs(wm) - 1 : j;
+                if (wm) wm &= wm - 1u;
                 const float s0 = dist.screen(P.X, __shfl_sync(PK_FULL, id, j));
                 const float s1 = dist.screen(P.X, __shfl_sync(PK_FULL, id, j1));
                 if (lane == j) mine = s0;
                 if (lane == j1) mine = s1;
             }
+            __syncwarp();
             if (lane < cnt) {
-                bad |= !screen_usable(mine);
-                asc[b + lane] = __float_as_uint(mine);
+                if (want) bad |= !screen_usable(mine);
+                asc[b + lane] = want ? __float_as_uint(mine) : 0x7f800000u;
             }
         }
         const bool any_bad = __any_sync(PK_FULL, bad);

@@ -60,6 +60,8 @@ struct TcArgs {
     float* out_d;          // (m, nsplit, K') screened distances
     const int* prank;      // (n,) density rank: only points with prank > qrank[row] are kept
     const int* qrank;      // (m,) (both null: plain kNN)
+    float* dump = nullptr;  // non-null: write every screened distance, dump[row * dump_ld + col] (no heaps)
+    long long dump_ld = 0;
 };
 
 // ---- screening kernel ------------------------------------------------------------------
@@ -240,6 +242,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
                     v[j] = __float_as_uint(dd);
                     mask |= (dd < thr ? 1u : 0u) << j;
                 }
+                if (A.dump) {  // dump mode: every column of the row, self included
+                    if (live) {
+                        float* o = A.dump + (size_t)q * A.dump_ld + cbase;
+#pragma unroll
+                        for (int j = 0; j < TC_CH; ++j)
+                            if (cbase + j < A.n) o[j] = __uint_as_float(v[j]);
+                    }
+                    continue;
+                }
                 if (A.prank) {  // nearest-denser search: only strictly denser points compete
                     const int* rk = rk_s + acc * TC_BN + ch * TC_CH;
 #pragma unroll
@@ -286,7 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
-        if (live) {
+        if (live && !A.dump) {
             const size_t base = ((size_t)q * A.nsplit + split) * TC_KP + (size_t)half * TC_KPH;
             for (int k = 0; k < TC_KPH; ++k) {
                 A.out_id[base + k] = hi[k * TC_BM + tid];
@@ -562,6 +573,78 @@ static int tc_knn_core(const float* x, int64_t n, int64_t dp, const int64_t* qid
     (void)iota;
     return 0;
 }
+
+__global__ void widen_ids_kernel(const int* in, int m, long long* out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < m) out[t] = in[t];
+}
+
+// Screened squared distances of every point to every start on the tensor cores
+// (fp16 operands, fp32 accumulation): dump[i * ld + j] ~ d(x_i, start_j) with
+// |dump - d| <= eps_scale |x_i| |start|_max (plus fp32 rounding of the norms);
+// qn[i] = |x_i|^2 (fp32), *smax2 = max_j |start_j|^2.  Used to narrow the
+// starts a build search screens in fp32 (beam.cuh seed_select_lazy).
+namespace pk {
+int tc_seed_dump(const float* x, int n, int dp, const int* starts, int s, float* dump, long long ld, float* qn,
+                 float* smax2, float* eps_scale, cudaStream_t st) {
+    if (!tc_supported()) {
+        set_error("tensor-core screens need an sm_100 device");
+        return 2;
+    }
+    const int kp = (dp + TC_BK - 1) / TC_BK * TC_BK;
+    __half *qh = nullptr, *ph = nullptr;
+    float* pn = nullptr;
+    long long* sid = nullptr;
+    PK_CHECK(scratch(&qh, (size_t)n * kp, st));
+    PK_CHECK(scratch(&ph, (size_t)s * kp, st));
+    PK_CHECK(scratch(&pn, (size_t)s, st));
+    PK_CHECK(scratch(&sid, (size_t)s, st));
+    widen_ids_kernel<<<(s + 255) / 256, 256, 0, st>>>(starts, s, sid);
+    {
+        ProfScope _ps("tc_prep_kernel", st);
+        tc_prep_kernel<<<(unsigned)n, 256, 0, st>>>(x, dp, nullptr, n, kp, qh, qn);
+        tc_prep_kernel<<<(unsigned)s, 256, 0, st>>>(x, dp, sid, s, kp, ph, pn);
+    }
+    PK_CHECK(cudaMemsetAsync(smax2, 0, sizeof(float), st));
+    {
+        ProfScope _ps("tc_max_kernel", st);
+        tc_max_kernel<<<grid_for(s, 256), 256, 0, st>>>(pn, s, smax2);
+    }
+    PK_CHECK_LAUNCH("tc_seed_prep");
+    CUtensorMap mq, mp;
+    int rc = make_map(&mq, qh, n, kp, TC_BM);
+    if (rc) return rc;
+    rc = make_map(&mp, ph, s, kp, TC_BN / 2);
+    if (rc) return rc;
+    const int qblocks = (n + 2 * TC_BM - 1) / (2 * TC_BM) * 2;
+    const int ntiles = (s + TC_BN - 1) / TC_BN;
+    TcArgs A;
+    A.qn = qn;
+    A.pn = pn;
+    A.qids = nullptr;
+    A.m = n;
+    A.n = s;
+    A.kblocks = kp / TC_BK;
+    A.tiles_per_split = ntiles;
+    A.nsplit = 1;
+    A.dbg = 0;
+    A.prank = nullptr;
+    A.qrank = nullptr;
+    A.out_id = nullptr;
+    A.out_d = nullptr;
+    A.dump = dump;
+    A.dump_ld = ld;
+    PK_CHECK(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
+    {
+        ProfScope _ps("tc_seed_screen_kernel", st);
+        tc_screen_kernel<<<dim3((unsigned)qblocks, 1u), TC_THREADS, TC_SMEM, st>>>(mq, mp, A);
+    }
+    PK_CHECK_LAUNCH("tc_seed_screen_kernel");
+    *eps_scale = 2.f * (2.f * ldexpf(1.f, -11) + (float)kp * ldexpf(1.f, -24));
+    for (void* p : {(void*)qh, (void*)ph, (void*)pn, (void*)sid}) release(p, st);
+    return 0;
+}
+}  // namespace pk
 
 extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
                                int64_t* out_ids, double* out_sqd, uint8_t* row_flags, uint64_t* uncertified,
