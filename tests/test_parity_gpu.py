@@ -339,6 +339,45 @@ def test_tensor_core_prune_equals_warp_prune(monkeypatch, case):
     assert np.array_equal(out["0"][0], out["1"][0])
 
 
+@pytest.mark.parametrize("case", ["c5", "dup128", "huge", "tiny"])
+def test_tensor_core_seeding_equals_fp32_seeding(monkeypatch, case):
+    """Float builds with >= 256 starts: the tcgen05 screens of every point
+    against the start set (fp16 operands, certified bound) only decide which
+    starts get an fp32 screen; the graph and the kNN rows equal the ones of the
+    plain fp32-screened seeding (PK_SEED_TC=0), also where the fp16 bound does
+    not hold (coordinates past the fp16 range, subnormal fp16 coordinates)."""
+    rng = np.random.default_rng(11)
+    if case == "c5":
+        data, _ = workloads.generate("C5", n=6_000, components=8)
+    else:
+        hubs = rng.normal(size=(12, 96))
+        lab = rng.integers(0, 12, 5_000)
+        data = hubs[lab] + 0.15 * rng.normal(size=(5_000, 96))
+        data[:40] = hubs[lab[:40]]  # duplicates: tied start distances
+        data[40:70] = data[300:330]
+        if case == "huge":
+            data[::7] *= 2.0e5  # fp16 overflow on every 7th row (queries and starts)
+        elif case == "tiny":
+            data *= 1.0e-6  # fp16 subnormals
+        data = data.astype(np.float32)
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PK_SEED_TC", flag)
+        p = pk.PointSet(data)
+        assert p.mode == _lib.MODE_SEQ64
+        _lib.prof_collect(reset=True)
+        _lib.prof_only([])
+        _lib.prof_enable(True)
+        g = pk.build_vamana(p, R=32, L_build=96, alpha=1.2, num_starts=400, seed=4, query_beam=96)
+        _lib.prof_enable(False)
+        ran = "tc_seed_screen_kernel" in _lib.prof_collect(reset=True)
+        assert ran == (flag == "1")
+        nb = g.knn_all(16)
+        out[flag] = (g.graph.adjacency.copy(), g.graph.degrees.copy(), nb.ids.copy(), nb.dists.copy())
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("kind", ["u8", "float"])
 def test_build_with_short_candidate_lists_matches_oracle(kind):
     """L_build < R: many items have at most R candidates, and the build still
