@@ -83,14 +83,10 @@ struct SearchParams {
     unsigned* seed_bi = nullptr;
     int* seed_bl = nullptr;
     int seed_save = 0, seed_load = 0;
-    // tensor-core screens of every point against every start (tc_seed_dump):
-    // [n][seed_ld] fp32 with |value - d| <= seed_eps |x| |start|_max + rounding
-    const float* seed_tc = nullptr;
-    long long seed_ld = 0;
-    const float* seed_qn = nullptr;     // [n] |x|^2
-    const float* seed_smax2 = nullptr;  // max |start|^2 (device scalar)
-    float seed_eps = 0.f;               // relative fp16/fp32 term
-    float seed_abs = 0.f;               // fp16 subnormal term, per unit of |x| + |start|_max
+    // tensor-core pre-screen of the start set (tc_seed_mask): [n][seed_mw] bits,
+    // set = the start may be among the point's take nearest
+    const unsigned* seed_mask = nullptr;
+    int seed_mw = 0;
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -553,58 +549,8 @@ struct WarpBeam {
         }
     }
 
-    // The take-th smallest of vals[0, s) (u32, in shared memory) by a radix
-    // select, 4 passes of 8 bits with a 256-bin histogram in `bins`; on return
-    // `need` = how many entries equal to the result belong to the take smallest.
     __device__ unsigned radix_kth(const unsigned* vals, int s, int take, unsigned* bins, int& need) {
-        const int lane = lane_id();
-        unsigned prefix = 0u;
-        need = take;
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            for (int x = lane; x < 256; x += 32) bins[x] = 0u;
-            __syncwarp();
-            for (int x = lane; x < s; x += 32) {
-                const unsigned v = vals[x];
-                if (shift == 24 || (v >> (shift + 8)) == prefix) atomicAdd(bins + ((v >> shift) & 255u), 1u);
-            }
-            __syncwarp();
-            // lane l owns bins 8l .. 8l + 7
-            unsigned c[8], tot = 0u;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                c[i] = bins[8 * lane + i];
-                tot += c[i];
-            }
-            unsigned incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned v = __shfl_up_sync(PK_FULL, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const unsigned excl = incl - tot;
-            const bool here = excl < (unsigned)need && incl >= (unsigned)need;
-            const int src = __ffs(__ballot_sync(PK_FULL, here)) - 1;
-            int bin = 0;
-            unsigned before = 0u;
-            if (lane == src) {
-                unsigned acc = excl;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if (acc + c[i] >= (unsigned)need) {
-                        bin = 8 * lane + i;
-                        break;
-                    }
-                    acc += c[i];
-                }
-                before = acc;
-            }
-            bin = __shfl_sync(PK_FULL, bin, src);
-            before = __shfl_sync(PK_FULL, before, src);
-            need -= (int)before;
-            prefix = (prefix << 8) | (unsigned)bin;
-            __syncwarp();
-        }
-        return prefix;
+        return warp_radix_kth(vals, s, take, bins, need);
     }
 
     // Seeding by selection for lazy keys (float data, strictly increasing start
@@ -620,35 +566,16 @@ struct WarpBeam {
         const int s = P.s;
         unsigned* asc = reinterpret_cast<unsigned*>(sm.hash);  // [s] fp32 screen values (bits)
         unsigned* bins = reinterpret_cast<unsigned*>(sm.bd);   // [256] histogram (L >= 128)
-        // tensor-core pre-screen: only starts whose low bound is not above the
-        // take-th high bound can be among the take nearest; the rest get no fp32 screen
-        const float* drow = nullptr;
-        float ebase = 0.f, T_hi = 0.f;
-        if (P.seed_tc) {
-            const unsigned q = (unsigned)((dist.q - P.X) / P.dp);
-            drow = P.seed_tc + (size_t)q * P.seed_ld;
-            const float qn = P.seed_qn[q], sm2 = *P.seed_smax2;
-            ebase = P.seed_eps * sqrtf(qn) * sqrtf(sm2) + P.seed_abs * (sqrtf(qn) + sqrtf(sm2)) +
-                    1e-6f * (qn + sm2);
-            for (int x = lane; x < s; x += 32) {
-                const float v = drow[x];
-                const float hi = v + ebase + 1e-5f * fabsf(v);
-                // non-finite (fp16 overflow): no bound, the start stays a candidate
-                asc[x] = isfinite(hi) ? __float_as_uint(fmaxf(hi, 0.f)) : 0x7f800000u;
-            }
-            __syncwarp();
-            int need_hi = 0;
-            T_hi = __uint_as_float(radix_kth(asc, s, min(L, s), bins, need_hi));
-        }
+        // tensor-core pre-screen (tc_seed_mask): only the starts whose low bound is
+        // not above the take-th high bound get an fp32 screen
+        const unsigned* mrow = nullptr;
+        if (P.seed_mask) mrow = P.seed_mask + (size_t)((dist.q - P.X) / P.dp) * P.seed_mw;
         bool bad = false;
         for (int b = 0; b < s; b += 32) {
             const int cnt = min(32, s - b);
             const unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
             bool want = lane < cnt;
-            if (drow && want) {
-                const float v = drow[b + lane];
-                want = !(v - ebase - 1e-5f * fabsf(v) > T_hi) || !isfinite(v);
-            }
+            if (mrow) want = want && ((mrow[b >> 5] >> lane) & 1u);
             unsigned wm = __ballot_sync(PK_FULL, want);
             float mine = __uint_as_float(0x7f800000u);
             while (wm) {

@@ -1229,8 +1229,8 @@ int config_kernel(K kern, size_t warp_bytes, int want_wpb, int* wpb_out, int* gr
 
 // tc_knn.cu: tensor-core screens of all points against the start set
 bool tc_supported();
-int tc_seed_dump(const float* x, int n, int dp, const int* starts, int s, float* dump, long long ld, float* qn,
-                 float* smax2, float* eps_scale, cudaStream_t st);
+int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int take, unsigned* mask, int mw,
+                 cudaStream_t st);
 
 template <int MODE, int QV>
 int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
@@ -1390,26 +1390,17 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         PK_CHECK(scratch(&ubm, (size_t)grid_s * wpb_s * A.P.uwords, st));
         A.P.ubm = ubm;
     }
-    // float data, one GPU: screens of every point against every start on the
-    // tensor cores up front; a search then fp32-screens only the starts whose
-    // low bound can reach its L-th high bound (beam.cuh seed_select_lazy)
-    float *seed_dump = nullptr, *seed_qn = nullptr, *seed_sm2 = nullptr;
-    const long long seed_ld = (s + 3) / 4 * 4;
-    if (MODE == MODE_SEQ64 && D.screen && A.P.lazy && A.P.seed_select && !ubm && !multi &&
-        s >= env_int("PK_SEED_TC_MIN", 256) && env_int("PK_SEED_TC", 1) == 1 && s > L &&
-        (long long)n * seed_ld <= (4ll << 30) && tc_supported()) {
-        PK_CHECK(scratch(&seed_dump, (size_t)n * seed_ld, st));
-        PK_CHECK(scratch(&seed_qn, (size_t)n, st));
-        PK_CHECK(scratch(&seed_sm2, 1, st));
-        float eps = 0.f;
-        if ((rc = tc_seed_dump(D.X, n, D.dp, starts, s, seed_dump, seed_ld, seed_qn, seed_sm2, &eps, st))) return rc;
-        A.P.seed_tc = seed_dump;
-        A.P.seed_ld = seed_ld;
-        A.P.seed_qn = seed_qn;
-        A.P.seed_smax2 = seed_sm2;
-        A.P.seed_eps = eps;
-        const int kp = (D.dp + 63) / 64 * 64;
-        A.P.seed_abs = 2.f * sqrtf((float)kp) * ldexpf(1.f, -24);
+    // float data, one GPU: the start set pre-screened on the tensor cores; a
+    // search fp32-screens only the starts whose bound can reach its take-th
+    // (tc_knn.cu tc_seed_mask, beam.cuh seed_select_lazy)
+    unsigned* seed_mask = nullptr;
+    if (MODE == MODE_SEQ64 && D.screen && A.P.lazy && A.P.seed_select && !ubm && !multi && L >= 128 && s > L && n >= 4096 &&
+        s >= env_int("PK_SEED_TC_MIN", 256) && s <= 8192 && env_int("PK_SEED_TC", 1) == 1 && tc_supported()) {
+        const int mw = (s + 31) / 32;
+        PK_CHECK(scratch(&seed_mask, (size_t)n * mw, st));
+        if ((rc = tc_seed_mask(D.X, n, D.dp, starts, s, std::min(L, s), seed_mask, mw, st))) return rc;
+        A.P.seed_mask = seed_mask;
+        A.P.seed_mw = mw;
     }
     A.D = D;
     A.L = L;
@@ -1605,7 +1596,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
                     (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)adjd, (void*)new_d,
-                    (void*)addd, (void*)seed_dump, (void*)seed_qn, (void*)seed_sm2, cub_tmp})
+                    (void*)addd, (void*)seed_mask, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

@@ -535,4 +535,58 @@ __device__ __forceinline__ int warp_excl_prefix(unsigned ballot) {
     return __popc(ballot & ((1u << lane_id()) - 1u));
 }
 
+// The take-th smallest of vals[0, s) (u32, in shared memory) by a radix
+// select, 4 passes of 8 bits with a 256-bin histogram in `bins`; on return
+// `need` = how many entries equal to the result belong to the take smallest.
+__device__ __forceinline__ unsigned warp_radix_kth(const unsigned* vals, int s, int take, unsigned* bins, int& need) {
+    const int lane = lane_id();
+    unsigned prefix = 0u;
+    need = take;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int x = lane; x < 256; x += 32) bins[x] = 0u;
+        __syncwarp();
+        for (int x = lane; x < s; x += 32) {
+            const unsigned v = vals[x];
+            if (shift == 24 || (v >> (shift + 8)) == prefix) atomicAdd(bins + ((v >> shift) & 255u), 1u);
+        }
+        __syncwarp();
+        // lane l owns bins 8l .. 8l + 7
+        unsigned c[8], tot = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            c[i] = bins[8 * lane + i];
+            tot += c[i];
+        }
+        unsigned incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(PK_FULL, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const unsigned excl = incl - tot;
+        const bool here = excl < (unsigned)need && incl >= (unsigned)need;
+        const int src = __ffs(__ballot_sync(PK_FULL, here)) - 1;
+        int bin = 0;
+        unsigned before = 0u;
+        if (lane == src) {
+            unsigned acc = excl;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (acc + c[i] >= (unsigned)need) {
+                    bin = 8 * lane + i;
+                    break;
+                }
+                acc += c[i];
+            }
+            before = acc;
+        }
+        bin = __shfl_sync(PK_FULL, bin, src);
+        before = __shfl_sync(PK_FULL, before, src);
+        need -= (int)before;
+        prefix = (prefix << 8) | (unsigned)bin;
+        __syncwarp();
+    }
+    return prefix;
+}
+
 }  // namespace pk

@@ -579,30 +579,79 @@ __global__ void widen_ids_kernel(const int* in, int m, long long* out) {
     if (t < m) out[t] = in[t];
 }
 
-// Screened squared distances of every point to every start on the tensor cores
-// (fp16 operands, fp32 accumulation): dump[i * ld + j] ~ d(x_i, start_j) with
-// |dump - d| <= eps_scale |x_i| |start|_max (plus fp32 rounding of the norms);
-// qn[i] = |x_i|^2 (fp32), *smax2 = max_j |start_j|^2.  Used to narrow the
-// starts a build search screens in fp32 (beam.cuh seed_select_lazy).
 namespace pk {
-int tc_seed_dump(const float* x, int n, int dp, const int* starts, int s, float* dump, long long ld, float* qn,
-                 float* smax2, float* eps_scale, cudaStream_t st) {
+// One warp per row of a screened chunk: hi = v + e, lo = v - e bound the exact
+// squared distance (e: the fp16-operand / fp32-accumulation bound of the
+// screen, the fp16 subnormal term, fp32 rounding of the norms, and a 1e-5
+// relative margin); T = the take-th smallest hi; bit j of the row's mask is set
+// unless lo_j > T (such a start is certainly outside the take nearest).  A
+// non-finite screen (fp16 overflow) keeps its start a candidate with hi = +inf.
+__global__ void seed_mask_kernel(const float* __restrict__ dump, long long ld, int rows, int s, int take,
+                                 const float* __restrict__ qn, const float* __restrict__ smax2, float eps, float eabs,
+                                 unsigned* __restrict__ mask, int mw) {
+    extern __shared__ unsigned seed_sh[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int spad = (s + 31) & ~31;
+    unsigned* hi = seed_sh + (size_t)w * (spad + 256);
+    unsigned* bins = hi + spad;
+    const float sm2 = *smax2;
+    for (int r = blockIdx.x * wpb + w; r < rows; r += gridDim.x * wpb) {
+        const float* drow = dump + (size_t)r * ld;
+        const float q2 = qn[r];
+        const float e = eps * sqrtf(q2) * sqrtf(sm2) + eabs * (sqrtf(q2) + sqrtf(sm2)) + 1e-6f * (q2 + sm2);
+        for (int x = lane; x < s; x += 32) {
+            const float v = drow[x];
+            const float h = v + e + 1e-5f * fabsf(v);
+            hi[x] = isfinite(h) ? __float_as_uint(fmaxf(h, 0.f)) : 0x7f800000u;
+        }
+        __syncwarp();
+        int need = 0;
+        const float T = __uint_as_float(warp_radix_kth(hi, s, take, bins, need));
+        for (int b = 0; b < s; b += 32) {
+            bool keep = false;
+            if (b + lane < s) {
+                const float v = drow[b + lane];
+                keep = !(v - e - 1e-5f * fabsf(v) > T) || !isfinite(v);
+            }
+            const unsigned m = __ballot_sync(PK_FULL, keep);
+            if (lane == 0) mask[(size_t)r * mw + (b >> 5)] = m;
+        }
+        __syncwarp();
+    }
+}
+
+// Tensor-core pre-screen of a build's start set: mask[i * mw + j / 32] bit j
+// set iff start j may be among the take nearest starts of point i (exact float64
+// squared distances).  The points are screened against the starts in chunks of
+// rows on the tcgen05 kernel (fp16 operands, fp32 TMEM accumulation, every
+// distance dumped), each chunk reduced to its bits by seed_mask_kernel.  Used by
+// beam.cuh seed_select_lazy to skip the fp32 screens of far starts.
+int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int take, unsigned* mask, int mw,
+                 cudaStream_t st) {
     if (!tc_supported()) {
         set_error("tensor-core screens need an sm_100 device");
         return 2;
     }
     const int kp = (dp + TC_BK - 1) / TC_BK * TC_BK;
+    const long long ld = (s + 3) / 4 * 4;
+    // equal chunks of <= 256 MB of screens (none much smaller than the others)
+    const long long cmax = env_int("PK_SEED_CHUNK", 0) >= 2 * TC_BM ? env_int("PK_SEED_CHUNK", 0)
+                                                                      : std::max<long long>(2 * TC_BM, (256ll << 20) / (ld * 4));
+    const long long nchunk = (n + cmax - 1) / cmax;
+    const int chunk = (int)((n + nchunk - 1) / nchunk);
     __half *qh = nullptr, *ph = nullptr;
-    float* pn = nullptr;
+    float *pn = nullptr, *qn = nullptr, *smax2 = nullptr, *dump = nullptr;
     long long* sid = nullptr;
-    PK_CHECK(scratch(&qh, (size_t)n * kp, st));
+    PK_CHECK(scratch(&qh, (size_t)chunk * kp, st));
     PK_CHECK(scratch(&ph, (size_t)s * kp, st));
     PK_CHECK(scratch(&pn, (size_t)s, st));
+    PK_CHECK(scratch(&qn, (size_t)chunk, st));
+    PK_CHECK(scratch(&smax2, 1, st));
     PK_CHECK(scratch(&sid, (size_t)s, st));
+    PK_CHECK(scratch(&dump, (size_t)chunk * ld, st));
     widen_ids_kernel<<<(s + 255) / 256, 256, 0, st>>>(starts, s, sid);
     {
         ProfScope _ps("tc_prep_kernel", st);
-        tc_prep_kernel<<<(unsigned)n, 256, 0, st>>>(x, dp, nullptr, n, kp, qh, qn);
         tc_prep_kernel<<<(unsigned)s, 256, 0, st>>>(x, dp, sid, s, kp, ph, pn);
     }
     PK_CHECK(cudaMemsetAsync(smax2, 0, sizeof(float), st));
@@ -612,36 +661,57 @@ int tc_seed_dump(const float* x, int n, int dp, const int* starts, int s, float*
     }
     PK_CHECK_LAUNCH("tc_seed_prep");
     CUtensorMap mq, mp;
-    int rc = make_map(&mq, qh, n, kp, TC_BM);
+    int rc = make_map(&mp, ph, s, kp, TC_BN / 2);
     if (rc) return rc;
-    rc = make_map(&mp, ph, s, kp, TC_BN / 2);
-    if (rc) return rc;
-    const int qblocks = (n + 2 * TC_BM - 1) / (2 * TC_BM) * 2;
-    const int ntiles = (s + TC_BN - 1) / TC_BN;
-    TcArgs A;
-    A.qn = qn;
-    A.pn = pn;
-    A.qids = nullptr;
-    A.m = n;
-    A.n = s;
-    A.kblocks = kp / TC_BK;
-    A.tiles_per_split = ntiles;
-    A.nsplit = 1;
-    A.dbg = 0;
-    A.prank = nullptr;
-    A.qrank = nullptr;
-    A.out_id = nullptr;
-    A.out_d = nullptr;
-    A.dump = dump;
-    A.dump_ld = ld;
     PK_CHECK(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
-    {
-        ProfScope _ps("tc_seed_screen_kernel", st);
-        tc_screen_kernel<<<dim3((unsigned)qblocks, 1u), TC_THREADS, TC_SMEM, st>>>(mq, mp, A);
+    // |screen - d| <= eps |x| |start|_max for normal fp16 operands (both roundings,
+    // kp fp32 accumulations, factor 2 of the cross term); subnormal fp16 operands
+    // add <= 2^-24 sqrt(kp) (|x| + |start|_max), taken twice
+    const float eps = 2.f * (2.f * ldexpf(1.f, -11) + (float)kp * ldexpf(1.f, -24));
+    const float eabs = 2.f * sqrtf((float)kp) * ldexpf(1.f, -24);
+    constexpr int kMaskWarps = 8;
+    const size_t msmem = (size_t)kMaskWarps * (((s + 31) & ~31) + 256) * sizeof(unsigned);
+    PK_CHECK(cudaFuncSetAttribute(seed_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+    int per_sm = 0;
+    PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seed_mask_kernel, kMaskWarps * 32, msmem));
+    for (int r0 = 0; r0 < n; r0 += chunk) {
+        const int rows = std::min(chunk, n - r0);
+        {
+            ProfScope _ps("tc_prep_kernel", st);
+            tc_prep_kernel<<<(unsigned)rows, 256, 0, st>>>(x + (size_t)r0 * dp, dp, nullptr, rows, kp, qh, qn);
+        }
+        if ((rc = make_map(&mq, qh, rows, kp, TC_BM))) return rc;
+        TcArgs A;
+        A.qn = qn;
+        A.pn = pn;
+        A.qids = nullptr;
+        A.m = rows;
+        A.n = s;
+        A.kblocks = kp / TC_BK;
+        A.tiles_per_split = (s + TC_BN - 1) / TC_BN;
+        A.nsplit = 1;
+        A.dbg = 0;
+        A.prank = nullptr;
+        A.qrank = nullptr;
+        A.out_id = nullptr;
+        A.out_d = nullptr;
+        A.dump = dump;
+        A.dump_ld = ld;
+        {
+            ProfScope _ps("tc_seed_screen_kernel", st);
+            const int qblocks = (rows + 2 * TC_BM - 1) / (2 * TC_BM) * 2;
+            tc_screen_kernel<<<dim3((unsigned)qblocks, 1u), TC_THREADS, TC_SMEM, st>>>(mq, mp, A);
+        }
+        PK_CHECK_LAUNCH("tc_seed_screen_kernel");
+        {
+            ProfScope _ps("seed_mask_kernel", st);
+            const int grid = std::min(sm_count() * std::max(1, per_sm), (rows + kMaskWarps - 1) / kMaskWarps);
+            seed_mask_kernel<<<grid, kMaskWarps * 32, msmem, st>>>(dump, ld, rows, s, take, qn, smax2, eps, eabs,
+                                                                   mask + (size_t)r0 * mw, mw);
+        }
+        PK_CHECK_LAUNCH("seed_mask_kernel");
     }
-    PK_CHECK_LAUNCH("tc_seed_screen_kernel");
-    *eps_scale = 2.f * (2.f * ldexpf(1.f, -11) + (float)kp * ldexpf(1.f, -24));
-    for (void* p : {(void*)qh, (void*)ph, (void*)pn, (void*)sid}) release(p, st);
+    for (void* p : {(void*)qh, (void*)ph, (void*)pn, (void*)qn, (void*)smax2, (void*)sid, (void*)dump}) release(p, st);
     return 0;
 }
 }  // namespace pk

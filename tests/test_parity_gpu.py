@@ -361,6 +361,8 @@ def test_tensor_core_seeding_equals_fp32_seeding(monkeypatch, case):
             data *= 1.0e-6  # fp16 subnormals
         data = data.astype(np.float32)
     out = {}
+    # several screening chunks of 1,300 rows on the C5 sample
+    monkeypatch.setenv("PK_SEED_CHUNK", "1300" if case == "c5" else "0")
     for flag in ("0", "1"):
         monkeypatch.setenv("PK_SEED_TC", flag)
         p = pk.PointSet(data)
@@ -368,7 +370,7 @@ def test_tensor_core_seeding_equals_fp32_seeding(monkeypatch, case):
         _lib.prof_collect(reset=True)
         _lib.prof_only([])
         _lib.prof_enable(True)
-        g = pk.build_vamana(p, R=32, L_build=96, alpha=1.2, num_starts=400, seed=4, query_beam=96)
+        g = pk.build_vamana(p, R=32, L_build=128, alpha=1.2, num_starts=400, seed=4, query_beam=128)
         _lib.prof_enable(False)
         ran = "tc_seed_screen_kernel" in _lib.prof_collect(reset=True)
         assert ran == (flag == "1")
