@@ -272,6 +272,10 @@ int pk_resolve_short(const float* x, int64_t n, int64_t dp, const uint32_t* x8, 
 int pk_resolve_short_scanned(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
                              const int64_t* qids, int64_t m, int64_t kk, const int64_t* dp_id, const double* dp_sqd,
                              int64_t* lam, double* delta, int64_t* unresolved, int64_t* n_unresolved, void* stream);
+/* Counters of the tensor-core count decision used by pk_resolve_short_scanned on
+ * float data: out2[0] = rows screened, out2[1] = rows the bounds left open (sent
+ * to the exact count scan); reset != 0 zeroes them.  Diagnostics only. */
+int pk_tc_count_stats(int64_t* out2, int reset);
 
 /* Scatter: lam[qids[i]] = src_id[i], delta[qids[i]] = sqrt(src_sqd[i])
  * (dependent.py:125-127). */

@@ -60,6 +60,7 @@ SIGNATURES = {
     "pk_count_below": [_P, _I, _I, _P, _I, _i, _P, _I, _P, _P, _P, _P],
     "pk_resolve_short": [_P, _I, _I, _P, _I, _i, _P, _P, _I, _I, _P, _P, _P, _P, _P],
     "pk_resolve_short_scanned": [_P, _I, _I, _P, _I, _i, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P],
+    "pk_tc_count_stats": [_P, _i],
     "pk_scatter_dependents": [_P, _I, _P, _P, _P, _P, _P],
     "pk_argmax_rank": [_P, _I, _P, _P],
     "pk_flag_noise": [_P, _I, _D, _P, _P, _P],

@@ -601,6 +601,30 @@ extern "C" int pk_count_below(const float* x, int64_t n, int64_t dp, const uint3
     return dispatch_scan<SCAN_COUNT>(mode, A, st, &nc);
 }
 
+namespace pk {
+int tc_count_decide(const float* x, int n, int dp, const long long* qids, int m, const double* key_d,
+                    const long long* key_i, long long kk, long long* cnt,
+                    int (*exact_count)(const long long*, int, const double*, const long long*, long long*, void*),
+                    void* ctx, cudaStream_t st);
+bool tc_supported();
+}  // namespace pk
+
+namespace {
+struct CountCtx {
+    const float* x;
+    int64_t n, dp;
+    const uint32_t* x8;
+    int64_t dw;
+    int mode;
+    void* stream;
+};
+int exact_count_cb(const long long* q, int m, const double* kd, const long long* ki, long long* out, void* ctx) {
+    const CountCtx& C = *static_cast<const CountCtx*>(ctx);
+    return pk_count_below(C.x, C.n, C.dp, C.x8, C.dw, C.mode, reinterpret_cast<const int64_t*>(q), m, kd,
+                          reinterpret_cast<const int64_t*>(ki), reinterpret_cast<int64_t*>(out), C.stream);
+}
+}  // namespace
+
 extern "C" int pk_resolve_short_scanned(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw,
                                         int mode, const int64_t* qids, int64_t m, int64_t kk, const int64_t* dp_id,
                                         const double* dp_sqd, int64_t* lam, double* delta, int64_t* unresolved,
@@ -614,7 +638,17 @@ extern "C" int pk_resolve_short_scanned(const float* x, int64_t n, int64_t dp, c
     unsigned char* fl = nullptr;
     PK_CHECK(scratch(&cnt, (size_t)m, st));
     PK_CHECK(scratch(&fl, (size_t)m, st));
-    int rc = pk_count_below(x, n, dp, x8, dw, mode, qids, m, dp_sqd, dp_id, reinterpret_cast<int64_t*>(cnt), stream);
+    int rc;
+    // float data: the decision count < kk from tensor-core bounds, exact counts
+    // only for the rows they leave open
+    if (mode == MODE_SEQ64 && x && m >= env_int("PK_TC_COUNT_MIN", 64) && n >= 4096 && env_int("PK_TC_COUNT", 1) == 1 &&
+        tc_supported()) {
+        CountCtx C{x, n, dp, x8, dw, mode, stream};
+        rc = tc_count_decide(x, (int)n, (int)dp, reinterpret_cast<const long long*>(qids), (int)m, dp_sqd,
+                             reinterpret_cast<const long long*>(dp_id), kk, cnt, exact_count_cb, &C, st);
+    } else {
+        rc = pk_count_below(x, n, dp, x8, dw, mode, qids, m, dp_sqd, dp_id, reinterpret_cast<int64_t*>(cnt), stream);
+    }
     if (rc) return rc;
     {
         ProfScope _ps("short_resolve_kernel", st);

@@ -62,6 +62,15 @@ struct TcArgs {
     const int* qrank;      // (m,) (both null: plain kNN)
     float* dump = nullptr;  // non-null: write every screened distance, dump[row * dump_ld + col] (no heaps)
     long long dump_ld = 0;
+    // count mode (cnt_key non-null, no heaps): per row, the points j != self, j !=
+    // cnt_kid[row] certainly below cnt_key[row] (hi < key) -> cnt_lo, possibly
+    // below (lo <= key or non-finite screen) -> cnt_hi; bounds as in tc_seed_mask
+    const double* cnt_key = nullptr;
+    const long long* cnt_kid = nullptr;
+    unsigned* cnt_lo = nullptr;
+    unsigned* cnt_hi = nullptr;
+    const float* pmax2 = nullptr;  // max ||p||^2 (device scalar)
+    float cnt_eps = 0.f, cnt_abs = 0.f;
 };
 
 // ---- screening kernel ------------------------------------------------------------------
@@ -198,6 +207,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
         float thr = __int_as_float(0x7f800000);
         int acc = 0;
         unsigned aphase = 0;
+        // count mode state
+        double ckey = 0.0;
+        long long ckid = -1;
+        float cerr = 0.f;
+        unsigned c_lo = 0u, c_hi = 0u;
+        if (A.cnt_key && live) {
+            ckey = A.cnt_key[q];
+            ckid = A.cnt_kid[q];
+            const float p2 = *A.pmax2;
+            cerr = A.cnt_eps * sqrtf(qn) * sqrtf(p2) + A.cnt_abs * (sqrtf(qn) + sqrtf(p2)) + 1e-6f * (qn + p2);
+        }
         constexpr int kChunks = TC_BN / TC_CH / 2;  // chunks per column half
         for (int t = t0; t < t1; ++t) {
             // this tile's point norms, staged once for the 256 epilogue threads
@@ -241,6 +261,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
                     const float dd = qn + pv[j] - 2.f * __uint_as_float(v[j]);
                     v[j] = __float_as_uint(dd);
                     mask |= (dd < thr ? 1u : 0u) << j;
+                }
+                if (A.cnt_key) {  // count mode
+                    if (live) {
+#pragma unroll
+                        for (int j = 0; j < TC_CH; ++j) {
+                            const long long col = cbase + j;
+                            if (col < A.n && col != self && col != ckid) {
+                                const float dd = __uint_as_float(v[j]);
+                                const float mg = cerr + 1e-5f * fabsf(dd);
+                                const bool fin = isfinite(dd + mg);
+                                c_lo += (fin && (double)(dd + mg) < ckey) ? 1u : 0u;
+                                c_hi += (!fin || !((double)(dd - mg) > ckey)) ? 1u : 0u;
+                            }
+                        }
+                    }
+                    continue;
                 }
                 if (A.dump) {  // dump mode: every column of the row, self included
                     if (live) {
@@ -297,7 +333,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
-        if (live && !A.dump) {
+        if (A.cnt_key && live) {
+            atomicAdd(A.cnt_lo + q, c_lo);
+            atomicAdd(A.cnt_hi + q, c_hi);
+        }
+        if (live && !A.dump && !A.cnt_key) {
             const size_t base = ((size_t)q * A.nsplit + split) * TC_KP + (size_t)half * TC_KPH;
             for (int k = 0; k < TC_KPH; ++k) {
                 A.out_id[base + k] = hi[k * TC_BM + tid];
@@ -714,6 +754,152 @@ int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int ta
     for (void* p : {(void*)qh, (void*)ph, (void*)pn, (void*)qn, (void*)smax2, (void*)sid, (void*)dump}) release(p, st);
     return 0;
 }
+
+long long tc_count_stats[2] = {0, 0};  // rows screened / rows sent to the exact count
+
+// Per row: the decision count < kk from the tensor-core bounds where they settle
+// it (cnt = the bound), else the row is flagged for the exact count.
+__global__ void count_decide_kernel(const unsigned* lo, const unsigned* hi, int m, long long kk, long long* cnt,
+                                    unsigned char* flag) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const bool below = (long long)hi[t] < kk, above = (long long)lo[t] >= kk;
+    cnt[t] = below ? (long long)hi[t] : (long long)lo[t];
+    flag[t] = !(below || above);
+}
+
+__global__ void iota64_kernel(long long* out, int m) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < m) out[t] = t;
+}
+
+__global__ void gather_rows_kernel(const long long* rows, const long long* nrows, const long long* qids,
+                                   const double* key_d, const long long* key_i, long long* sq, double* sd,
+                                   long long* si) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= *nrows) return;
+    const long long r = rows[t];
+    sq[t] = qids[r];
+    sd[t] = key_d[r];
+    si[t] = key_i[r];
+}
+
+__global__ void scatter_counts_kernel(const long long* rows, const long long* nrows, const long long* sc,
+                                      long long* cnt) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < *nrows) cnt[rows[t]] = sc[t];
+}
+
+int compact_flagged(const long long* in, const unsigned char* flags, long long n, long long* out, long long* count,
+                    cudaStream_t st);
+
+// count[r] such that (count[r] < kk) == (#{j != qids[r] : (d(q, j), j) < (key_d[r],
+// key_i[r])} < kk), the count itself exact whenever the tensor-core bounds leave
+// the decision open: member rows screened against all points on tcgen05 (fp16
+// operands, fp32 accumulators, counting epilogue), undecided rows counted by
+// `exact_count(rows, m', keys...)` (the scan kernels).  Used by the doubling
+// rounds' short-row resolution (scan.cu pk_resolve_short_scanned) on float data.
+int tc_count_decide(const float* x, int n, int dp, const long long* qids, int m, const double* key_d,
+                    const long long* key_i, long long kk, long long* cnt,
+                    int (*exact_count)(const long long*, int, const double*, const long long*, long long*, void*),
+                    void* ctx, cudaStream_t st) {
+    if (!tc_supported()) {
+        set_error("tensor-core screens need an sm_100 device");
+        return 2;
+    }
+    const int kp = (dp + TC_BK - 1) / TC_BK * TC_BK;
+    __half *qh = nullptr, *ph = nullptr;
+    float *qn = nullptr, *pn = nullptr, *pmax2 = nullptr;
+    unsigned *lo = nullptr, *hi = nullptr;
+    PK_CHECK(scratch(&qh, (size_t)m * kp, st));
+    PK_CHECK(scratch(&ph, (size_t)n * kp, st));
+    PK_CHECK(scratch(&qn, (size_t)m, st));
+    PK_CHECK(scratch(&pn, (size_t)n, st));
+    PK_CHECK(scratch(&pmax2, 1, st));
+    PK_CHECK(scratch(&lo, (size_t)m, st));
+    PK_CHECK(scratch(&hi, (size_t)m, st));
+    {
+        ProfScope _ps("tc_prep_kernel", st);
+        tc_prep_kernel<<<(unsigned)m, 256, 0, st>>>(x, dp, qids, m, kp, qh, qn);
+        tc_prep_kernel<<<(unsigned)n, 256, 0, st>>>(x, dp, nullptr, n, kp, ph, pn);
+    }
+    PK_CHECK(cudaMemsetAsync(pmax2, 0, sizeof(float), st));
+    PK_CHECK(cudaMemsetAsync(lo, 0, sizeof(unsigned) * (size_t)m, st));
+    PK_CHECK(cudaMemsetAsync(hi, 0, sizeof(unsigned) * (size_t)m, st));
+    {
+        ProfScope _ps("tc_max_kernel", st);
+        tc_max_kernel<<<grid_for(n, 256), 256, 0, st>>>(pn, n, pmax2);
+    }
+    PK_CHECK_LAUNCH("tc_count_prep");
+    CUtensorMap mq, mp;
+    int rc = make_map(&mq, qh, m, kp, TC_BM);
+    if (rc) return rc;
+    if ((rc = make_map(&mp, ph, n, kp, TC_BN / 2))) return rc;
+    const int qblocks = (m + 2 * TC_BM - 1) / (2 * TC_BM) * 2;
+    const int ntiles = (n + TC_BN - 1) / TC_BN;
+    int nsplit = std::max(1, std::min(ntiles, (2 * sm_count() + qblocks - 1) / qblocks));
+    const int per = (ntiles + nsplit - 1) / nsplit;
+    nsplit = (ntiles + per - 1) / per;
+    TcArgs A;
+    A.qn = qn;
+    A.pn = pn;
+    A.qids = qids;
+    A.m = m;
+    A.n = n;
+    A.kblocks = kp / TC_BK;
+    A.tiles_per_split = per;
+    A.nsplit = nsplit;
+    A.dbg = 0;
+    A.prank = nullptr;
+    A.qrank = nullptr;
+    A.out_id = nullptr;
+    A.out_d = nullptr;
+    A.cnt_key = key_d;
+    A.cnt_kid = key_i;
+    A.cnt_lo = lo;
+    A.cnt_hi = hi;
+    A.pmax2 = pmax2;
+    A.cnt_eps = 2.f * (2.f * ldexpf(1.f, -11) + (float)kp * ldexpf(1.f, -24));
+    A.cnt_abs = 2.f * sqrtf((float)kp) * ldexpf(1.f, -24);
+    PK_CHECK(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
+    {
+        ProfScope _ps("tc_count_screen_kernel", st);
+        tc_screen_kernel<<<dim3((unsigned)qblocks, (unsigned)nsplit), TC_THREADS, TC_SMEM, st>>>(mq, mp, A);
+    }
+    PK_CHECK_LAUNCH("tc_count_screen_kernel");
+    for (void* p : {(void*)qh, (void*)ph, (void*)qn, (void*)pn, (void*)pmax2}) release(p, st);
+    unsigned char* flag = nullptr;
+    long long *rows = nullptr, *nrows = nullptr, *iota = nullptr;
+    PK_CHECK(scratch(&flag, (size_t)m, st));
+    PK_CHECK(scratch(&rows, (size_t)m, st));
+    PK_CHECK(scratch(&nrows, 1, st));
+    PK_CHECK(scratch(&iota, (size_t)m, st));
+    count_decide_kernel<<<(m + 255) / 256, 256, 0, st>>>(lo, hi, m, kk, cnt, flag);
+    iota64_kernel<<<(m + 255) / 256, 256, 0, st>>>(iota, m);
+    PK_CHECK_LAUNCH("count_decide_kernel");
+    if ((rc = compact_flagged(iota, flag, m, rows, nrows, st))) return rc;
+    long long nb = 0;
+    PK_CHECK(cudaMemcpyAsync(&nb, nrows, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    PK_CHECK(cudaStreamSynchronize(st));
+    if (nb > 0) {
+        long long *sq = nullptr, *si = nullptr, *sc = nullptr;
+        double* sd = nullptr;
+        PK_CHECK(scratch(&sq, (size_t)nb, st));
+        PK_CHECK(scratch(&si, (size_t)nb, st));
+        PK_CHECK(scratch(&sd, (size_t)nb, st));
+        PK_CHECK(scratch(&sc, (size_t)nb, st));
+        gather_rows_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(rows, nrows, qids, key_d, key_i, sq, sd, si);
+        PK_CHECK_LAUNCH("gather_rows_kernel");
+        if ((rc = exact_count(sq, (int)nb, sd, si, sc, ctx))) return rc;
+        scatter_counts_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(rows, nrows, sc, cnt);
+        PK_CHECK_LAUNCH("scatter_counts_kernel");
+        for (void* p : {(void*)sq, (void*)si, (void*)sd, (void*)sc}) release(p, st);
+    }
+    tc_count_stats[0] += m;
+    tc_count_stats[1] += nb;
+    for (void* p : {(void*)lo, (void*)hi, (void*)flag, (void*)rows, (void*)nrows, (void*)iota}) release(p, st);
+    return 0;
+}
 }  // namespace pk
 
 extern "C" int pk_brute_knn_tc(const float* x, int64_t n, int64_t dp, const int64_t* qids, int64_t m, int64_t k,
@@ -753,4 +939,11 @@ extern "C" int pk_dp_scan_tc(const float* x, int64_t n, int64_t dp, const int64_
     release(prank, st);
     release(qrank, st);
     return rc;
+}
+
+extern "C" int pk_tc_count_stats(int64_t* out2, int reset) {
+    out2[0] = tc_count_stats[0];
+    out2[1] = tc_count_stats[1];
+    if (reset) tc_count_stats[0] = tc_count_stats[1] = 0;
+    return 0;
 }

@@ -380,6 +380,43 @@ def test_tensor_core_seeding_equals_fp32_seeding(monkeypatch, case):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("case", ["c5", "dup128", "huge"])
+def test_tensor_core_count_decision_equals_exact_count(monkeypatch, case):
+    """Float data, doubling rounds: the short rows' "fewer than kk points closer
+    than the nearest denser point" decision taken from tcgen05 bounds (exact count
+    scan only for the rows the bounds leave open) gives the same lambda, delta and
+    labels as the exact count scan (PK_TC_COUNT=0)."""
+    import ctypes
+
+    rng = np.random.default_rng(21)
+    if case == "c5":
+        data, _ = workloads.generate("C5", n=8_000, components=12)
+    else:
+        hubs = rng.normal(size=(12, 96))
+        lab = rng.integers(0, 12, 6_000)
+        data = hubs[lab] + 0.2 * rng.normal(size=(6_000, 96))
+        data[:50] = hubs[lab[:50]]  # duplicates: ties at the key distance
+        data[50:90] = data[400:440]
+        if case == "huge":
+            data[::9] *= 3.0e5  # fp16 overflow: those rows stay undecided
+        data = data.astype(np.float32)
+    monkeypatch.setenv("PK_TC_COUNT_MIN", "1")
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PK_TC_COUNT", flag)
+        st = (ctypes.c_int64 * 2)()
+        _lib.lib().pk_tc_count_stats(st, 1)
+        res = pk.run_pipeline(pk.PointSet(data), pk.VamanaConfig(R=16, L_build=32, L=32, alpha=1.1, seed=0), k=16,
+                              density_kind="kth", center_policy=pk.ProductCenter(10), noise_policy=pk.NoisePolicy(0.0),
+                              doubling_params=pk.DoublingParams(initial_k=32, threshold=0))
+        _lib.lib().pk_tc_count_stats(st, 1)
+        assert (st[0] > 0) == (flag == "1")
+        s = res.state
+        out[flag] = [s.rho, s.lam, s.delta, res.clustering.labels]
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("kind", ["u8", "float"])
 def test_build_with_short_candidate_lists_matches_oracle(kind):
     """L_build < R: many items have at most R candidates, and the build still

@@ -2,6 +2,7 @@
 
     python tools/run_config.py C4 [N] [brute]
 """
+import ctypes
 import os
 import sys
 import time
@@ -36,7 +37,9 @@ _lib.prof_enable(False)
 prof = _lib.prof_collect(reset=True)
 print(f"total {el:.3f}s stages { {k: round(v, 3) for k, v in out['timings'].items()} } rounds {trace}")
 print("kernels", [(k, round(v[1], 1)) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])[:8]])
-print("tc", index.TC_STATS)
+_cs = (ctypes.c_int64 * 2)()
+_lib.lib().pk_tc_count_stats(_cs, 1)
+print("tc", index.TC_STATS, "count decisions (rows, left open):", tuple(_cs))
 labels = _lib.to_host(out["labels"])
 print("ARI vs generator", pk.ari(labels, truth))
 # second pass in the same process: one-time set-up (module loading, pool growth) excluded
