@@ -87,6 +87,8 @@ struct SearchParams {
     // set = the start may be among the point's take nearest
     const unsigned* seed_mask = nullptr;
     int seed_mw = 0;
+    // exact integer start distances (u8 d = 128 builds, u8_seed_table): [n][s]
+    const unsigned* seed_tab = nullptr;
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
 
@@ -113,6 +115,7 @@ struct WarpBeam {
     int vl;
     unsigned* err;
     long long evals;  // distance evaluations (lane 0 count)
+    unsigned qid = 0xffffffffu;  // member query id where known (build searches)
     unsigned* ubm;    // counting mode only: this warp's bitmap of evaluated ids
     long long uniq;   // distinct ids evaluated (the roofline's U)
     bool lazy;        // lazy keys (float data, set by seed())
@@ -652,13 +655,19 @@ struct WarpBeam {
         const int s = P.s;
         unsigned* dsc = reinterpret_cast<unsigned*>(sm.hash);  // [s] seed distances
         unsigned* bins = reinterpret_cast<unsigned*>(sm.bd);   // [256] histogram
-        for (int b = 0; b < s; b += 32) {
-            const int cnt = min(32, s - b);
-            const unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
-            count_unique(id, cnt);
-            const double dd = dist.eval(P.X, (int)id, cnt);
-            if (lane == 0) evals += cnt;
-            if (lane < cnt) dsc[b + lane] = (unsigned)dd;
+        if (P.seed_tab && qid != 0xffffffffu) {
+            // precomputed on the integer tensor cores: the same exact distances
+            const unsigned* row = P.seed_tab + (size_t)qid * s;
+            for (int x = lane; x < s; x += 32) dsc[x] = __ldg(row + x);
+        } else {
+            for (int b = 0; b < s; b += 32) {
+                const int cnt = min(32, s - b);
+                const unsigned id = lane < cnt ? (unsigned)P.starts[b + lane] : 0u;
+                count_unique(id, cnt);
+                const double dd = dist.eval(P.X, (int)id, cnt);
+                if (lane == 0) evals += cnt;
+                if (lane < cnt) dsc[b + lane] = (unsigned)dd;
+            }
         }
         __syncwarp();
         const int take = min(L, s);

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         auto dist = make(p);
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, A.L, A.vlog_i + (size_t)t * A.vcap, A.vlog_d + (size_t)t * A.vcap, A.vcap, A.err);
+        wb.qid = p;
         wb.begin_counting(A.P.ubm ? A.P.ubm + ((size_t)blockIdx.x * wpb + wib) * A.P.uwords : nullptr, A.P.uwords);
         wb.seed(A.P, dist, false, uniq);
         if (A.P.seed_save) wb.save_seed(A.P, p);
@@ -1231,6 +1232,8 @@ int config_kernel(K kern, size_t warp_bytes, int want_wpb, int* wpb_out, int* gr
 bool tc_supported();
 int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int take, unsigned* mask, int mw,
                  cudaStream_t st);
+// scan.cu: exact u8 distances of every point to every start on the integer tensor cores
+int u8_seed_table(const unsigned* x8, int n, const int* starts, int s, unsigned* tab, cudaStream_t st);
 
 template <int MODE, int QV>
 int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
@@ -1401,6 +1404,15 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         if ((rc = tc_seed_mask(D.X, n, D.dp, starts, s, std::min(L, s), seed_mask, mw, st))) return rc;
         A.P.seed_mask = seed_mask;
         A.P.seed_mw = mw;
+    }
+    // u8 rows of d = 128: the exact start distances of every point from one
+    // integer tensor-core pass (beam.cuh seed_select reads them)
+    unsigned* seed_tab = nullptr;
+    if (MODE == MODE_EXACT_U8 && D.dw == 32 && D.X8 && A.P.seed_select && !ubm && !multi && L >= 128 &&
+        (L & (L - 1)) == 0 && s > 32 && (long long)n * s <= (1ll << 31) && env_int("PK_SEED_TAB", 1) == 1) {
+        PK_CHECK(scratch(&seed_tab, (size_t)n * s, st));
+        if ((rc = u8_seed_table(D.X8, n, starts, s, seed_tab, st))) return rc;
+        A.P.seed_tab = seed_tab;
     }
     A.D = D;
     A.L = L;
@@ -1596,7 +1608,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
                     (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)adjd, (void*)new_d,
-                    (void*)addd, (void*)seed_mask, cub_tmp})
+                    (void*)addd, (void*)seed_mask, (void*)seed_tab, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

@@ -34,7 +34,7 @@ struct ScanArgs {
     long long* count;          // (m,) SCAN_COUNT
 };
 
-enum { SCAN_DENSER = 0, SCAN_COUNT = 1 };
+enum { SCAN_DENSER = 0, SCAN_COUNT = 1, SCAN_DUMP = 2 };
 
 // distances from one point row to the QT staged queries
 template <int MODE>
@@ -408,14 +408,18 @@ __device__ __forceinline__ void cu_stage(const unsigned* __restrict__ X8, int n,
 // OP = SCAN_COUNT: count[q] += #{j != q : (d, j) < key}; OP = SCAN_DENSER:
 // best[q] = min over j with rank[j] > rank[q] of the packed key (d << 32 | j)
 // (exact integer distances < 2^32, ids < 2^30: the u64 order is the (d, id) order).
+// OP = SCAN_DUMP: dump[q * n + j] = d(Q8 row q, X8 row j) for every column (qids
+// null: query q is row q of Q8).  Query rows come from Q8, columns from X8.
 template <int OP>
-__global__ void __launch_bounds__(128) u8_tc_scan_kernel(const unsigned* __restrict__ X8, int n,
+__global__ void __launch_bounds__(128) u8_tc_scan_kernel(const unsigned* __restrict__ Q8,
+                                                        const unsigned* __restrict__ X8, int n,
                                                         const long long* __restrict__ qids, int m,
                                                         const double* __restrict__ key_d,
                                                         const long long* __restrict__ key_i,
                                                         const long long* __restrict__ rank, int tiles_per_block,
                                                         long long* __restrict__ count,
-                                                        unsigned long long* __restrict__ best) {
+                                                        unsigned long long* __restrict__ best,
+                                                        unsigned* __restrict__ dump) {
     __shared__ __align__(16) unsigned qs[CU_Q * 32];
     __shared__ __align__(16) unsigned ps[2][CU_P * 32];
     __shared__ unsigned pn[2][CU_P];
@@ -425,8 +429,8 @@ __global__ void __launch_bounds__(128) u8_tc_scan_kernel(const unsigned* __restr
     const int q0 = blockIdx.x * CU_Q;
     for (int e = tid; e < CU_Q * 8; e += 128) {
         const int r = e >> 3, ch = e & 7;
-        const long long qi = qids[min(q0 + r, m - 1)];
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(X8 + (size_t)qi * 32 + ch * 4));
+        const long long qi = qids ? qids[min(q0 + r, m - 1)] : (long long)min(q0 + r, m - 1);
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(Q8 + (size_t)qi * 32 + ch * 4));
         *reinterpret_cast<uint4*>(qs + r * 32 + ((ch ^ (r & 7)) << 2)) = v;
     }
     const int t0 = blockIdx.y * tiles_per_block;
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(128) u8_tc_scan_kernel(const unsigned* __restr
         nb = __dp4a(y, y, nb);
     }
     const bool va = q0 + ra < m, vb = q0 + rb < m;
-    const long long sa = va ? qids[q0 + ra] : -1, sb = vb ? qids[q0 + rb] : -1;
+    const long long sa = (va && qids) ? qids[q0 + ra] : -1, sb = (vb && qids) ? qids[q0 + rb] : -1;
     double ka = -1.0, kb = -1.0;
     unsigned ia = 0u, ib = 0u;
     long long rka = 0x7fffffffffffffffLL, rkb = 0x7fffffffffffffffLL;
@@ -460,7 +464,7 @@ __global__ void __launch_bounds__(128) u8_tc_scan_kernel(const unsigned* __restr
         kb = vb ? key_d[q0 + rb] : -1.0;
         ia = va ? (unsigned)key_i[q0 + ra] : 0u;
         ib = vb ? (unsigned)key_i[q0 + rb] : 0u;
-    } else {
+    } else if constexpr (OP == SCAN_DENSER) {
         if (va) rka = rank[sa];
         if (vb) rkb = rank[sb];
     }
@@ -501,7 +505,10 @@ __global__ void __launch_bounds__(128) u8_tc_scan_kernel(const unsigned* __restr
                 if (j >= n) continue;
                 const unsigned pj = pn[buf][c0 + h];
                 const unsigned ua = na + pj - 2u * (unsigned)d[h], ub = nb + pj - 2u * (unsigned)d[2 + h];
-                if constexpr (OP == SCAN_COUNT) {
+                if constexpr (OP == SCAN_DUMP) {
+                    if (va) dump[(size_t)(q0 + ra) * n + j] = ua;
+                    if (vb) dump[(size_t)(q0 + rb) * n + j] = ub;
+                } else if constexpr (OP == SCAN_COUNT) {
                     if (va && (long long)j != sa && key_lt((double)ua, (unsigned)j, ka, ia)) ++ca;
                     if (vb && (long long)j != sb && key_lt((double)ub, (unsigned)j, kb, ib)) ++cb;
                 } else {
@@ -524,7 +531,7 @@ __global__ void __launch_bounds__(128) u8_tc_scan_kernel(const unsigned* __restr
             if (va && ca) atomicAdd(reinterpret_cast<unsigned long long*>(count + q0 + ra), (unsigned long long)ca);
             if (vb && cb) atomicAdd(reinterpret_cast<unsigned long long*>(count + q0 + rb), (unsigned long long)cb);
         }
-    } else {
+    } else if constexpr (OP == SCAN_DENSER) {
 #pragma unroll
         for (int o = 1; o <= 2; o <<= 1) {
             ba = min(ba, __shfl_xor_sync(PK_FULL, ba, o));
@@ -549,19 +556,41 @@ __global__ void u8_tc_best_kernel(const unsigned long long* best, int m, long lo
 template <int OP>
 int launch_u8_tc_scan(const unsigned* x8, int64_t n, const int64_t* qids, int64_t m, const double* key_d,
                       const int64_t* key_i, const int64_t* rank, long long* count, unsigned long long* best,
-                      cudaStream_t st) {
+                      cudaStream_t st, const unsigned* q8 = nullptr, unsigned* dump = nullptr) {
     const int qt = (int)((m + CU_Q - 1) / CU_Q);
     const int ntile = (int)((n + CU_P - 1) / CU_P);
     int splits = std::max(1, std::min(ntile, (sm_count() * 32 + qt - 1) / qt));
     const int per = (ntile + splits - 1) / splits;
     splits = (ntile + per - 1) / per;
-    ProfScope _ps(OP == SCAN_COUNT ? "count_u8_tc_kernel" : "denser_u8_tc_kernel", st);
+    ProfScope _ps(OP == SCAN_COUNT ? "count_u8_tc_kernel" : OP == SCAN_DUMP ? "seed_u8_tc_kernel" : "denser_u8_tc_kernel",
+                  st);
     u8_tc_scan_kernel<OP><<<dim3(qt, splits), 128, 0, st>>>(
-        x8, (int)n, reinterpret_cast<const long long*>(qids), (int)m, key_d, reinterpret_cast<const long long*>(key_i),
-        reinterpret_cast<const long long*>(rank), per, count, best);
+        q8 ? q8 : x8, x8, (int)n, reinterpret_cast<const long long*>(qids), (int)m, key_d, reinterpret_cast<const long long*>(key_i),
+        reinterpret_cast<const long long*>(rank), per, count, best, dump);
     PK_CHECK_LAUNCH("u8_tc_scan_kernel");
     return 0;
 }
+
+__global__ void gather_rows8_kernel(const unsigned* x8, const int* starts, int s, unsigned* out) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < s * 32; t += gridDim.x * blockDim.x)
+        out[t] = x8[(size_t)starts[t >> 5] * 32 + (t & 31)];
+}
+
+namespace pk {
+// Exact squared distances of every u8 row (d = 128) to every start:
+// tab[i * s + j] = |x_i - x_starts[j]|^2, from one integer tensor-core pass over
+// the gathered start rows (build.cu: the build's seeding reads them).
+int u8_seed_table(const unsigned* x8, int n, const int* starts, int s, unsigned* tab, cudaStream_t st) {
+    unsigned* rows = nullptr;
+    PK_CHECK(scratch(&rows, (size_t)s * 32, st));
+    gather_rows8_kernel<<<(s * 32 + 255) / 256, 256, 0, st>>>(x8, starts, s, rows);
+    PK_CHECK_LAUNCH("gather_rows8_kernel");
+    const int rc = launch_u8_tc_scan<SCAN_DUMP>(rows, s, nullptr, n, nullptr, nullptr, nullptr, nullptr, nullptr, st,
+                                                x8, tab);
+    release(rows, st);
+    return rc;
+}
+}  // namespace pk
 
 int dp_scan_u8_tc(const uint32_t* x8, int64_t n, const int64_t* rank, const int64_t* qids, int64_t m, int64_t* out_id,
                   double* out_sqd, cudaStream_t st) {

@@ -417,6 +417,34 @@ def test_tensor_core_count_decision_equals_exact_count(monkeypatch, case):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("case", ["c2", "c3", "dup"])
+def test_u8_seed_table_equals_warp_seeding(monkeypatch, case):
+    """u8 rows of d = 128: the build's start distances precomputed on the integer
+    tensor cores (exact) give the same graph and kNN rows as the warp-evaluated
+    seeding (PK_SEED_TAB=0)."""
+    if case in ("c2", "c3"):
+        data, _ = workloads.generate(case.upper(), n=20_000, components=20)
+    else:
+        rng = np.random.default_rng(31)
+        data = rng.integers(0, 4, size=(12_000, 128)).astype(np.float32)  # heavy ties
+        data[:100] = data[100:200]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PK_SEED_TAB", flag)
+        p = pk.PointSet(data)
+        assert p.mode == _lib.MODE_EXACT_U8
+        _lib.prof_collect(reset=True)
+        _lib.prof_only([])
+        _lib.prof_enable(True)
+        g = pk.build_vamana(p, R=32, L_build=128, alpha=1.1, seed=5, query_beam=128)
+        _lib.prof_enable(False)
+        assert ("seed_u8_tc_kernel" in _lib.prof_collect(reset=True)) == (flag == "1")
+        nb = g.knn_all(16)
+        out[flag] = (g.graph.adjacency.copy(), g.graph.degrees.copy(), nb.ids.copy(), nb.dists.copy())
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("kind", ["u8", "float"])
 def test_build_with_short_candidate_lists_matches_oracle(kind):
     """L_build < R: many items have at most R candidates, and the build still
