@@ -48,6 +48,10 @@ inline void release(void* p, cudaStream_t st) {
 inline size_t beam_smem_bytes(int L, int H) {
     return (((((size_t)L * 12 + 7) & ~(size_t)7) + (size_t)H * 2 + 15) & ~(size_t)15) + 128 + 4 * 64;
 }
+// spilled beam (carve_beam_spill): shared memory for the seen table and scratch,
+// a global slab of spill_slab_bytes(L) per warp for the beam itself
+inline size_t spill_smem_bytes(int H) { return (((size_t)H * 2 + 15) & ~(size_t)15) + 128 + 4 * 64; }
+inline size_t spill_slab_bytes(int L) { return ((size_t)L * 12 + 15) & ~(size_t)15; }
 inline size_t sort_smem_bytes(int cap) {
     return (size_t)cap * 13 + 128;
 }

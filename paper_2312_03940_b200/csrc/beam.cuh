@@ -57,6 +57,25 @@ __device__ __forceinline__ BeamSmem carve_beam(unsigned char* base, int L, int H
     return s;
 }
 
+// Beams wider than shared memory (doubling rounds that reach k ~ 16k and
+// beyond; the reference doubles up to n - 1, dependent.py:118-126): the
+// sorted beam bd[L] | bi[L] lives in a per-warp global slab, the seen table
+// and the scratch stay in shared memory.  The walk is the same code on
+// generic pointers, so the result is the same as the in-smem beam.
+// smem layout: hash[H] (u16) | spos[32] | cbuf[kCbuf] (host: spill_smem_bytes)
+__device__ __forceinline__ BeamSmem carve_beam_spill(unsigned char* base, unsigned char* slab, int L, int H) {
+    BeamSmem s;
+    s.bd = reinterpret_cast<double*>(slab);
+    s.bi = reinterpret_cast<unsigned*>(slab + (size_t)L * 8);
+    s.hash = reinterpret_cast<unsigned short*>(base);
+    s.hmask = (unsigned)H - 1u;
+    s.hbits = __ffs(H) - 1;
+    const size_t tail = ((size_t)H * 2 + 15) & ~(size_t)15;
+    s.spos = reinterpret_cast<int*>(base + tail);
+    s.cbuf = reinterpret_cast<unsigned*>(base + tail + 128);
+    return s;
+}
+
 struct SearchParams {
     const float* X;          // (n, dp)
     int dp;

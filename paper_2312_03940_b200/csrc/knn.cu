@@ -14,13 +14,15 @@ template <int MODE, int QV>
 __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 6 : 8) : 8) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
                                                        int L, int kk, int H, size_t warp_bytes,
                                                        long long* __restrict__ out_ids, double* __restrict__ out_d,
-                                                       long long* __restrict__ counts, long long* evals_out) {
+                                                       long long* __restrict__ counts, long long* evals_out,
+                                                       unsigned char* gbeam, size_t gstride) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int lane = lane_id();
     unsigned char* mine = smem + (size_t)wib * warp_bytes;
-    BeamSmem sm = carve_beam(mine, L, H);
+    BeamSmem sm = gbeam ? carve_beam_spill(mine, gbeam + ((size_t)blockIdx.x * wpb + wib) * gstride, L, H)
+                        : carve_beam(mine, L, H);
     long long ev = 0, ex = 0, un = 0;
     const bool uniq = starts_increasing(P);
     for (long long t = (long long)blockIdx.x * wpb + wib; t < m; t += (long long)gridDim.x * wpb) {
@@ -67,9 +69,9 @@ template <class Dist>
 __global__ void single_search_kernel(SearchParams P, Dist dist, unsigned self, int L, int k, int H,
                                      long long* top_ids, double* top_d, long long* top_count,
                                      long long* vis_ids, double* vis_d, int vcap, long long* vis_count,
-                                     unsigned* vtmp_i, double* vtmp_d) {
+                                     unsigned* vtmp_i, double* vtmp_d, unsigned char* gbeam) {
     extern __shared__ __align__(16) unsigned char smem[];
-    BeamSmem sm = carve_beam(smem, L, H);
+    BeamSmem sm = gbeam ? carve_beam_spill(smem, gbeam, L, H) : carve_beam(smem, L, H);
     __shared__ unsigned s_err;
     if (threadIdx.x == 0) s_err = 0;
     __syncwarp();
@@ -283,8 +285,10 @@ __global__ void check_exact32_kernel(const float* x, long long total, int dp, in
 __global__ void finish_exact32_kernel(const int* bad, const unsigned* range, int d, int* flag) {
     double span = (double)from_ordered(range[0]) - (double)from_ordered(range[1]);
     double bound = (double)d * span * span;
-    // 2: bytes (x - min) hold every coordinate exactly; 1: float32 sums exact
-    *flag = *bad ? 0 : span <= 255.0 ? 2 : bound < 16777216.0 ? 1 : 0;
+    // 2: bytes (x - min) hold every coordinate exactly; 1: float32 sums exact.
+    // The integer kernels hold a query row in at most 8 slices of 128 floats /
+    // 32 packed words, so rows wider than 1024 take the float64 policy.
+    *flag = (*bad || d > 1024) ? 0 : span <= 255.0 ? 2 : bound < 16777216.0 ? 1 : 0;
 }
 
 __global__ void pack_u8_kernel(const float* x, long long n, int dp, int d, const unsigned* range, int dw,
@@ -346,10 +350,10 @@ template <int MODE, int QV>
 int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, int kk, int H,
                     long long* out_ids, double* out_d, long long* counts, long long* evals, cudaStream_t st) {
     size_t wb = align16(beam_smem_bytes(L, H));
-    if (wb > (size_t)max_smem_optin()) {
-        set_error("beam width too large for shared memory");
-        return 2;
-    }
+    // beams past the shared-memory opt-in: the beam goes to a global slab per warp
+    const bool spill = wb > (size_t)max_smem_optin();
+    const size_t gstride = spill ? spill_slab_bytes(L) : 0;
+    if (spill) wb = align16(spill_smem_bytes(H));
     // warps per block: the most resident warps per SM (wide beams: a block of 2
     // x 64 KB leaves a third warp's worth of the SM's shared memory unused)
     const size_t sm_bytes = (size_t)max_smem_optin() + 1024;  // per-SM capacity (one block's reserve)
@@ -370,7 +374,14 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     long long blocks = ((long long)m + wpb - 1) / wpb;
     long long cap = (long long)sm_count() * per_sm;
     int grid = (int)(blocks < cap ? blocks : cap);
+    if (spill) {
+        // slabs for at most ~1 GiB of beams (the widest rounds hold few queries)
+        const long long max_warps = std::max<long long>(wpb, (1ll << 30) / (long long)gstride);
+        grid = (int)std::min<long long>(grid, max_warps / wpb);
+    }
     if (grid < 1) grid = 1;
+    unsigned char* gbeam = nullptr;
+    if (spill) PK_CHECK(scratch(&gbeam, (size_t)grid * wpb * gstride, st));
     // counting mode (bench.py's untimed pass): exact number of distinct ids
     // evaluated, added to evals[2] (the caller then passes 3 counters)
     SearchParams Pc = P;
@@ -382,10 +393,12 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     }
     {
         ProfScope _ps("beam_knn_kernel", st);
-        kern<<<grid, 32 * wpb, wb * wpb, st>>>(Pc, qids, m, L, kk, H, wb, out_ids, out_d, counts, evals);
+        kern<<<grid, 32 * wpb, wb * wpb, st>>>(Pc, qids, m, L, kk, H, wb, out_ids, out_d, counts, evals, gbeam,
+                                               gstride);
     }
     PK_CHECK_LAUNCH("beam_knn_kernel");
     if (ubm) release(ubm, st);
+    if (gbeam) release(gbeam, st);
     return 0;
 }
 
@@ -626,6 +639,11 @@ extern "C" int pk_beam_search_single(const float* x, int64_t n, int64_t dp, cons
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s};
     int H = choose_hash((int)L, 0, n);
     size_t bytes = align16(beam_smem_bytes((int)L, H));
+    unsigned char* gbeam = nullptr;
+    if (bytes > (size_t)max_smem_optin()) {  // wide beam: global slab (carve_beam_spill)
+        bytes = align16(spill_smem_bytes(H));
+        PK_CHECK(scratch(&gbeam, spill_slab_bytes((int)L), st));
+    }
     unsigned* vi = nullptr;
     double* vd = nullptr;
     PK_CHECK(scratch(&vi, (size_t)vcap, st));
@@ -639,7 +657,7 @@ extern "C" int pk_beam_search_single(const float* x, int64_t n, int64_t dp, cons
             kern<<<1, 32, bytes, st>>>(P, Seq64Member{x + (size_t)qid * dp, (int)dp}, self, (int)L, (int)k, H,
                                        reinterpret_cast<long long*>(top_ids), top_sqd, reinterpret_cast<long long*>(top_count),
                                        reinterpret_cast<long long*>(vis_ids), vis_sqd, (int)vcap,
-                                       reinterpret_cast<long long*>(vis_count), vi, vd);
+                                       reinterpret_cast<long long*>(vis_count), vi, vd, gbeam);
         }
     } else {
         auto kern = single_search_kernel<Seq64Vector>;
@@ -649,12 +667,13 @@ extern "C" int pk_beam_search_single(const float* x, int64_t n, int64_t dp, cons
             kern<<<1, 32, bytes, st>>>(P, Seq64Vector{qvec, (int)dp}, self, (int)L, (int)k, H,
                                        reinterpret_cast<long long*>(top_ids), top_sqd, reinterpret_cast<long long*>(top_count),
                                        reinterpret_cast<long long*>(vis_ids), vis_sqd, (int)vcap,
-                                       reinterpret_cast<long long*>(vis_count), vi, vd);
+                                       reinterpret_cast<long long*>(vis_count), vi, vd, gbeam);
         }
     }
     PK_CHECK_LAUNCH("single_search_kernel");
     release(vi, st);
     release(vd, st);
+    release(gbeam, st);
     return 0;
 }
 
