@@ -181,6 +181,15 @@ int pk_build_vamana_sharded(const float* x, int64_t n, int64_t dp, const uint32_
 int pk_pcg64_permutation(const uint64_t* state, int has_uint32, uint32_t uinteger, int64_t n, int32_t* out,
                          uint64_t* state_out);
 
+/* Host helper (no device work): parse the vertex records of a PECG graph file
+ * (everything after the 16-byte header and the start ids: per vertex a u32
+ * degree followed by that many u32 neighbour ids; vamana.py:243-267 replaces
+ * its per-vertex Python loop) into adj (n, R) int32 padded with -1 and
+ * deg (n,) int32.  Returns 0, or 3 = truncated at vertex info[0], 4 = vertex
+ * info[0] has degree info[1] > R, 5 = info[0] trailing bytes. */
+int pk_parse_pecg(const uint32_t* words, int64_t nwords, int64_t n, int64_t R, int32_t* adj, int32_t* deg,
+                  int64_t* info);
+
 /* Host helper: index of the first non-finite value of x[0, count) in
  * row-major order (-1 if none) -> *first_bad; all host threads scan.  The
  * PointSet finiteness check (core.py:17-54). */

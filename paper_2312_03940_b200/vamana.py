@@ -110,7 +110,9 @@ class GraphIndex:
 
     def device_arrays(self):
         """(adj (n,R) int32, deg (n,) int32, starts (s,) int32) on device."""
-        if self._adj is not None or self._deg is not None:
+        frozen = (self._uploaded == "read-only" and self._adj_t is not None and self._deg_t is not None
+                  and not self._adj.flags.writeable and not self._deg.flags.writeable)
+        if (self._adj is not None or self._deg is not None) and not frozen:
             adj, deg = self.adjacency, self.degrees
             dig = _digest(adj, deg)
             if self._adj_t is None or self._deg_t is None or dig != self._uploaded:
@@ -451,30 +453,62 @@ def save_graph(g: GraphIndex, path) -> None:
 
 
 def load_graph(path, points: PointSet, alpha: float = 1.0) -> GraphIndex:
-    """Read a graph written by save_graph (vamana.py:243-267)."""
+    """Read a graph written by save_graph (format and errors of vamana.py:243-267).
+
+    The vertex records are parsed by one native pass (pk_parse_pecg) straight
+    into pinned host buffers, then uploaded once; the returned host arrays are
+    read-only views of those buffers (the device copy stays authoritative)."""
     with open(path, "rb") as f:
-        blob = f.read()
-    if blob[:4] != GRAPH_MAGIC:
-        raise ValueError(f"{path}: bad magic {blob[:4]!r}")
-    n, R, ns = struct.unpack_from("<III", blob, 4)
-    if n != points.n:
-        raise ValueError(f"{path}: graph has {n} vertices but points has {points.n}")
-    off = 16
-    starts = np.frombuffer(blob, "<u4", ns, off).astype(np.int64)
-    off += 4 * ns
-    words = np.frombuffer(blob, "<u4", (len(blob) - off) // 4, off)
-    adj = np.full((n, R), -1, dtype=np.int32)
-    deg = np.zeros(n, dtype=np.int32)
-    pos = 0
-    for i in range(n):
-        if pos >= words.shape[0]:
-            raise ValueError(f"{path}: truncated at vertex {i}")
-        d = int(words[pos])
-        if d > R:
-            raise ValueError(f"{path}: vertex {i} degree {d} exceeds bound {R}")
-        adj[i, :d] = words[pos + 1 : pos + 1 + d].astype(np.int32)
-        deg[i] = d
-        pos += 1 + d
-    if off + 4 * pos != len(blob):
-        raise ValueError(f"{path}: {len(blob) - off - 4 * pos} trailing bytes")
-    return GraphIndex(points, adj, deg, R, starts, alpha)
+        head = f.read(16)
+        if head[:4] != GRAPH_MAGIC:
+            raise ValueError(f"{path}: bad magic {head[:4]!r}")
+        if len(head) < 16:
+            raise ValueError(f"{path}: truncated header")
+        n, R, ns = struct.unpack_from("<III", head, 4)
+        if n != points.n:
+            raise ValueError(f"{path}: graph has {n} vertices but points has {points.n}")
+        starts_raw = f.read(4 * ns)
+        if len(starts_raw) != 4 * ns:
+            raise ValueError(f"{path}: truncated start list")
+        body = f.read()
+    starts = np.frombuffer(starts_raw, "<u4").astype(np.int64)
+    words = np.frombuffer(body, "<u4", len(body) // 4)
+    odd = len(body) % 4
+    pinned = _host_cuda()
+    if pinned:
+        import torch
+
+        adj_h = torch.empty((n, R), dtype=torch.int32, pin_memory=True)
+        deg_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        adj, deg = adj_h.numpy(), deg_h.numpy()
+    else:
+        adj = np.empty((n, R), np.int32)
+        deg = np.empty(n, np.int32)
+    info = np.zeros(2, np.int64)
+    rc = _lib.lib().pk_parse_pecg(words.ctypes.data, words.shape[0], n, R, adj.ctypes.data, deg.ctypes.data,
+                                  info.ctypes.data)
+    if rc == 3:
+        raise ValueError(f"{path}: truncated at vertex {info[0]}")
+    if rc == 4:
+        raise ValueError(f"{path}: vertex {info[0]} degree {info[1]} exceeds bound {R}")
+    if rc == 5 or (rc == 0 and odd):
+        raise ValueError(f"{path}: {int(info[0]) + odd if rc == 5 else odd} trailing bytes")
+    if rc != 0:
+        raise RuntimeError(f"pk_parse_pecg failed ({rc})")
+    g = GraphIndex(points, adj, deg, R, starts, alpha)
+    if pinned:
+        g._adj_t = adj_h.to(_lib.device(), non_blocking=True)
+        g._deg_t = deg_h.to(_lib.device(), non_blocking=True)
+        adj.flags.writeable = False
+        deg.flags.writeable = False
+        g._uploaded = "read-only"
+    return g
+
+
+def _host_cuda() -> bool:
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # noqa: BLE001
+        return False

@@ -120,9 +120,51 @@ def test_pecg_errors(tmp_path):
     pk.save_graph(g, path)
     with pytest.raises(ValueError, match="vertices"):
         pk.load_graph(path, pk.PointSet(np.zeros((2, 2), np.float32)))
-    path.write_bytes(path.read_bytes() + b"\x00\x00\x00\x00")
+    good = path.read_bytes()
+    path.write_bytes(good + b"\x00\x00\x00\x00")
     with pytest.raises(ValueError, match="trailing"):
         pk.load_graph(path, g.points)
+    path.write_bytes(good + b"\x00\x00")
+    with pytest.raises(ValueError, match="2 trailing bytes"):
+        pk.load_graph(path, g.points)
+    path.write_bytes(good[:-4])
+    with pytest.raises(ValueError, match="truncated"):
+        pk.load_graph(path, g.points)
+    # vertex 0's degree word (after the 16-byte header and one start id) set past R
+    blob = bytearray(good)
+    blob[20:24] = (9).to_bytes(4, "little")
+    path.write_bytes(bytes(blob))
+    with pytest.raises(ValueError, match="vertex 0 degree 9 exceeds bound 4"):
+        pk.load_graph(path, g.points)
+
+
+def test_pecg_parse_matches_python_loop(tmp_path):
+    """pk_parse_pecg equals the reference's per-vertex loop (vamana.py:253-264)
+    on a random graph with ragged degrees."""
+    import struct
+
+    rng = np.random.default_rng(5)
+    n, R = 500, 12
+    p = pk.PointSet(rng.normal(size=(n, 3)).astype(np.float32))
+    deg = rng.integers(0, R + 1, n).astype(np.int32)
+    adj = np.full((n, R), -1, np.int32)
+    for i in range(n):
+        adj[i, : deg[i]] = rng.choice(n, deg[i], replace=False)
+    g = pk.GraphIndex(p, adj, deg, R, np.array([3, 9], np.int64), 1.0)
+    path = tmp_path / "r.bin"
+    pk.save_graph(g, path)
+    blob = path.read_bytes()
+    off = 16 + 8
+    want_adj = np.full((n, R), -1, np.int32)
+    want_deg = np.zeros(n, np.int32)
+    for i in range(n):
+        (d,) = struct.unpack_from("<I", blob, off)
+        want_adj[i, :d] = np.frombuffer(blob, "<u4", d, off + 4).astype(np.int32)
+        want_deg[i] = d
+        off += 4 + 4 * d
+    back = pk.load_graph(path, p)
+    assert np.array_equal(back.adjacency, want_adj)
+    assert np.array_equal(back.degrees, want_deg)
 
 
 def test_metrics():

@@ -247,12 +247,16 @@ def test_integer_data_wider_than_1024_columns_matches_oracle():
 
 
 def test_doubling_to_n_minus_1_spills_beam_and_matches_oracle():
-    """threshold = 0 on C3-shaped data (every rho = 0, rank = id order): the
-    lowest ids stay unresolved until the doubling reaches k = n - 1 = 19,999,
+    """threshold = 0 on C3-shaped data (every rho = 0, rank = id order): id 1
+    stays unresolved until the doubling reaches k = n - 1 = 19,999,
     whose beam (12 B x L) no longer fits in shared memory and runs from the
     global slab (reference keeps doubling up to n - 1: dependent.py:118-126)."""
     n = 20_000
-    data, _ = workloads.generate("C3", n=n, components=20)
+    data, _ = workloads.generate("C3", n=n, components=1)
+    # id 0 (the only point denser than id 1) becomes id 1's farthest point, so
+    # id 1 is resolved only by the round at k = n - 1
+    far = int(np.argmax(((data.astype(np.float64) - data[1]) ** 2).sum(1)))
+    data[[0, far]] = data[[far, 0]]
     res = pk.run_pipeline(pk.PointSet(data), pk.VamanaConfig(R=64, L_build=128, L=128, alpha=1.1, seed=0), k=32,
                           density_kind="exp_sum", center_policy=pk.ProductCenter(20), noise_policy=pk.NoisePolicy(0.0),
                           doubling_params=pk.DoublingParams(initial_k=64, threshold=0))
