@@ -1231,9 +1231,50 @@ int config_kernel(K kern, size_t warp_bytes, int want_wpb, int* wpb_out, int* gr
 // tc_knn.cu: tensor-core screens of all points against the start set
 bool tc_supported();
 int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int take, unsigned* mask, int mw,
-                 cudaStream_t st);
+                 int* near, cudaStream_t st);
 // scan.cu: exact u8 distances of every point to every start on the integer tensor cores
 int u8_seed_table(const unsigned* x8, int n, const int* starts, int s, unsigned* tab, cudaStream_t st);
+
+// ---- locality order of the batches' points ------------------------------------
+// key of position i of the insertion order: (batch of i, nearest start of the
+// point); batches are [2^b - 1, 2^(b+1) - 1), so the batch is floor(log2(i + 1))
+__global__ void locality_keys_kernel(const int* order, int n, const int* near, int sbits, unsigned* keys, int* vals) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned b = 31u - (unsigned)__clz((unsigned)i + 1u);
+        const int p = order[i];
+        keys[i] = (b << sbits) | (unsigned)near[p];
+        vals[i] = p;
+    }
+}
+
+// A permutation of `order` that keeps every batch's set of points and sorts
+// each batch by nearest start (stable radix sort of the composite keys).
+int locality_order(const int* order, int n, const int* near, int s, int** out, cudaStream_t st) {
+    int sbits = 1;
+    while ((1 << sbits) < s) ++sbits;
+    const int end_bit = sbits + 5;  // <= 32 batches
+    unsigned *k0 = nullptr, *k1 = nullptr;
+    int* v0 = nullptr;
+    PK_CHECK(scratch(&k0, (size_t)n, st));
+    PK_CHECK(scratch(&k1, (size_t)n, st));
+    PK_CHECK(scratch(&v0, (size_t)n, st));
+    PK_CHECK(scratch(out, (size_t)n, st));
+    {
+        ProfScope _ps("locality_keys_kernel", st);
+        locality_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(order, n, near, sbits, k0, v0);
+    }
+    PK_CHECK_LAUNCH("locality_keys_kernel");
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0, k1, v0, *out, n, 0, end_bit, st);
+    void* tmp = nullptr;
+    PK_CHECK(cudaMallocAsync(&tmp, bytes + 16, st));
+    {
+        ProfScope _ps("cub_DeviceRadixSort_SortPairs", st);
+        PK_CHECK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0, k1, v0, *out, n, 0, end_bit, st));
+    }
+    for (void* p : {(void*)k0, (void*)k1, (void*)v0, tmp}) release(p, st);
+    return 0;
+}
 
 template <int MODE, int QV>
 int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* starts, int s, const int* order,
@@ -1397,13 +1438,26 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     // search fp32-screens only the starts whose bound can reach its take-th
     // (tc_knn.cu tc_seed_mask, beam.cuh seed_select_lazy)
     unsigned* seed_mask = nullptr;
+    int* near = nullptr;
     if (MODE == MODE_SEQ64 && D.screen && A.P.lazy && A.P.seed_select && !ubm && !multi && L >= 128 && s > L && n >= 4096 &&
         s >= env_int("PK_SEED_TC_MIN", 256) && s <= 8192 && env_int("PK_SEED_TC", 1) == 1 && tc_supported()) {
         const int mw = (s + 31) / 32;
         PK_CHECK(scratch(&seed_mask, (size_t)n * mw, st));
-        if ((rc = tc_seed_mask(D.X, n, D.dp, starts, s, std::min(L, s), seed_mask, mw, st))) return rc;
+        if (env_int("PK_LOCALITY", 1) == 1) PK_CHECK(scratch(&near, (size_t)n, st));
+        if ((rc = tc_seed_mask(D.X, n, D.dp, starts, s, std::min(L, s), seed_mask, mw, near, st))) return rc;
         A.P.seed_mask = seed_mask;
         A.P.seed_mw = mw;
+    }
+    // Search order inside each batch: a batch's searches and prunes are
+    // independent (every search reads the graph as it stood before the batch,
+    // the re-prunes sort their candidates), so the points of a batch may run in
+    // any order without changing the graph.  Grouped by their nearest start,
+    // the warps running at the same time walk the same region of the data and
+    // share its rows in L2 instead of each pulling its own from HBM.
+    int* lorder = nullptr;
+    if (near && n >= (1 << 16) && s <= (1 << 20)) {
+        if ((rc = locality_order(order, n, near, s, &lorder, st))) return rc;
+        order = lorder;
     }
     // u8 rows of d = 128: the exact start distances of every point from one
     // integer tensor-core pass (beam.cuh seed_select reads them)
@@ -1608,7 +1662,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
                     (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)adjd, (void*)new_d,
-                    (void*)addd, (void*)seed_mask, (void*)seed_tab, cub_tmp})
+                    (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

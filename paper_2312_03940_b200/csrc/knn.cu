@@ -15,7 +15,8 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
                                                        int L, int kk, int H, size_t warp_bytes,
                                                        long long* __restrict__ out_ids, double* __restrict__ out_d,
                                                        long long* __restrict__ counts, long long* evals_out,
-                                                       unsigned char* gbeam, size_t gstride) {
+                                                       unsigned char* gbeam, size_t gstride,
+                                                       const int* __restrict__ ord) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
@@ -25,7 +26,8 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
                         : carve_beam(mine, L, H);
     long long ev = 0, ex = 0, un = 0;
     const bool uniq = starts_increasing(P);
-    for (long long t = (long long)blockIdx.x * wpb + wib; t < m; t += (long long)gridDim.x * wpb) {
+    for (int t0 = blockIdx.x * wpb + wib; t0 < m; t0 += gridDim.x * wpb) {
+        const int t = ord ? __ldg(ord + t0) : t0;  // processing order (locality) != output row order
         const unsigned qi = (unsigned)qids[t];
         auto dist = DistFor<MODE, QV>::make(P.data(), qi);
         WarpBeam<decltype(dist)> wb;
@@ -35,8 +37,8 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         else wb.seed(P, dist, false, uniq);
         if (!P.seed_only) wb.walk(P, dist);
         un += wb.uniq;
-        long long* oi = out_ids + t * kk;
-        double* od = out_d + t * kk;
+        long long* oi = out_ids + (size_t)t * kk;
+        double* od = out_d + (size_t)t * kk;
         int got;
         if constexpr (has_screen<decltype(dist)>::value)
             got = wb.emit(qi, kk, oi, od, [&](unsigned id) { return dist.eval_one(P.X, (int)id); });
@@ -346,6 +348,46 @@ int choose_hash(int L, int hash_bits, long long n) {
     return h;
 }
 
+// keys of the member queries for the locality order: the nearest start (first
+// entry of the seeded beam the build saved for the query)
+__global__ void seed_near_keys_kernel(const long long* qids, int m, const unsigned* seed_bi, int L, unsigned* keys,
+                                      int* vals) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
+        keys[t] = seed_bi[(size_t)qids[t] * L] & PK_IDMASK;
+        vals[t] = t;
+    }
+}
+
+// Processing order of a large batch of member queries, grouped by nearest
+// start: the warps running at the same time search the same region of the data
+// and share its rows in L2 (the results do not depend on the order).
+int query_locality_order(const SearchParams& P, const long long* qids, int m, int L, long long n, int** ord,
+                         cudaStream_t st) {
+    int bits = 1;
+    while ((1ll << bits) < n) ++bits;
+    unsigned *k0 = nullptr, *k1 = nullptr;
+    int* v0 = nullptr;
+    PK_CHECK(scratch(&k0, (size_t)m, st));
+    PK_CHECK(scratch(&k1, (size_t)m, st));
+    PK_CHECK(scratch(&v0, (size_t)m, st));
+    PK_CHECK(scratch(ord, (size_t)m, st));
+    {
+        ProfScope _ps("seed_near_keys_kernel", st);
+        seed_near_keys_kernel<<<grid_for(m, 256), 256, 0, st>>>(qids, m, P.seed_bi, L, k0, v0);
+    }
+    PK_CHECK_LAUNCH("seed_near_keys_kernel");
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0, k1, v0, *ord, m, 0, bits, st);
+    void* tmp = nullptr;
+    PK_CHECK(cudaMallocAsync(&tmp, bytes + 16, st));
+    {
+        ProfScope _ps("cub_DeviceRadixSort_SortPairs", st);
+        PK_CHECK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0, k1, v0, *ord, m, 0, bits, st));
+    }
+    for (void* p : {(void*)k0, (void*)k1, (void*)v0, tmp}) release(p, st);
+    return 0;
+}
+
 template <int MODE, int QV>
 int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, int kk, int H,
                     long long* out_ids, double* out_d, long long* counts, long long* evals, cudaStream_t st) {
@@ -382,6 +424,11 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     if (grid < 1) grid = 1;
     unsigned char* gbeam = nullptr;
     if (spill) PK_CHECK(scratch(&gbeam, (size_t)grid * wpb * gstride, st));
+    int* ord = nullptr;
+    if (P.seed_load && m >= (1 << 16) && env_int("PK_LOCALITY", 1) == 1) {
+        const int rc = query_locality_order(P, qids, m, L, P.n_points, &ord, st);
+        if (rc) return rc;
+    }
     // counting mode (bench.py's untimed pass): exact number of distinct ids
     // evaluated, added to evals[2] (the caller then passes 3 counters)
     SearchParams Pc = P;
@@ -394,11 +441,12 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     {
         ProfScope _ps("beam_knn_kernel", st);
         kern<<<grid, 32 * wpb, wb * wpb, st>>>(Pc, qids, m, L, kk, H, wb, out_ids, out_d, counts, evals, gbeam,
-                                               gstride);
+                                               gstride, ord);
     }
     PK_CHECK_LAUNCH("beam_knn_kernel");
     if (ubm) release(ubm, st);
     if (gbeam) release(gbeam, st);
+    if (ord) release(ord, st);
     return 0;
 }
 

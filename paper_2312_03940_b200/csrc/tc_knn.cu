@@ -628,7 +628,7 @@ namespace pk {
 // non-finite screen (fp16 overflow) keeps its start a candidate with hi = +inf.
 __global__ void seed_mask_kernel(const float* __restrict__ dump, long long ld, int rows, int s, int take,
                                  const float* __restrict__ qn, const float* __restrict__ smax2, float eps, float eabs,
-                                 unsigned* __restrict__ mask, int mw) {
+                                 unsigned* __restrict__ mask, int mw, int* __restrict__ near) {
     extern __shared__ unsigned seed_sh[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int spad = (s + 31) & ~31;
@@ -639,10 +639,29 @@ __global__ void seed_mask_kernel(const float* __restrict__ dump, long long ld, i
         const float* drow = dump + (size_t)r * ld;
         const float q2 = qn[r];
         const float e = eps * sqrtf(q2) * sqrtf(sm2) + eabs * (sqrtf(q2) + sqrtf(sm2)) + 1e-6f * (q2 + sm2);
+        float best = __int_as_float(0x7f800000);
+        int bj = 0;
         for (int x = lane; x < s; x += 32) {
             const float v = drow[x];
             const float h = v + e + 1e-5f * fabsf(v);
             hi[x] = isfinite(h) ? __float_as_uint(fmaxf(h, 0.f)) : 0x7f800000u;
+            if (v < best) {
+                best = v;
+                bj = x;
+            }
+        }
+        if (near) {
+            // screened nearest start (a locality key for the search order, not a result)
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ob = __shfl_xor_sync(PK_FULL, best, o);
+                const int oj = __shfl_xor_sync(PK_FULL, bj, o);
+                if (ob < best || (ob == best && oj < bj)) {
+                    best = ob;
+                    bj = oj;
+                }
+            }
+            if (lane == 0) near[r] = bj;
         }
         __syncwarp();
         int need = 0;
@@ -667,7 +686,7 @@ __global__ void seed_mask_kernel(const float* __restrict__ dump, long long ld, i
 // distance dumped), each chunk reduced to its bits by seed_mask_kernel.  Used by
 // beam.cuh seed_select_lazy to skip the fp32 screens of far starts.
 int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int take, unsigned* mask, int mw,
-                 cudaStream_t st) {
+                 int* near, cudaStream_t st) {
     if (!tc_supported()) {
         set_error("tensor-core screens need an sm_100 device");
         return 2;
@@ -747,7 +766,8 @@ int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int ta
             ProfScope _ps("seed_mask_kernel", st);
             const int grid = std::min(sm_count() * std::max(1, per_sm), (rows + kMaskWarps - 1) / kMaskWarps);
             seed_mask_kernel<<<grid, kMaskWarps * 32, msmem, st>>>(dump, ld, rows, s, take, qn, smax2, eps, eabs,
-                                                                   mask + (size_t)r0 * mw, mw);
+                                                                   mask + (size_t)r0 * mw, mw,
+                                                                   near ? near + r0 : nullptr);
         }
         PK_CHECK_LAUNCH("seed_mask_kernel");
     }

@@ -16,6 +16,7 @@ configuration (index config, k, density kind, policies, doubling params).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -46,16 +47,33 @@ WORKLOADS = {
 }
 
 
-def _gauss_mixture(rng, n, d, comps, center_scale, sigma, weights=None, chunk=131072):
-    means = rng.normal(0.0, center_scale, (comps, d))
+def _gauss_mixture(rng, n, d, comps, center_scale, sigma, weights=None, seed=0, normalise=False, chunk=65536):
+    """means ~ N(0, center_scale^2 I), labels from `rng`; the noise of chunk c
+    comes from its own stream default_rng([seed, 0x5EED, c]) in float32, so
+    the chunks are drawn (and L2-normalised) on all host threads in parallel
+    -- the 1.3 G coordinates of C5 in seconds instead of a minute."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    means = rng.normal(0.0, center_scale, (comps, d)).astype(np.float32)
     if weights is None:
         labels = rng.integers(0, comps, n)
     else:
         labels = rng.choice(comps, size=n, p=weights)
     out = np.empty((n, d), np.float32)
-    for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
-        out[lo:hi] = means[labels[lo:hi]] + rng.normal(0.0, sigma, (hi - lo, d))
+
+    def fill(c):
+        lo, hi = c * chunk, min(n, (c + 1) * chunk)
+        x = np.random.default_rng([seed, 0x5EED, c]).standard_normal((hi - lo, d), dtype=np.float32)
+        x *= np.float32(sigma)
+        x += means[labels[lo:hi]]
+        if normalise:
+            nrm = np.sqrt(np.einsum("ij,ij->i", x, x, dtype=np.float64))
+            x /= nrm.astype(np.float32)[:, None]
+        out[lo:hi] = x
+
+    chunks = (n + chunk - 1) // chunk
+    with ThreadPoolExecutor(max_workers=min(chunks, os.cpu_count() or 1) or 1) as ex:
+        list(ex.map(fill, range(chunks)))
     return out, labels.astype(np.int64)
 
 
@@ -67,11 +85,6 @@ def _sift_shaped(rng, n, d, comps, chunk=131072):
         hi = min(n, lo + chunk)
         out[lo:hi] = np.clip(np.round(rng.normal(mu[labels[lo:hi]], 20.0)), 0, 255)
     return out, labels.astype(np.int64)
-
-
-def _normalise_rows(x):
-    nrm = np.sqrt((x.astype(np.float64) ** 2).sum(axis=1, keepdims=True))
-    return (x / nrm).astype(np.float32)
 
 
 def generate(name: str, n: int | None = None, seed: int = 0, components: int | None = None):
@@ -94,11 +107,9 @@ def generate(name: str, n: int | None = None, seed: int = 0, components: int | N
     if name == "C4":
         wts = (np.arange(comps) + 1.0) ** -1.1
         wts /= wts.sum()
-        x, labels = _gauss_mixture(rng, n, w.d, comps, 1.0, 0.3, wts)
-        return _normalise_rows(x), labels
+        return _gauss_mixture(rng, n, w.d, comps, 1.0, 0.3, wts, seed=seed, normalise=True)
     if name == "C5":
-        x, labels = _gauss_mixture(rng, n, w.d, comps, 1.0, 0.5)
-        return _normalise_rows(x), labels
+        return _gauss_mixture(rng, n, w.d, comps, 1.0, 0.5, seed=seed, normalise=True)
     raise KeyError(name)
 
 
