@@ -91,6 +91,7 @@ struct SearchParams {
     int uwords = 0;            // 32-bit words per bitmap
     long long n_points = 0;    // n (bitmap size in counting mode)
     int prefetch = 1;          // L1 prefetch of the next expansion's adjacency row
+    int prefetch_rows = 1;     // float data: L2 prefetch of every candidate row of an expansion (PK_PREFETCH_ROWS)
     int lazy = 1;              // float data: lazy keys (fp32 screen values until a decision needs the exact one)
     int seed_only = 0;         // profiling aid (PK_SEED_ONLY): stop after seeding
     int seed_select = 1;       // exact integer modes: seed by selection instead of merges (PK_SEED_SELECT)
@@ -870,6 +871,20 @@ struct WarpBeam {
         __syncwarp();
     }
 
+    // Ask L2 for every row of this batch of candidates at once (lane l takes
+    // 128-byte line l of each row).  The fp32 screens then read the rows two at
+    // a time -- all the registers allow -- and find them on their way from HBM
+    // instead of issuing one HBM round trip per pair.
+    __device__ void prefetch_rows(const SearchParams& P, unsigned cid, int cnt) {
+        const int lane = lane_id();
+        const int lines = (P.dp * 4 + 127) >> 7;
+        for (int j = 0; j < cnt; ++j) {
+            const unsigned id = __shfl_sync(PK_FULL, cid, j);
+            const char* r = reinterpret_cast<const char*>(P.X + (size_t)id * P.dp);
+            for (int l = lane; l < lines; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + ((size_t)l << 7)));
+        }
+    }
+
     // evaluate and merge the c candidates staged in cbuf
     template <class D>
     __device__ void flush(const SearchParams& P, const D& dist, int c) {
@@ -882,6 +897,7 @@ struct WarpBeam {
             count_unique(cid, cnt);
             if constexpr (has_screen<D>::value) {
                 if (lazy) {
+                    if (P.prefetch_rows && cnt > 2) prefetch_rows(P, cid, cnt);
                     insert_lazy<false>(P, dist, cid, cnt);
                     continue;
                 }

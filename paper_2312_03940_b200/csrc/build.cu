@@ -56,7 +56,7 @@ struct BuildArgs {
 // phase 1: one warp per inserted point searches the adjacency snapshot and
 // logs its visited set (_kernels.py:349-358)
 template <int MODE, int QV>
-__global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 6 : 8) : 8) build_search_kernel(BuildArgs A) {
+__global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 5 : 8) : 8) build_search_kernel(BuildArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
@@ -1419,6 +1419,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s};
     A.P.screen = D.screen;
     A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
+    A.P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && dp >= 512;  // measured: helps rows of 4 KB (C5), not 1.5 KB (C4)
     A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
     A.P.seed_select = env_int("PK_SEED_SELECT", 1);
     if (SH.seed_bd && SH.seed_bi && SH.seed_bl && SH.world == 1) {

@@ -11,7 +11,7 @@ namespace pk {
 
 // ---- beam kNN of member queries (_kernels.py:230-262) --------------------------------
 template <int MODE, int QV>
-__global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 6 : 8) : 8) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
+__global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 5 : 8) : 8) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
                                                        int L, int kk, int H, size_t warp_bytes,
                                                        long long* __restrict__ out_ids, double* __restrict__ out_d,
                                                        long long* __restrict__ counts, long long* evals_out,
@@ -622,6 +622,7 @@ extern "C" int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const u
     P.screen = env_int("PK_SCREEN", 1) == 1;
     P.n_points = n;
     P.prefetch = env_int("PK_PREFETCH", 1) == 1;
+    P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && dp >= 512;  // measured: helps rows of 4 KB (C5), not 1.5 KB (C4)
     P.lazy = env_int("PK_LAZY", 1) == 1 && n < (int64_t)PK_IDMASK;
     P.seed_only = env_int("PK_SEED_ONLY", 0);
     P.seed_select = env_int("PK_SEED_SELECT", 1);
