@@ -1419,7 +1419,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s};
     A.P.screen = D.screen;
     A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
-    A.P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && dp >= 512;  // measured: helps rows of 4 KB (C5), not 1.5 KB (C4)
+    A.P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && D.dp >= 512;  // measured: helps 4 KB rows (C5), not 1.5 KB (C4)
     A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
     A.P.seed_select = env_int("PK_SEED_SELECT", 1);
     if (SH.seed_bd && SH.seed_bi && SH.seed_bl && SH.world == 1) {
