@@ -571,8 +571,10 @@ def main_ours(args):
         e2e_stage_ms.append({k_: round(v * 1e3, 2) for k_, v in res.timings.items()})
         h2d = n * w.d * 4
         st = res.state
-        d2h = sum(a.nbytes for a in (st.rho, st.lam, st.delta, st.neighbors.ids, st.neighbors.dists,
-                                     res.clustering.labels, res.clustering.centers, res.clustering.noise))
+        arrays = [st.rho, st.lam, st.delta, res.clustering.labels, res.clustering.centers, res.clustering.noise]
+        if st.neighbors is not None:  # multi-GPU: the kNN rows are gathered to rank 0 only
+            arrays += [st.neighbors.ids, st.neighbors.dists]
+        d2h = sum(a.nbytes for a in arrays)
     del res
     t_e2e = torch.tensor([sum(e2e_steps_ms)], dtype=torch.float64, device="cuda")
     if world > 1:

@@ -235,6 +235,12 @@ int pk_densities(int kind, const int64_t* ids, const double* dists, int64_t n, i
  * (density.density_kth_normalized, density.py:48-55, 69-73). */
 int pk_normalize_rho(const double* base, const int64_t* ids, int64_t n, int64_t k, double* out, void* stream);
 
+/* pk_normalize_rho for the rows of points row0 .. row0 + m - 1 only (one rank's
+ * chunk of the kNN rows; base covers all n points): out[i] = base[row0 + i] * k
+ * / sum_j base[ids[i][j]] in numpy's summation order (density.py:48-55). */
+int pk_normalize_rho_rows(const double* base, const int64_t* ids, int64_t row0, int64_t m, int64_t k, double* out,
+                          void* stream);
+
 /* rank[i] in 1..n, higher = denser, ties by smaller id; *nan_flag (device
  * int) set when rho has a NaN.  Replaces density.rank_order (density.py:116-129). */
 int pk_rank_order(const double* rho, int64_t n, int64_t* rank, int* nan_flag, void* stream);

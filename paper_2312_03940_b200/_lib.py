@@ -55,6 +55,7 @@ SIGNATURES = {
     "pk_sqrt": [_P, _I, _P, _P],
     "pk_densities": [_i, _P, _P, _I, _I, _P, _P],
     "pk_normalize_rho": [_P, _P, _I, _I, _P, _P],
+    "pk_normalize_rho_rows": [_P, _P, _I, _I, _I, _P, _P],
     "pk_rank_order": [_P, _I, _P, _P, _P],
     "pk_resolve_lists": [_P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "pk_dp_scan": [_P, _I, _I, _P, _I, _i, _P, _P, _I, _P, _P, _P],

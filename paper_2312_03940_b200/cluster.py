@@ -370,25 +370,35 @@ def _sync():
 
 
 def _knn_all_device(index: KnnIndex, n: int, k: int, comm=None):
-    """knn_all on device; with `comm` each rank answers a contiguous chunk of
-    the queries and the (n, k) rows are all-gathered."""
+    """knn_all on device -> (ids_t, sqd_t, row0): every row on one GPU; with
+    `comm` only this rank's contiguous chunk of the query rows (starting at
+    point row0) -- the rows are never all-gathered."""
     import torch
 
     dev = _lib.device()
     if comm is None or comm.world == 1:
-        return index.knn_batch_device(torch.arange(n, dtype=torch.int64, device=dev), k)
+        ids, sqd = index.knn_batch_device(torch.arange(n, dtype=torch.int64, device=dev), k)
+        return ids, sqd, 0
     lo, hi = comm.my_range(n)
-    c = comm.chunk(n)
-    kk = max(0, min(k, n - 1))
-    ids = torch.full((comm.world * c, kk), -1, dtype=torch.int64, device=dev)
-    sqd = torch.full((comm.world * c, kk), float("inf"), dtype=torch.float64, device=dev)
-    if hi > lo:
-        li, ls = index.knn_batch_device(torch.arange(lo, hi, dtype=torch.int64, device=dev), k)
-        ids[lo:hi] = li
-        sqd[lo:hi] = ls
-    comm.all_gather_chunks(ids, c)
-    comm.all_gather_chunks(sqd, c)
-    return ids[:n], sqd[:n]
+    ids, sqd = index.knn_batch_device(torch.arange(lo, hi, dtype=torch.int64, device=dev), k)
+    return ids, sqd, lo
+
+
+def _densities_sharded(kind: str, ids_t, dists_t, row0: int, n: int, comm):
+    """rho of all n points from each rank's own rows: densities of the local
+    rows, then one all-gather of rho (kth_normalized: all-gather the raw kth
+    values, normalise the local rows against them, all-gather again)."""
+    from .density import densities_device
+
+    if kind == "kth_normalized":
+        base = comm.all_gather_rows(densities_device("kth", ids_t, dists_t), n)
+        import torch
+
+        m, k = ids_t.shape
+        rho = torch.empty(m, dtype=torch.float64, device=ids_t.device)
+        _lib.call("pk_normalize_rho_rows", base, ids_t.contiguous(), row0, m, k, rho, _lib.stream())
+        return comm.all_gather_rows(rho, n)
+    return comm.all_gather_rows(densities_device(kind, ids_t, dists_t), n)
 
 
 def run_pipeline_device(p: PointSet, index_config: IndexConfig, k: int, density_kind: str,
@@ -412,24 +422,40 @@ def run_pipeline_device(p: PointSet, index_config: IndexConfig, k: int, density_
     t1 = time.perf_counter()
     if k < 1:
         raise ValueError(f"k must be >= 1, got {k}")
-    ids_t, sqd_t = _knn_all_device(index, n, k, comm)
+    ids_t, sqd_t, row0 = _knn_all_device(index, n, k, comm)
     dists_t = sqrt_device(sqd_t)
-    check_neighborhoods(density_kind, p, Neighborhoods.on_device(ids_t, dists_t))
-    rho_t = densities_device(density_kind, ids_t, dists_t)
+    sharded = comm is not None and comm.world > 1
+    if sharded:
+        check_neighborhoods(density_kind, p, _RowsView(n, ids_t.shape[1]))
+        rho_t = _densities_sharded(density_kind, ids_t, dists_t, row0, n, comm)
+    else:
+        check_neighborhoods(density_kind, p, Neighborhoods.on_device(ids_t, dists_t))
+        rho_t = densities_device(density_kind, ids_t, dists_t)
     _sync()
     t2 = time.perf_counter()
-    lam_t, delta_t, rank_t = dependents_device(index, p, rho_t, ids_t, dists_t, doubling_params, trace, comm)
+    lam_t, delta_t, rank_t = dependents_device(index, p, rho_t, ids_t, dists_t, doubling_params, trace, comm,
+                                               row0=row0)
     _sync()
     t3 = time.perf_counter()
-    labels_t, c_t, n_t = _apply_policies_device(rho_t, lam_t, delta_t, ids_t, center_policy, noise_policy, rank_t)
+    # the local-center policy reads every kNN row: the only step that needs them all
+    rows_all = comm.all_gather_rows(ids_t, n) if sharded and isinstance(center_policy, LocalCenter) else ids_t
+    labels_t, c_t, n_t = _apply_policies_device(rho_t, lam_t, delta_t, rows_all, center_policy, noise_policy, rank_t)
     _sync()
     t4 = time.perf_counter()
     timings["index"] = t1 - t0
     timings["density"] = t2 - t1
     timings["dependent"] = t3 - t2
     timings["unionfind"] = t4 - t3
-    return dict(index=index, ids=ids_t, dists=dists_t, rho=rho_t, lam=lam_t, delta=delta_t, labels=labels_t,
-                centers=c_t, noise=n_t, timings=timings)
+    return dict(index=index, ids=ids_t, dists=dists_t, rows=(row0, row0 + ids_t.shape[0]), rho=rho_t, lam=lam_t,
+                delta=delta_t, labels=labels_t, centers=c_t, noise=n_t, timings=timings)
+
+
+class _RowsView:
+    """Shape-only stand-in for the full Neighborhoods in the argument checks of
+    a sharded run (each rank holds only its own rows)."""
+
+    def __init__(self, n, k):
+        self.n, self.k = n, k
 
 
 def run_pipeline(
@@ -443,13 +469,21 @@ def run_pipeline(
     comm=None,
 ) -> PipelineResult:
     """Index build, kNN, densities, dependent points, policies, union-find.
-    `comm` (shard.Comm) splits the work across one process per GPU; every
-    rank returns the full result."""
+    `comm` (shard.Comm) splits the work across one process per GPU; every rank
+    returns the full clustering, rho, lam and delta, and rank 0 also the full
+    (n, k) kNN rows (gathered to it alone; the other ranks' state carries
+    neighbors=None)."""
     out = run_pipeline_device(p, index_config, k, density_kind, center_policy, noise_policy, doubling_params,
                               comm=comm)
-    rho, lam, delta, ids, dists, labels, centers, noise = _to_host_many(
-        [out["rho"], out["lam"], out["delta"], out["ids"], out["dists"], out["labels"],
-         _ids_of_device(out["centers"]), _ids_of_device(out["noise"])])
-    state = DpcState(rho=rho, dependents=Dependents(lam, delta), neighbors=Neighborhoods(ids, dists))
+    ids_t, dists_t = out["ids"], out["dists"]
+    if comm is not None and comm.world > 1:
+        ids_t = comm.gather_rows_to_root(ids_t, p.n)
+        dists_t = comm.gather_rows_to_root(dists_t, p.n)
+    rows = [ids_t, dists_t] if ids_t is not None else []
+    got = _to_host_many([out["rho"], out["lam"], out["delta"], out["labels"], _ids_of_device(out["centers"]),
+                         _ids_of_device(out["noise"])] + rows)
+    rho, lam, delta, labels, centers, noise = got[:6]
+    nbrs = Neighborhoods(got[6], got[7]) if rows else None
+    state = DpcState(rho=rho, dependents=Dependents(lam, delta), neighbors=nbrs)
     clustering = Clustering(labels, centers, noise)
     return PipelineResult(clustering=clustering, state=state, timings=out["timings"])

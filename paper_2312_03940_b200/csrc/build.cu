@@ -1440,11 +1440,15 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     // (tc_knn.cu tc_seed_mask, beam.cuh seed_select_lazy)
     unsigned* seed_mask = nullptr;
     int* near = nullptr;
-    if (MODE == MODE_SEQ64 && D.screen && A.P.lazy && A.P.seed_select && !ubm && !multi && L >= 128 && s > L && n >= 4096 &&
+    // (replicated on every rank of a sharded build: the mask is per point and the
+    // same on every rank, so each rank's searches of its chunk use it unchanged)
+    if (MODE == MODE_SEQ64 && D.screen && A.P.lazy && A.P.seed_select && !ubm && L >= 128 && s > L && n >= 4096 &&
         s >= env_int("PK_SEED_TC_MIN", 256) && s <= 8192 && env_int("PK_SEED_TC", 1) == 1 && tc_supported()) {
         const int mw = (s + 31) / 32;
         PK_CHECK(scratch(&seed_mask, (size_t)n * mw, st));
-        if (env_int("PK_LOCALITY", 1) == 1) PK_CHECK(scratch(&near, (size_t)n, st));
+        // (one GPU only: ranks must agree on the chunk of every batch, and the order
+        // below is derived from floating-point screens)
+        if (env_int("PK_LOCALITY", 1) == 1 && !multi) PK_CHECK(scratch(&near, (size_t)n, st));
         if ((rc = tc_seed_mask(D.X, n, D.dp, starts, s, std::min(L, s), seed_mask, mw, near, st))) return rc;
         A.P.seed_mask = seed_mask;
         A.P.seed_mw = mw;
@@ -1463,7 +1467,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     // u8 rows of d = 128: the exact start distances of every point from one
     // integer tensor-core pass (beam.cuh seed_select reads them)
     unsigned* seed_tab = nullptr;
-    if (MODE == MODE_EXACT_U8 && D.dw == 32 && D.X8 && A.P.seed_select && !ubm && !multi && L >= 128 &&
+    if (MODE == MODE_EXACT_U8 && D.dw == 32 && D.X8 && A.P.seed_select && !ubm && L >= 128 &&
         (L & (L - 1)) == 0 && s > 32 && (long long)n * s <= (1ll << 31) && env_int("PK_SEED_TAB", 1) == 1) {
         PK_CHECK(scratch(&seed_tab, (size_t)n * s, st));
         if ((rc = u8_seed_table(D.X8, n, starts, s, seed_tab, st))) return rc;

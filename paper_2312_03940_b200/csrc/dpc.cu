@@ -91,13 +91,14 @@ __global__ void density_rows_kernel(int kind, const double* dists, long long n, 
 }
 
 // rho * k / sum(rho[neighbours]) with inf for zero / nan (density.py:48-55)
+// (rows i of this call are points row0 + i: a rank's own chunk of the kNN rows)
 __global__ void normalize_kernel(const double* base, const long long* ids, long long n, int k, double* out,
-                                 double* tmp) {
+                                 double* tmp, long long row0) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         double* t = tmp + i * k;
         for (int j = 0; j < k; ++j) t[j] = base[ids[i * k + j]];
         double den = np_pairwise_sum(t, k);
-        double v = base[i] * (double)k / den;
+        double v = base[row0 + i] * (double)k / den;
         if (den == 0.0 || isnan(v)) v = __longlong_as_double(0x7ff0000000000000LL);
         out[i] = v;
     }
@@ -328,7 +329,7 @@ extern "C" int pk_densities(int kind, const int64_t* ids, const double* dists, i
         }
         {
             ProfScope _ps("normalize_kernel", st);
-            normalize_kernel<<<g, 128, 0, st>>>(base, reinterpret_cast<const long long*>(ids), n, (int)k, rho, tmp);
+            normalize_kernel<<<g, 128, 0, st>>>(base, reinterpret_cast<const long long*>(ids), n, (int)k, rho, tmp, 0);
         }
         release(base, st);
     } else {
@@ -342,20 +343,25 @@ extern "C" int pk_densities(int kind, const int64_t* ids, const double* dists, i
     return 0;
 }
 
-extern "C" int pk_normalize_rho(const double* base, const int64_t* ids, int64_t n, int64_t k, double* out,
-                                void* stream) {
+extern "C" int pk_normalize_rho_rows(const double* base, const int64_t* ids, int64_t row0, int64_t m, int64_t k,
+                                     double* out, void* stream) {
     cudaStream_t st = as_stream(stream);
-    if (n <= 0) return 0;
+    if (m <= 0) return 0;
     double* tmp = nullptr;
-    PK_CHECK(scratch(&tmp, (size_t)n * k, st));
+    PK_CHECK(scratch(&tmp, (size_t)m * k, st));
     {
         ProfScope _ps("normalize_kernel", st);
-        normalize_kernel<<<grid_for(n, 128), 128, 0, st>>>(base, reinterpret_cast<const long long*>(ids), n, (int)k, out,
-                                                          tmp);
+        normalize_kernel<<<grid_for(m, 128), 128, 0, st>>>(base, reinterpret_cast<const long long*>(ids), m, (int)k, out,
+                                                          tmp, row0);
     }
     PK_CHECK_LAUNCH("normalize_kernel");
     release(tmp, st);
     return 0;
+}
+
+extern "C" int pk_normalize_rho(const double* base, const int64_t* ids, int64_t n, int64_t k, double* out,
+                                void* stream) {
+    return pk_normalize_rho_rows(base, ids, 0, n, k, out, stream);
 }
 
 extern "C" int pk_rank_order(const double* rho, int64_t n, int64_t* rank, int* nan_flag, void* stream) {

@@ -188,10 +188,12 @@ def _dp_scan_tc(p: PointSet, rank_t, q, m: int, sid, ssq):
 
 
 def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: DoublingParams, trace=None,
-                      comm=None):
+                      comm=None, row0: int = 0):
     """(lam_t, delta_t) on device; `trace` collects (unresolved, kq) per round.
-    With `comm` every doubling round and the final scan split the sorted
-    unresolved ids across the ranks (shard.py)."""
+    ids_t / dists_t are the kNN rows of points row0, row0 + 1, ... (all n on
+    one GPU).  With `comm` each rank resolves its own rows in phase 1, and
+    every doubling round and the final scan split the sorted unresolved ids
+    across the ranks (shard.py)."""
     import torch
 
     def mine(t):
@@ -214,10 +216,10 @@ def dependents_device(g: KnnIndex, p: PointSet, rho_t, ids_t, dists_t, params: D
     top_t = torch.zeros(1, dtype=torch.int64, device=dev)
     _lib.call("pk_argmax_rank", rank_t, n, top_t, _lib.stream())
     top = int(top_t.item())
-    all_t = torch.arange(n, dtype=torch.int64, device=dev)
-    todo, m, _, _ = _resolve(rank_t, all_t, ids_t, dists_t, lam_t, delta_t, top)
+    own_t = torch.arange(row0, row0 + ids_t.shape[0], dtype=torch.int64, device=dev)
+    todo, m, _, _ = _resolve(rank_t, own_t, ids_t, dists_t, lam_t, delta_t, top)
     if comm is not None:
-        todo = torch.sort(todo).values  # same order on every rank
+        todo, m = regroup(todo)  # every rank's phase-1 leftovers, sorted: the same list on every rank
     if n > 1:
         kdep = params.validated_against(ids_t.shape[1]).initial_k
         if not isinstance(g, BruteForceIndex):

@@ -9,16 +9,23 @@ exchange steps are the ones the reference algorithm has:
   (PK_XCHG_OUTLISTS).  The reverse-edge re-prunes of a batch are split by
   target (u % world) and the re-pruned rows are all-gathered (PK_XCHG_ROWS).
   Every rank ends with the same graph, identical to the single-GPU build.
-* kNN densities (cluster.py:299): queries cut into contiguous chunks, the
-  (n, k) rows all-gathered, densities computed replicated.
-* dependent points (dependent.py:96-133): phase 1 is replicated (a cheap
-  pass over resident lists); each doubling round and the final scan split the
-  (sorted) unresolved ids, and the per-round unresolved sets are all-gathered;
-  lam / delta are merged with one MAX / MIN all-reduce (each point is resolved
-  by exactly one rank; untouched entries hold -1 / +inf).
-* policies + union-find: replicated (O(n) passes).
+* kNN densities (cluster.py:299): queries cut into contiguous chunks; each
+  rank keeps its own (chunk, k) rows and computes their densities; only rho
+  is all-gathered (n x 8 B; kth_normalized all-gathers the raw kth values
+  first, then normalises its rows against them, then all-gathers again).
+* dependent points (dependent.py:96-133): phase 1 runs on each rank's own
+  rows; the unresolved ids are all-gathered (variable length) and every
+  doubling round and the final scan split the sorted set again; lam / delta
+  are merged with one MAX / MIN all-reduce (each point is resolved by exactly
+  one rank; untouched entries hold -1 / +inf).
+* policies + union-find: replicated on the identical rho / lam / delta (the
+  local-center policy, which reads the kNN rows, all-gathers them first).
+* the returned state: the (n, k) rows are gathered to rank 0 only.
 
-`Comm` wraps torch.distributed (NCCL on GPUs; gloo in the CPU tests).
+`Comm` wraps torch.distributed (NCCL on GPUs; gloo in the CPU tests).  The
+collectives are the same calls on both backends (all_gather_into_tensor,
+all_reduce, gather); with gloo, device tensors are staged through host
+copies (several ranks sharing one device in a functional test).
 """
 
 from __future__ import annotations
@@ -61,43 +68,42 @@ class Comm:
         return lo, min(m, lo + c)
 
     # ---- collectives
+    def _host_staged(self, t: torch.Tensor) -> bool:
+        """gloo cannot reduce / gather device tensors: stage them through the host."""
+        return self.backend != "nccl" and t.device.type != "cpu"
+
+    def _all_gather_tensor(self, out: torch.Tensor, send: torch.Tensor) -> None:
+        """dist.all_gather_into_tensor(out, send) on either backend."""
+        if self._host_staged(send):
+            ho = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_gather_into_tensor(ho, send.cpu(), group=self.group)
+            out.copy_(ho)
+        else:
+            dist.all_gather_into_tensor(out, send.contiguous(), group=self.group)
+
     def all_gather_chunks(self, buf: torch.Tensor, chunk: int) -> None:
         """In-place all-gather of equal chunks: rank r owns buf[r*chunk:(r+1)*chunk]
         (flat first dimension); afterwards every rank holds all world*chunk."""
         if self.world == 1 or chunk == 0:
             return
         full = buf[: self.world * chunk]
-        own = full[self.rank * chunk:(self.rank + 1) * chunk]
-        if self.backend == "nccl":
-            dist.all_gather_into_tensor(full, own, group=self.group)
-        else:  # gloo: host copies (CPU tests, or a functional check with several ranks on one device)
-            src = own.cpu()
-            parts = [torch.empty_like(src) for _ in range(self.world)]
-            dist.all_gather(parts, src, group=self.group)
-            for r, t in enumerate(parts):
-                if r != self.rank:
-                    full[r * chunk:(r + 1) * chunk].copy_(t)
+        own = full[self.rank * chunk:(self.rank + 1) * chunk].clone()
+        self._all_gather_tensor(full, own)
 
     def all_gather_into(self, out: torch.Tensor, send: torch.Tensor) -> None:
         """out[r*len(send):(r+1)*len(send)] = send of rank r."""
         if self.world == 1:
             out[: send.shape[0]].copy_(send)
             return
-        if self.backend == "nccl":
-            dist.all_gather_into_tensor(out[: self.world * send.shape[0]], send, group=self.group)
-        else:
-            src = send.cpu()
-            parts = [torch.empty_like(src) for _ in range(self.world)]
-            dist.all_gather(parts, src, group=self.group)
-            out[: self.world * send.shape[0]].copy_(torch.cat(parts))
+        self._all_gather_tensor(out[: self.world * send.shape[0]], send)
 
     def all_gather_counts(self, count: int, device) -> list[int]:
-        t = torch.tensor([count], dtype=torch.int64, device=device if self.backend == "nccl" else "cpu")
+        dev = device if self.backend == "nccl" else "cpu"
         if self.world == 1:
             return [count]
-        parts = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(parts, t, group=self.group)
-        return [int(x.item()) for x in parts]
+        out = torch.empty(self.world, dtype=torch.int64, device=dev)
+        self._all_gather_tensor(out, torch.tensor([count], dtype=torch.int64, device=dev))
+        return [int(x) for x in out.tolist()]
 
     def all_gather_varlen(self, t: torch.Tensor) -> torch.Tensor:
         """Concatenation over ranks (rank order) of tensors of different lengths."""
@@ -113,16 +119,43 @@ class Comm:
         self.all_gather_into(out, pad)
         return torch.cat([out[r * maxc:r * maxc + counts[r]] for r in range(self.world)])
 
+    def all_gather_rows(self, local: torch.Tensor, n: int) -> torch.Tensor:
+        """Rows [lo, hi) of every rank (my_range(n)) -> the full (n, ...) array."""
+        if self.world == 1:
+            return local
+        c = self.chunk(n)
+        pad = torch.empty((c,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        pad[: local.shape[0]] = local
+        out = torch.empty((self.world * c,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        self._all_gather_tensor(out, pad)
+        return out[:n]
+
+    def gather_rows_to_root(self, local: torch.Tensor, n: int, root: int = 0):
+        """Rows [lo, hi) of every rank -> the full (n, ...) array on `root`, None elsewhere."""
+        if self.world == 1:
+            return local
+        c = self.chunk(n)
+        pad = torch.empty((c,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        pad[: local.shape[0]] = local
+        staged = self._host_staged(pad)
+        send = pad.cpu() if staged else pad
+        parts = [torch.empty_like(send) for _ in range(self.world)] if self.rank == root else None
+        dist.gather(send, parts, dst=root, group=self.group)
+        if self.rank != root:
+            return None
+        full = torch.cat(parts)[:n]
+        return full.to(local.device) if staged else full
+
     def all_reduce(self, t: torch.Tensor, op: str) -> None:
         if self.world == 1:
             return
         rop = {"max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN, "sum": dist.ReduceOp.SUM}[op]
-        if self.backend == "nccl" or t.device.type == "cpu":
-            dist.all_reduce(t, op=rop, group=self.group)
-        else:
+        if self._host_staged(t):
             h = t.cpu()
             dist.all_reduce(h, op=rop, group=self.group)
             t.copy_(h)
+        else:
+            dist.all_reduce(t, op=rop, group=self.group)
 
     def max_time(self, ms: float, device) -> float:
         t = torch.tensor([ms], dtype=torch.float64, device=device)

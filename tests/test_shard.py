@@ -113,6 +113,53 @@ def test_collectives_gloo_world2():
     _run(2, _gathers)
 
 
+def _row_collectives(comm):
+    """all_gather_rows / gather_rows_to_root over the my_range split (the
+    sharded pipeline's rho exchange and the rank-0 gather of the kNN rows)."""
+    r = comm.rank
+    n = 7
+    lo, hi = comm.my_range(n)
+    local = torch.arange(lo * 3, hi * 3, dtype=torch.int64).view(-1, 3)
+    full = comm.all_gather_rows(local, n)
+    assert torch.equal(full, torch.arange(n * 3, dtype=torch.int64).view(n, 3))
+    rho = torch.arange(lo, hi, dtype=torch.float64) * 0.5
+    assert comm.all_gather_rows(rho, n).tolist() == [0.5 * i for i in range(n)]
+    root = comm.gather_rows_to_root(local, n)
+    if r == 0:
+        assert torch.equal(root, torch.arange(n * 3, dtype=torch.int64).view(n, 3))
+    else:
+        assert root is None
+    assert comm.all_gather_counts(r + 5, "cpu") == [5, 6]
+
+
+def test_row_collectives_gloo_world2():
+    _run(2, _row_collectives)
+
+
+def _sharded_density_rows(comm):
+    """kth_normalized from per-rank rows == the single-rank computation, with
+    the row offset of pk_normalize_rho_rows emulated by the host restatement
+    (rho_i = base_i * k / sum_j base[ids_ij]): the exchange pattern (gather raw
+    kth, normalise own rows, gather rho) on two ranks."""
+    import numpy as np
+
+    n, k = 9, 3
+    rng = np.random.default_rng(4)
+    ids = torch.from_numpy(rng.integers(0, n, (n, k)).astype(np.int64))
+    base_full = torch.from_numpy(rng.uniform(0.5, 2.0, n))
+    lo, hi = comm.my_range(n)
+    base = comm.all_gather_rows(base_full[lo:hi].clone(), n)
+    assert torch.equal(base, base_full)
+    own = base[lo:hi] * k / base[ids[lo:hi]].sum(1)
+    rho = comm.all_gather_rows(own, n)
+    want = base_full * k / base_full[ids].sum(1)
+    assert torch.allclose(rho, want, rtol=0, atol=0)
+
+
+def test_sharded_density_exchange_gloo_world2():
+    _run(2, _sharded_density_rows)
+
+
 def _build_exchange(comm):
     r, w = comm.rank, comm.world
     n, R = 50, 4
@@ -197,8 +244,12 @@ def _pipeline_digest(comm):
     kw = workloads.pipeline_args("C1", pk, n_centers=10)
     out = run_pipeline_device(pk.PointSet(data), **kw, comm=comm)
     adj, deg = out["index"].graph.device_arrays()[:2]
+    ids, dists = out["ids"], out["dists"]
+    if comm is not None:  # each rank holds only its own rows
+        assert out["rows"] == comm.my_range(data.shape[0])
+        ids, dists = comm.all_gather_rows(ids, data.shape[0]), comm.all_gather_rows(dists, data.shape[0])
     h = {}
-    for name, t in (("adj", adj), ("deg", deg), ("ids", out["ids"]), ("dists", out["dists"]), ("rho", out["rho"]),
+    for name, t in (("adj", adj), ("deg", deg), ("ids", ids), ("dists", dists), ("rho", out["rho"]),
                     ("lam", out["lam"]), ("delta", out["delta"]), ("labels", out["labels"])):
         h[name] = hashlib.sha256(t.detach().cpu().numpy().tobytes()).hexdigest()
     return h
