@@ -190,6 +190,12 @@ int pk_pcg64_permutation(const uint64_t* state, int has_uint32, uint32_t uintege
 int pk_parse_pecg(const uint32_t* words, int64_t nwords, int64_t n, int64_t R, int32_t* adj, int32_t* deg,
                   int64_t* info);
 
+/* Diagnostics: the beam walk's per-phase clock64 cycle sums (expand, row
+ * prefetch, fp32 screens, resolve, merge, emit, seeding); zeros unless the
+ * library was compiled with -DPK_PHASE_TIMERS (tools/variant.sh). */
+int pk_phase_timers(unsigned long long* out8, int reset);
+int pk_phase_timers_build(unsigned long long* out8, int reset);
+
 /* Host helper: index of the first non-finite value of x[0, count) in
  * row-major order (-1 if none) -> *first_bad; all host threads scan.  The
  * PointSet finiteness check (core.py:17-54). */

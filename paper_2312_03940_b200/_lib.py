@@ -49,6 +49,8 @@ SIGNATURES = {
     "pk_pcg64_permutation": [_P, _i, ctypes.c_uint32, _I, _P, _P],
     "pk_find_nonfinite": [_P, _I, _P],
     "pk_parse_pecg": [_P, _I, _I, _I, _P, _P, _P],
+    "pk_phase_timers": [_P, _i],
+    "pk_phase_timers_build": [_P, _i],
     "pk_scan_points": [_P, _I, _I, _I, _P, _P],
     "pk_robust_prune": [_P, _I, _I, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P],
     "pk_nearest_to_centroid": [_P, _I, _I, _P, _P],

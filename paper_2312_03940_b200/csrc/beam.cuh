@@ -489,10 +489,14 @@ struct WarpBeam {
     template <bool CheckDups, class D>
     __device__ void insert_lazy(const SearchParams& P, const D& dist, unsigned cid, int cnt) {
         unsigned cidf;
+        PK_PT_BEGIN
         double v = approx(P, dist, cid, cnt, cidf);
+        PK_PT_NEXT(2);
         bool valid = lane_id() < cnt;
         resolve(P, dist, v, cidf, valid);
+        PK_PT_NEXT(3);
         merge<CheckDups>(v, cidf, valid);
+        PK_PT_END(4);
     }
 
     // build: exact distances for the visit-log entries logged with lazy keys
@@ -776,6 +780,7 @@ struct WarpBeam {
     __device__ void walk(const SearchParams& P, const D& dist) {
         const int lane = lane_id();
         for (;;) {
+            PK_PT_BEGIN
             const int pos = next_unvisited();
             if (pos < 0) break;
             const unsigned pf = sm.bi[pos] & PK_IDAPX;
@@ -833,6 +838,7 @@ struct WarpBeam {
                 c += nb;
             }
             __syncwarp();
+            PK_PT_END(0);
             flush(P, dist, c);
         }
     }
@@ -897,7 +903,9 @@ struct WarpBeam {
             count_unique(cid, cnt);
             if constexpr (has_screen<D>::value) {
                 if (lazy) {
+                    PK_PT_BEGIN
                     if (P.prefetch_rows && cnt > 2) prefetch_rows(P, cid, cnt);
+                    PK_PT_END(1);
                     insert_lazy<false>(P, dist, cid, cnt);
                     continue;
                 }

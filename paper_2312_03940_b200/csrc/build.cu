@@ -72,8 +72,12 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         wb.init(sm, A.L, A.vlog_i + (size_t)t * A.vcap, A.vlog_d + (size_t)t * A.vcap, A.vcap, A.err);
         wb.qid = p;
         wb.begin_counting(A.P.ubm ? A.P.ubm + ((size_t)blockIdx.x * wpb + wib) * A.P.uwords : nullptr, A.P.uwords);
-        wb.seed(A.P, dist, false, uniq);
-        if (A.P.seed_save) wb.save_seed(A.P, p);
+        {
+            PK_PT_BEGIN
+            wb.seed(A.P, dist, false, uniq);
+            if (A.P.seed_save) wb.save_seed(A.P, p);
+            PK_PT_END(6);
+        }
         wb.walk(A.P, dist);
         if constexpr (has_screen<decltype(dist)>::value)
             if (wb.lazy) wb.finalize_log(A.P, dist);
@@ -1822,5 +1826,21 @@ extern "C" int pk_nearest_to_centroid(const float* x, int64_t n, int64_t dp, int
     release(cen, st);
     release(bd, st);
     release(bi, st);
+    return 0;
+}
+
+// Diagnostics: the build searches' phase timers (see pk_phase_timers).
+extern "C" int pk_phase_timers_build(unsigned long long* out8, int reset) {
+#ifdef PK_PHASE_TIMERS
+    PK_CHECK(cudaDeviceSynchronize());
+    PK_CHECK(cudaMemcpyFromSymbol(out8, pk_phase_cycles, sizeof(unsigned long long) * 8));
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        PK_CHECK(cudaMemcpyToSymbol(pk_phase_cycles, z, sizeof z));
+    }
+#else
+    (void)reset;
+    for (int i = 0; i < 8; ++i) out8[i] = 0;
+#endif
     return 0;
 }

@@ -20,6 +20,31 @@
 #define PK_IDMASK 0x1fffffffu
 #define PK_IDAPX 0x7fffffffu // id + lazy-key flags (visit-log entries)
 
+// Phase timers of the beam walk (diagnostics build only: nvcc -DPK_PHASE_TIMERS;
+// tools/variant.sh): clock64 cycles per phase summed over warps (lane 0) into
+// pk_phase_cycles[] -- 0 expand (next entry, adjacency row, seen filter),
+// 1 row prefetch, 2 fp32 screens, 3 resolve, 4 merge, 5 emit, 6 seeding.
+// One copy per translation unit (no relocatable device code): knn.cu's holds
+// the query walks (pk_phase_timers), build.cu's the build searches
+// (pk_phase_timers_build).
+#ifdef PK_PHASE_TIMERS
+static __device__ unsigned long long pk_phase_cycles[8];
+#define PK_PT_BEGIN long long _pt0 = clock64();
+#define PK_PT_END(ph)                                                                             \
+    do {                                                                                          \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&pk_phase_cycles[ph], (unsigned long long)(clock64() - _pt0)); \
+    } while (0)
+#define PK_PT_NEXT(ph) \
+    do {               \
+        PK_PT_END(ph); \
+        _pt0 = clock64(); \
+    } while (0)
+#else
+#define PK_PT_BEGIN
+#define PK_PT_END(ph) do { } while (0)
+#define PK_PT_NEXT(ph) do { } while (0)
+#endif
+
 namespace pk {
 
 constexpr int kWarp = 32;

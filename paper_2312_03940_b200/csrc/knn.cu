@@ -33,13 +33,18 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, L, nullptr, nullptr, 0, nullptr);
         wb.begin_counting(P.ubm ? P.ubm + ((size_t)blockIdx.x * wpb + wib) * P.uwords : nullptr, P.uwords);
-        if (P.seed_load) wb.load_seed(P, dist, qi);
-        else wb.seed(P, dist, false, uniq);
+        {
+            PK_PT_BEGIN
+            if (P.seed_load) wb.load_seed(P, dist, qi);
+            else wb.seed(P, dist, false, uniq);
+            PK_PT_END(6);
+        }
         if (!P.seed_only) wb.walk(P, dist);
         un += wb.uniq;
         long long* oi = out_ids + (size_t)t * kk;
         double* od = out_d + (size_t)t * kk;
         int got;
+        PK_PT_BEGIN
         if constexpr (has_screen<decltype(dist)>::value)
             got = wb.emit(qi, kk, oi, od, [&](unsigned id) { return dist.eval_one(P.X, (int)id); });
         else
@@ -49,6 +54,7 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
             od[x] = __longlong_as_double(0x7ff0000000000000LL);
         }
         if (lane == 0) counts[t] = got;
+        PK_PT_END(5);
         ev += wb.evals;
         ex += wb.vl;
         __syncwarp();
@@ -752,5 +758,22 @@ extern "C" int pk_sqrt(const double* sqd, int64_t count, double* out, void* stre
         sqrt_kernel<<<grid_for(count, 256), 256, 0, st>>>(sqd, count, out);
     }
     PK_CHECK_LAUNCH("sqrt_kernel");
+    return 0;
+}
+
+// Diagnostics: read (and with reset != 0 clear) the query walks' phase timers;
+// all zero unless the library was built with -DPK_PHASE_TIMERS.
+extern "C" int pk_phase_timers(unsigned long long* out8, int reset) {
+#ifdef PK_PHASE_TIMERS
+    PK_CHECK(cudaDeviceSynchronize());
+    PK_CHECK(cudaMemcpyFromSymbol(out8, pk_phase_cycles, sizeof(unsigned long long) * 8));
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        PK_CHECK(cudaMemcpyToSymbol(pk_phase_cycles, z, sizeof z));
+    }
+#else
+    (void)reset;
+    for (int i = 0; i < 8; ++i) out8[i] = 0;
+#endif
     return 0;
 }
