@@ -65,6 +65,13 @@ inline size_t cand_smem_bytes(int cap, int dw, int S, bool u8) {
 
 int choose_hash(int L, int hash_bits, long long n);
 
+// n-bit device bitmap of the start ids (SearchParams::start_bm), only with
+// PK_START_SKIP=1: exact, and it halves the C5 build's re-evaluations (4.3 ->
+// 2.1 %), but the dependent bitmap load per neighbour costs more time than the
+// evaluations it saves (measured, tools/count_probe.py + tools/ab_env.py).
+// Caller releases it.
+cudaError_t start_bitmap(const int* starts, int s, long long n, unsigned** out, cudaStream_t st);
+
 // integer tuning knob from the environment (default when unset / invalid)
 inline int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);

@@ -92,6 +92,8 @@ struct SearchParams {
     long long n_points = 0;    // n (bitmap size in counting mode)
     int prefetch = 1;          // L1 prefetch of the next expansion's adjacency row
     int prefetch_rows = 1;     // float data: L2 prefetch of every candidate row of an expansion (PK_PREFETCH_ROWS)
+    int spec_rows = 0;         // float data: L2 requests for the predicted next expansion's rows (PK_SPEC_ROWS)
+    const unsigned* start_bm = nullptr;  // n-bit bitmap of the start ids: skipped in the walk (PK_START_SKIP)
     int lazy = 1;              // float data: lazy keys (fp32 screen values until a decision needs the exact one)
     int seed_only = 0;         // profiling aid (PK_SEED_ONLY): stop after seeding
     int seed_select = 1;       // exact integer modes: seed by selection instead of merges (PK_SEED_SELECT)
@@ -140,6 +142,7 @@ struct WarpBeam {
     long long uniq;   // distinct ids evaluated (the roofline's U)
     bool lazy;        // lazy keys (float data, set by seed())
     long long exact;  // exact float64 evaluations in lazy mode (lane 0 count)
+    unsigned spec_id; // node whose neighbours' rows were requested speculatively (insert_lazy)
 
     __device__ void init(const BeamSmem& s_, int L_, unsigned* vi, double* vd, int vcap_, unsigned* err_) {
         sm = s_;
@@ -158,6 +161,7 @@ struct WarpBeam {
         uniq = 0;
         lazy = false;
         exact = 0;
+        spec_id = 0xffffffffu;
         unsigned* h32 = reinterpret_cast<unsigned*>(sm.hash);
         for (unsigned h = lane_id(); h <= sm.hmask / 2; h += 32) h32[h] = 0xffffffffu;
         __syncwarp();
@@ -485,18 +489,87 @@ struct WarpBeam {
         }
     }
 
-    // lazy-mode batch insert: approx -> resolve -> merge
+    // lazy-mode batch insert: approx -> resolve -> merge.  `spec` (the last
+    // group of an expansion, P.spec_rows): once the screens are known, the next
+    // expansion is predicted (the better of the next unvisited beam entry and
+    // the best new candidate that beats the beam's worst key), its adjacency
+    // row is loaded while resolve() runs, and its unseen neighbours' rows are
+    // requested from L2 before the merge -- the next expansion's screens then
+    // find them on their way from HBM.  A wrong guess only costs bandwidth.
     template <bool CheckDups, class D>
-    __device__ void insert_lazy(const SearchParams& P, const D& dist, unsigned cid, int cnt) {
+    __device__ void insert_lazy(const SearchParams& P, const D& dist, unsigned cid, int cnt, bool spec = false) {
         unsigned cidf;
         PK_PT_BEGIN
         double v = approx(P, dist, cid, cnt, cidf);
         PK_PT_NEXT(2);
+        unsigned pn = 0xffffffffu;
+        int sa = -1, sb = -1, snd = 0;
+        if (spec) {
+            pn = predict_next(v, cid, cnt);
+            if (pn != 0xffffffffu) {
+                const int* row = P.adj + (size_t)pn * P.R;
+                const int lane = lane_id();
+                sa = lane < P.R ? __ldg(row + lane) : -1;
+                sb = lane + 32 < P.R ? __ldg(row + lane + 32) : -1;
+                snd = __ldg(P.deg + pn);
+            }
+        }
         bool valid = lane_id() < cnt;
         resolve(P, dist, v, cidf, valid);
         PK_PT_NEXT(3);
+        if (pn != 0xffffffffu && P.spec_rows == 1) {
+            prefetch_unseen(P, sa, sb, snd);
+            spec_id = pn;
+        }
+        PK_PT_NEXT(1);
         merge<CheckDups>(v, cidf, valid);
-        PK_PT_END(4);
+        PK_PT_NEXT(4);
+        if (pn != 0xffffffffu && P.spec_rows == 2) {
+            prefetch_unseen(P, sa, sb, snd);
+            spec_id = pn;
+        }
+        PK_PT_END(1);
+    }
+
+    // the node the next expansion will most likely take (see insert_lazy)
+    __device__ unsigned predict_next(double v, unsigned cid, int cnt) {
+        const int lane = lane_id();
+        const int nu = next_unvisited();
+        const double inf = __longlong_as_double(0x7ff0000000000000LL);
+        const double bk = nu >= 0 ? sm.bd[nu] : inf;
+        const double lim = bl == L ? sm.bd[L - 1] : inf;
+        const double cv = lane < cnt ? v : inf;
+        double m = cv;
+#pragma unroll
+        for (int s = 16; s; s >>= 1) m = fmin(m, __shfl_xor_sync(PK_FULL, m, s));
+        if (m < bk && m < lim) {
+            const int src = __ffs(__ballot_sync(PK_FULL, cv == m)) - 1;
+            return __shfl_sync(PK_FULL, cid, src);
+        }
+        return nu >= 0 ? (sm.bi[nu] & PK_IDMASK) : 0xffffffffu;
+    }
+
+    // L2 requests for the rows of a predicted expansion's neighbours that the
+    // seen table does not hold (lane l: row slots l and l + 32, every line)
+    __device__ void prefetch_unseen(const SearchParams& P, int sa, int sb, int snd) {
+        const int lane = lane_id();
+        auto is_start = [&](int w) { return P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u); };
+        const bool ga = lane < snd && sa >= 0 && !seen_probe(sm.hash, sm.hmask, sm.hbits, (unsigned)sa) && !is_start(sa);
+        const bool gb = lane + 32 < snd && sb >= 0 && !seen_probe(sm.hash, sm.hmask, sm.hbits, (unsigned)sb) && !is_start(sb);
+        const unsigned ba = __ballot_sync(PK_FULL, ga), bb = __ballot_sync(PK_FULL, gb);
+        if (!(ba | bb)) return;
+        // row by row (lane l takes line l): a row's lines go out back to back
+        const int lines = (P.dp * 4 + 127) >> 7;
+        for (unsigned b = ba; b; b &= b - 1) {
+            const unsigned id = (unsigned)__shfl_sync(PK_FULL, sa, __ffs(b) - 1);
+            const char* r = reinterpret_cast<const char*>(P.X + (size_t)id * P.dp);
+            for (int l = lane; l < lines; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + ((size_t)l << 7)));
+        }
+        for (unsigned b = bb; b; b &= b - 1) {
+            const unsigned id = (unsigned)__shfl_sync(PK_FULL, sb, __ffs(b) - 1);
+            const char* r = reinterpret_cast<const char*>(P.X + (size_t)id * P.dp);
+            for (int l = lane; l < lines; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + ((size_t)l << 7)));
+        }
     }
 
     // build: exact distances for the visit-log entries logged with lazy keys
@@ -827,6 +900,8 @@ struct WarpBeam {
             for (int e0 = 0; e0 < nd; e0 += 32) {
                 int w = e0 + lane < nd ? (e0 == 0 ? w_a : e0 == 32 ? w_b : __ldg(row + e0 + lane)) : -1;
                 bool cand = w >= 0;
+                // a start was merged at seeding: it is in the beam or can never re-enter it
+                if (cand && P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u)) cand = false;
                 if (cand && seen_or_insert(sm.hash, sm.hmask, sm.hbits, (unsigned)w)) cand = false;
                 unsigned b = __ballot_sync(PK_FULL, cand);
                 const int nb = __popc(b);
@@ -839,7 +914,12 @@ struct WarpBeam {
             }
             __syncwarp();
             PK_PT_END(0);
-            flush(P, dist, c);
+            const bool hit = spec_id == p;  // this expansion's rows were requested during the last merge
+#ifdef PK_PHASE_TIMERS
+            if (lane == 0 && spec_id != 0xffffffffu) atomicAdd(&pk_phase_cycles[7], hit ? (1ull << 32) + 1ull : 1ull);
+#endif
+            spec_id = 0xffffffffu;
+            flush(P, dist, c, hit);
         }
     }
 
@@ -893,7 +973,7 @@ struct WarpBeam {
 
     // evaluate and merge the c candidates staged in cbuf
     template <class D>
-    __device__ void flush(const SearchParams& P, const D& dist, int c) {
+    __device__ void flush(const SearchParams& P, const D& dist, int c, bool spec_hit = false) {
         const int lane = lane_id();
         __syncwarp();
         for (int g = 0; g < c; g += 32) {
@@ -904,9 +984,9 @@ struct WarpBeam {
             if constexpr (has_screen<D>::value) {
                 if (lazy) {
                     PK_PT_BEGIN
-                    if (P.prefetch_rows && cnt > 2) prefetch_rows(P, cid, cnt);
+                    if (P.prefetch_rows && cnt > 2 && !spec_hit) prefetch_rows(P, cid, cnt);
                     PK_PT_END(1);
-                    insert_lazy<false>(P, dist, cid, cnt);
+                    insert_lazy<false>(P, dist, cid, cnt, P.spec_rows && g + 32 >= c);
                     continue;
                 }
             }

@@ -1424,6 +1424,10 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.P.screen = D.screen;
     A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     A.P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && D.dp >= 512;  // measured: helps 4 KB rows (C5), not 1.5 KB (C4)
+    A.P.spec_rows = env_int("PK_SPEC_ROWS", 0);
+    unsigned* sbm = nullptr;  // start ids re-met as neighbours are skipped (see pk_beam_knn_seeded)
+    PK_CHECK(start_bitmap(starts, s, n, &sbm, st));
+    A.P.start_bm = sbm;
     A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
     A.P.seed_select = env_int("PK_SEED_SELECT", 1);
     if (SH.seed_bd && SH.seed_bi && SH.seed_bl && SH.world == 1) {
@@ -1671,7 +1675,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
                     (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)adjd, (void*)new_d,
-                    (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, cub_tmp})
+                    (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, (void*)sbm, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

@@ -103,6 +103,15 @@ __device__ __forceinline__ bool seen_or_insert(unsigned short* hash, unsigned ma
     return false;
 }
 
+// read-only probe of the seen table (speculative row requests)
+__device__ __forceinline__ bool seen_probe(const unsigned short* hash, unsigned mask, int hbits, unsigned id) {
+    const unsigned set = id & (mask >> 2);
+    const unsigned tag = id >> (hbits - 2);
+    const uint2 v = reinterpret_cast<const uint2*>(hash)[set];
+    const unsigned t2 = tag | (tag << 16);
+    return (__vcmpeq2(v.x, t2) | __vcmpeq2(v.y, t2)) != 0u;
+}
+
 // ---- distance policies ---------------------------------------------------------
 //
 // Both policies return, for lane i < c, the squared distance between the query

@@ -330,6 +330,23 @@ __global__ void start_bitmap_kernel(const int* starts, int s, unsigned* bm) {
         atomicOr(bm + (starts[x] >> 5), 1u << (starts[x] & 31));
 }
 
+int grid_for(long long work, int block);
+
+cudaError_t start_bitmap(const int* starts, int s, long long n, unsigned** out, cudaStream_t st) {
+    *out = nullptr;
+    if (env_int("PK_START_SKIP", 0) != 1 || s <= 0) return cudaSuccess;
+    const size_t words = (size_t)((n + 31) / 32);
+    cudaError_t e = scratch(out, words, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(*out, 0, words * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    {
+        ProfScope _ps("start_bitmap_kernel", st);
+        start_bitmap_kernel<<<grid_for(s, 256), 256, 0, st>>>(starts, s, *out);
+    }
+    return cudaGetLastError();
+}
+
 int grid_for(long long work, int block) {
     long long g = (work + block - 1) / block;
     long long cap = (long long)sm_count() * 16;
@@ -621,14 +638,12 @@ extern "C" int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const u
         set_error("too many points for the beam kernels (ids are 30-bit)");
         return 2;
     }
-    // Start points re-met as neighbours are simply re-evaluated (and dropped
-    // by the key-equality check when already in the beam): cheaper than a
-    // dependent bitmap load on every neighbour.
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, x8, (int)dw};
     P.screen = env_int("PK_SCREEN", 1) == 1;
     P.n_points = n;
     P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && dp >= 512;  // measured: helps rows of 4 KB (C5), not 1.5 KB (C4)
+    P.spec_rows = env_int("PK_SPEC_ROWS", 0);
     P.lazy = env_int("PK_LAZY", 1) == 1 && n < (int64_t)PK_IDMASK;
     P.seed_only = env_int("PK_SEED_ONLY", 0);
     P.seed_select = env_int("PK_SEED_SELECT", 1);
@@ -649,11 +664,17 @@ extern "C" int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const u
         set_error("u8 mode needs the packed rows");
         return 2;
     }
+    // every start was merged into the seeded beam: one re-met as a neighbour is
+    // either in the beam or above its L-th key, which never increases -- skip it
+    unsigned* sbm = nullptr;
+    PK_CHECK(start_bitmap(starts, (int)s, n, &sbm, st));
+    P.start_bm = sbm;
     int rc = mode == MODE_EXACT_U8
                  ? dispatch_beam_knn<MODE_EXACT_U8>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st)
              : mode == MODE_EXACT32
                  ? dispatch_beam_knn<MODE_EXACT32>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st)
                  : dispatch_beam_knn<MODE_SEQ64>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st);
+    release(sbm, st);
     if (rc) return rc;
     if (brute_fallback) {
         int* list = nullptr;

@@ -24,6 +24,11 @@ def read(reset=True, fn="pk_phase_timers"):
 
 
 def show(tag, v):
+    spec = int(v[7])
+    v = v.copy()
+    v[7] = 0
+    if spec:
+        print(tag, f"speculative row requests: {spec & 0xffffffff} predictions, {spec >> 32} hits")
     tot = v.sum()
     if tot == 0:
         print(tag, "no timers (library built without -DPK_PHASE_TIMERS)")
