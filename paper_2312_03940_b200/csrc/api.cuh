@@ -52,6 +52,12 @@ inline size_t beam_smem_bytes(int L, int H) {
 // a global slab of spill_slab_bytes(L) per warp for the beam itself
 inline size_t spill_smem_bytes(int H) { return (((size_t)H * 2 + 15) & ~(size_t)15) + 128 + 4 * 64; }
 inline size_t spill_slab_bytes(int L) { return ((size_t)L * 12 + 15) & ~(size_t)15; }
+// row ring behind the beam state (carve_ring): slots x dp floats + one mbarrier per slot
+inline size_t ring_smem_bytes(int dp, int slots) { return slots ? (size_t)slots * dp * 4 + (size_t)slots * 8 : 0; }
+// slots of the row ring for a float search with lazy keys (PK_RING, default 2,
+// a power of two; 0 = rows through registers): rows of >= 1 KB that the fp32
+// screen covers
+inline int ring_slots(int dp, int qv, bool lazy_screen);
 inline size_t sort_smem_bytes(int cap) {
     return (size_t)cap * 13 + 128;
 }
@@ -65,13 +71,6 @@ inline size_t cand_smem_bytes(int cap, int dw, int S, bool u8) {
 
 int choose_hash(int L, int hash_bits, long long n);
 
-// n-bit device bitmap of the start ids (SearchParams::start_bm), only with
-// PK_START_SKIP=1: exact, and it halves the C5 build's re-evaluations (4.3 ->
-// 2.1 %), but the dependent bitmap load per neighbour costs more time than the
-// evaluations it saves (measured, tools/count_probe.py + tools/ab_env.py).
-// Caller releases it.
-cudaError_t start_bitmap(const int* starts, int s, long long n, unsigned** out, cudaStream_t st);
-
 // integer tuning knob from the environment (default when unset / invalid)
 inline int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -79,6 +78,15 @@ inline int env_int(const char* name, int dflt) {
     char* end = nullptr;
     const long x = std::strtol(v, &end, 10);
     return (end && *end == 0 && x >= 0) ? (int)x : dflt;  // "0" switches a default-on knob off
+}
+
+inline int ring_slots(int dp, int qv, bool lazy_screen) {
+    if (!lazy_screen || dp < 256 || dp > 128 * qv) return 0;
+    int s = env_int("PK_RING", 2);
+    if (s <= 0) return 0;
+    if (s > 8) s = 8;
+    while (s & (s - 1)) s &= s - 1;  // power of two
+    return s;
 }
 
 // ---- launch accounting -------------------------------------------------------

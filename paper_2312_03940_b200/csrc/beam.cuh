@@ -37,6 +37,10 @@ struct BeamSmem {
     int hbits;
     int* spos;        // [32] scratch: sorted insert positions
     unsigned* cbuf;   // [kCbuf] scratch: compacted candidate ids
+    // row ring (float data, lazy keys): candidate rows staged by bulk copies
+    float4* ring = nullptr;            // [ring_s][dp / 4]
+    unsigned long long* bars = nullptr;  // [ring_s] mbarriers, one per slot
+    int ring_s = 0;                    // slots (a power of two), 0 = no ring
 };
 
 constexpr int kCbuf = 64;  // compacted-candidate buffer (ids) per warp
@@ -76,6 +80,42 @@ __device__ __forceinline__ BeamSmem carve_beam_spill(unsigned char* base, unsign
     return s;
 }
 
+// Row ring behind a warp's beam state (host: ring_smem_bytes in api.cuh):
+// rows[ring_s][dp] f32 | bars[ring_s] u64, at `base` (16-byte aligned).  The
+// fp32 screens of the lazy-key searches read whole candidate rows; a warp that
+// loads them through registers gets one 4 KB row per ~1.1 us whatever it keeps
+// in flight (tools/gather_probe2.cu), the bulk-copy engine delivers the same
+// rows into shared memory 2-3 times faster and needs no registers for the rows
+// in flight.  Lane 0 initialises the barriers once per kernel.
+// Seen table in a per-warp global slab (L2-resident: 8 KB per warp), beam and
+// scratch in shared memory: frees the shared memory the row ring needs without
+// giving up resident warps.  One L2 round trip per expansion instead of a
+// shared-memory one; the table is only ever touched by its own warp.
+// smem layout: bd[L] | bi[L] | spos[32] | cbuf[kCbuf]  (host: beam_smem_bytes(L, 0))
+__device__ __forceinline__ BeamSmem carve_beam_gh(unsigned char* base, unsigned char* slab, int L, int H) {
+    BeamSmem s = carve_beam(base, L, 0);
+    s.hash = reinterpret_cast<unsigned short*>(slab);
+    s.hmask = (unsigned)H - 1u;
+    s.hbits = __ffs(H) - 1;
+    return s;
+}
+
+__device__ __forceinline__ size_t ring_smem_bytes_dev(int dp, int slots) {
+    return ((size_t)slots * dp * 4 + (size_t)slots * 8 + 15) & ~(size_t)15;
+}
+__device__ __forceinline__ void carve_ring(BeamSmem& s, unsigned char* base, int dp, int slots) {
+    s.ring_s = slots;
+    if (!slots) return;
+    s.ring = reinterpret_cast<float4*>(base);
+    s.bars = reinterpret_cast<unsigned long long*>(base + (size_t)slots * dp * 4);
+    if (lane_id() == 0) {
+        for (int i = 0; i < slots; ++i) mbar_init(s.bars + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+}
+
 struct SearchParams {
     const float* X;          // (n, dp)
     int dp;
@@ -92,8 +132,9 @@ struct SearchParams {
     long long n_points = 0;    // n (bitmap size in counting mode)
     int prefetch = 1;          // L1 prefetch of the next expansion's adjacency row
     int prefetch_rows = 1;     // float data: L2 prefetch of every candidate row of an expansion (PK_PREFETCH_ROWS)
-    int spec_rows = 0;         // float data: L2 requests for the predicted next expansion's rows (PK_SPEC_ROWS)
-    const unsigned* start_bm = nullptr;  // n-bit bitmap of the start ids: skipped in the walk (PK_START_SKIP)
+    int ring = 0;              // float data, lazy keys: slots of the per-warp row ring (0 = rows through registers)
+    unsigned char* ghash = nullptr;  // seen tables in global memory (carve_beam_gh): [warps][ghash_stride]
+    size_t ghash_stride = 0;
     int lazy = 1;              // float data: lazy keys (fp32 screen values until a decision needs the exact one)
     int seed_only = 0;         // profiling aid (PK_SEED_ONLY): stop after seeding
     int seed_select = 1;       // exact integer modes: seed by selection instead of merges (PK_SEED_SELECT)
@@ -140,9 +181,9 @@ struct WarpBeam {
     unsigned qid = 0xffffffffu;  // member query id where known (build searches)
     unsigned* ubm;    // counting mode only: this warp's bitmap of evaluated ids
     long long uniq;   // distinct ids evaluated (the roofline's U)
+    unsigned rt = 0;  // row ring: rows consumed so far by this warp (slot and barrier phase; survives init())
     bool lazy;        // lazy keys (float data, set by seed())
     long long exact;  // exact float64 evaluations in lazy mode (lane 0 count)
-    unsigned spec_id; // node whose neighbours' rows were requested speculatively (insert_lazy)
 
     __device__ void init(const BeamSmem& s_, int L_, unsigned* vi, double* vd, int vcap_, unsigned* err_) {
         sm = s_;
@@ -161,7 +202,6 @@ struct WarpBeam {
         uniq = 0;
         lazy = false;
         exact = 0;
-        spec_id = 0xffffffffu;
         unsigned* h32 = reinterpret_cast<unsigned*>(sm.hash);
         for (unsigned h = lane_id(); h <= sm.hmask / 2; h += 32) h32[h] = 0xffffffffu;
         __syncwarp();
@@ -318,16 +358,57 @@ struct WarpBeam {
     // Lane i < cnt: the level-1 lazy key of candidate cid (fp32 screen value,
     // PK_APX|PK_A32 in cidf); where the fp32 value is unusable (underflow /
     // overflow) the float64 one (PK_APX, or exact when it is 0).
+    // fp32 screens through the row ring: every lane of `mask` holds a row id and
+    // gets its row's screen value (other lanes keep `mine`).  Rows stream through
+    // the ring_s slots: the lane that holds an id issues its bulk copy, the warp
+    // waits for the oldest slot, screens it from shared memory and hands the slot
+    // to the next row, so ring_s rows are in flight until the last ones drain.
+    template <class D>
+    __device__ float ring_screens(const SearchParams& P, const D& dist, unsigned id, unsigned mask, float mine) {
+        const int lane = lane_id();
+        const int S = sm.ring_s, nv = P.dp >> 2;
+        const unsigned bytes = (unsigned)P.dp * 4u;
+        const int sh = 31 - __clz(S);
+        unsigned pend = mask;  // rows not requested yet
+        unsigned ti = rt;      // next request's sequence number
+        auto issue = [&]() {
+            const int j = __ffs(pend) - 1;
+            pend &= pend - 1u;
+            if (lane == j) {
+                const int slot = (int)(ti & (unsigned)(S - 1));
+                mbar_expect_tx(sm.bars + slot, bytes);
+                bulk_g2s(sm.ring + (size_t)slot * nv, P.X + (size_t)id * P.dp, bytes, sm.bars + slot);
+            }
+            ++ti;
+        };
+        for (int i = 0; i < S && pend; ++i) issue();
+        for (unsigned w = mask; w; w &= w - 1u) {
+            const int j = __ffs(w) - 1;
+            const int slot = (int)(rt & (unsigned)(S - 1));
+            mbar_wait(sm.bars + slot, (rt >> sh) & 1u);
+            const float v = dist.screen_smem(sm.ring + (size_t)slot * nv);
+            if (lane == j) mine = v;
+            ++rt;
+            __syncwarp();  // every lane has read the slot before it is refilled
+            if (pend) issue();
+        }
+        return mine;
+    }
+
     template <class D>
     __device__ double approx(const SearchParams& P, const D& dist, unsigned cid, int cnt, unsigned& cidf) {
         const int lane = lane_id();
         float mine = 0.f;
-        for (int j = 0; j < cnt; j += 2) {
-            const int j1 = j + 1 < cnt ? j + 1 : j;
-            const float s0 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j));
-            const float s1 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j1));
-            if (lane == j) mine = s0;
-            if (lane == j1) mine = s1;
+        if constexpr (uses_ring<D>::value) {
+            mine = ring_screens(P, dist, cid, cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u), 0.f);
+        } else {
+            for (int j = 0; j < cnt; j += 2) {
+                const int j1 = j + 1 < cnt ? j + 1 : j;
+                const float s0 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j));
+                const float s1 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j1));
+                if (lane == j) mine = s0;
+                if (lane == j1) mine = s1;
+            }
         }
         double v = (double)mine;
         cidf = cid | PK_APX | PK_A32;
@@ -489,87 +570,18 @@ struct WarpBeam {
         }
     }
 
-    // lazy-mode batch insert: approx -> resolve -> merge.  `spec` (the last
-    // group of an expansion, P.spec_rows): once the screens are known, the next
-    // expansion is predicted (the better of the next unvisited beam entry and
-    // the best new candidate that beats the beam's worst key), its adjacency
-    // row is loaded while resolve() runs, and its unseen neighbours' rows are
-    // requested from L2 before the merge -- the next expansion's screens then
-    // find them on their way from HBM.  A wrong guess only costs bandwidth.
+    // lazy-mode batch insert: approx -> resolve -> merge
     template <bool CheckDups, class D>
-    __device__ void insert_lazy(const SearchParams& P, const D& dist, unsigned cid, int cnt, bool spec = false) {
+    __device__ void insert_lazy(const SearchParams& P, const D& dist, unsigned cid, int cnt) {
         unsigned cidf;
         PK_PT_BEGIN
         double v = approx(P, dist, cid, cnt, cidf);
         PK_PT_NEXT(2);
-        unsigned pn = 0xffffffffu;
-        int sa = -1, sb = -1, snd = 0;
-        if (spec) {
-            pn = predict_next(v, cid, cnt);
-            if (pn != 0xffffffffu) {
-                const int* row = P.adj + (size_t)pn * P.R;
-                const int lane = lane_id();
-                sa = lane < P.R ? __ldg(row + lane) : -1;
-                sb = lane + 32 < P.R ? __ldg(row + lane + 32) : -1;
-                snd = __ldg(P.deg + pn);
-            }
-        }
         bool valid = lane_id() < cnt;
         resolve(P, dist, v, cidf, valid);
         PK_PT_NEXT(3);
-        if (pn != 0xffffffffu && P.spec_rows == 1) {
-            prefetch_unseen(P, sa, sb, snd);
-            spec_id = pn;
-        }
-        PK_PT_NEXT(1);
         merge<CheckDups>(v, cidf, valid);
-        PK_PT_NEXT(4);
-        if (pn != 0xffffffffu && P.spec_rows == 2) {
-            prefetch_unseen(P, sa, sb, snd);
-            spec_id = pn;
-        }
-        PK_PT_END(1);
-    }
-
-    // the node the next expansion will most likely take (see insert_lazy)
-    __device__ unsigned predict_next(double v, unsigned cid, int cnt) {
-        const int lane = lane_id();
-        const int nu = next_unvisited();
-        const double inf = __longlong_as_double(0x7ff0000000000000LL);
-        const double bk = nu >= 0 ? sm.bd[nu] : inf;
-        const double lim = bl == L ? sm.bd[L - 1] : inf;
-        const double cv = lane < cnt ? v : inf;
-        double m = cv;
-#pragma unroll
-        for (int s = 16; s; s >>= 1) m = fmin(m, __shfl_xor_sync(PK_FULL, m, s));
-        if (m < bk && m < lim) {
-            const int src = __ffs(__ballot_sync(PK_FULL, cv == m)) - 1;
-            return __shfl_sync(PK_FULL, cid, src);
-        }
-        return nu >= 0 ? (sm.bi[nu] & PK_IDMASK) : 0xffffffffu;
-    }
-
-    // L2 requests for the rows of a predicted expansion's neighbours that the
-    // seen table does not hold (lane l: row slots l and l + 32, every line)
-    __device__ void prefetch_unseen(const SearchParams& P, int sa, int sb, int snd) {
-        const int lane = lane_id();
-        auto is_start = [&](int w) { return P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u); };
-        const bool ga = lane < snd && sa >= 0 && !seen_probe(sm.hash, sm.hmask, sm.hbits, (unsigned)sa) && !is_start(sa);
-        const bool gb = lane + 32 < snd && sb >= 0 && !seen_probe(sm.hash, sm.hmask, sm.hbits, (unsigned)sb) && !is_start(sb);
-        const unsigned ba = __ballot_sync(PK_FULL, ga), bb = __ballot_sync(PK_FULL, gb);
-        if (!(ba | bb)) return;
-        // row by row (lane l takes line l): a row's lines go out back to back
-        const int lines = (P.dp * 4 + 127) >> 7;
-        for (unsigned b = ba; b; b &= b - 1) {
-            const unsigned id = (unsigned)__shfl_sync(PK_FULL, sa, __ffs(b) - 1);
-            const char* r = reinterpret_cast<const char*>(P.X + (size_t)id * P.dp);
-            for (int l = lane; l < lines; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + ((size_t)l << 7)));
-        }
-        for (unsigned b = bb; b; b &= b - 1) {
-            const unsigned id = (unsigned)__shfl_sync(PK_FULL, sb, __ffs(b) - 1);
-            const char* r = reinterpret_cast<const char*>(P.X + (size_t)id * P.dp);
-            for (int l = lane; l < lines; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + ((size_t)l << 7)));
-        }
+        PK_PT_END(4);
     }
 
     // build: exact distances for the visit-log entries logged with lazy keys
@@ -678,6 +690,10 @@ struct WarpBeam {
             if (mrow) want = want && ((mrow[b >> 5] >> lane) & 1u);
             unsigned wm = __ballot_sync(PK_FULL, want);
             float mine = __uint_as_float(0x7f800000u);
+            if constexpr (uses_ring<D>::value) {
+                mine = ring_screens(P, dist, id, wm, mine);
+                wm = 0u;
+            }
             while (wm) {
                 const int j = __ffs(wm) - 1;
                 wm &= wm - 1u;
@@ -897,12 +913,28 @@ struct WarpBeam {
                 }
             }
             int c = 0;
+            // ring kernels (seen table in global memory): the sets of the first 64
+            // slots are read together, one L2 round trip instead of two
+            uint2 v_a = make_uint2(0u, 0u), v_b = v_a;
+            if constexpr (uses_ring<D>::value) {
+                if (lane >= nd) w_a = -1;
+                if (lane + 32 >= nd) w_b = -1;
+                if (w_a >= 0) v_a = seen_load(sm.hash, sm.hmask, (unsigned)w_a);
+                if (w_b >= 0) v_b = seen_load(sm.hash, sm.hmask, (unsigned)w_b);
+            }
             for (int e0 = 0; e0 < nd; e0 += 32) {
                 int w = e0 + lane < nd ? (e0 == 0 ? w_a : e0 == 32 ? w_b : __ldg(row + e0 + lane)) : -1;
                 bool cand = w >= 0;
-                // a start was merged at seeding: it is in the beam or can never re-enter it
-                if (cand && P.start_bm && ((__ldg(P.start_bm + (w >> 5)) >> (w & 31)) & 1u)) cand = false;
-                if (cand && seen_or_insert(sm.hash, sm.hmask, sm.hbits, (unsigned)w)) cand = false;
+                if (cand) {
+                    bool seen;
+                    if constexpr (uses_ring<D>::value)
+                        seen = e0 == 0   ? seen_apply(sm.hash, sm.hmask, sm.hbits, (unsigned)w, v_a)
+                               : e0 == 32 ? seen_apply(sm.hash, sm.hmask, sm.hbits, (unsigned)w, v_b)
+                                          : seen_or_insert(sm.hash, sm.hmask, sm.hbits, (unsigned)w);
+                    else
+                        seen = seen_or_insert(sm.hash, sm.hmask, sm.hbits, (unsigned)w);
+                    if (seen) cand = false;
+                }
                 unsigned b = __ballot_sync(PK_FULL, cand);
                 const int nb = __popc(b);
                 if (c + nb > kCbuf) {  // very wide rows: flush before the buffer overflows
@@ -914,12 +946,7 @@ struct WarpBeam {
             }
             __syncwarp();
             PK_PT_END(0);
-            const bool hit = spec_id == p;  // this expansion's rows were requested during the last merge
-#ifdef PK_PHASE_TIMERS
-            if (lane == 0 && spec_id != 0xffffffffu) atomicAdd(&pk_phase_cycles[7], hit ? (1ull << 32) + 1ull : 1ull);
-#endif
-            spec_id = 0xffffffffu;
-            flush(P, dist, c, hit);
+            flush(P, dist, c);
         }
     }
 
@@ -973,7 +1000,7 @@ struct WarpBeam {
 
     // evaluate and merge the c candidates staged in cbuf
     template <class D>
-    __device__ void flush(const SearchParams& P, const D& dist, int c, bool spec_hit = false) {
+    __device__ void flush(const SearchParams& P, const D& dist, int c) {
         const int lane = lane_id();
         __syncwarp();
         for (int g = 0; g < c; g += 32) {
@@ -984,9 +1011,10 @@ struct WarpBeam {
             if constexpr (has_screen<D>::value) {
                 if (lazy) {
                     PK_PT_BEGIN
-                    if (P.prefetch_rows && cnt > 2 && !spec_hit) prefetch_rows(P, cid, cnt);
+                    if constexpr (!uses_ring<D>::value)
+                        if (P.prefetch_rows && cnt > 2) prefetch_rows(P, cid, cnt);
                     PK_PT_END(1);
-                    insert_lazy<false>(P, dist, cid, cnt, P.spec_rows && g + 32 >= c);
+                    insert_lazy<false>(P, dist, cid, cnt);
                     continue;
                 }
             }
@@ -997,12 +1025,17 @@ struct WarpBeam {
                 if (bl == L && P.screen && P.dp >= 256 && P.dp <= 128 * D::kQV) {
                     const double wd = sm.bd[L - 1];
                     bool drop = false;
-                    for (int j = 0; j < cnt; j += 2) {
-                        const int j1 = j + 1 < cnt ? j + 1 : j;
-                        const float s0 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j));
-                        const float s1 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j1));
-                        if (lane == j && s0 > 1e-20f && s0 < 1e30f && (double)s0 * (1.0 - kScreenEps) > wd) drop = true;
-                        if (lane == j1 && s1 > 1e-20f && s1 < 1e30f && (double)s1 * (1.0 - kScreenEps) > wd) drop = true;
+                    if constexpr (uses_ring<D>::value) {
+                        const float sv = ring_screens(P, dist, cid, cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u), 0.f);
+                        drop = lane < cnt && sv > 1e-20f && sv < 1e30f && (double)sv * (1.0 - kScreenEps) > wd;
+                    } else {
+                        for (int j = 0; j < cnt; j += 2) {
+                            const int j1 = j + 1 < cnt ? j + 1 : j;
+                            const float s0 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j));
+                            const float s1 = dist.screen(P.X, __shfl_sync(PK_FULL, cid, j1));
+                            if (lane == j && s0 > 1e-20f && s0 < 1e30f && (double)s0 * (1.0 - kScreenEps) > wd) drop = true;
+                            if (lane == j1 && s1 > 1e-20f && s1 < 1e30f && (double)s1 * (1.0 - kScreenEps) > wd) drop = true;
+                        }
                     }
                     const bool keep = lane < cnt && !drop;
                     const unsigned b = __ballot_sync(PK_FULL, keep);

@@ -55,14 +55,20 @@ struct BuildArgs {
 
 // phase 1: one warp per inserted point searches the adjacency snapshot and
 // logs its visited set (_kernels.py:349-358)
-template <int MODE, int QV>
+template <int MODE, int QV, bool RING>
 __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 5 : 8) : 8) build_search_kernel(BuildArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int lane = lane_id();
-    BeamSmem sm = carve_beam(smem + (size_t)wib * A.search_bytes, A.L, A.H);
-    const MakeAt<MODE, QV> make{A.D};
+    BeamSmem sm = A.P.ghash ? carve_beam_gh(smem + (size_t)wib * A.search_bytes,
+                                            A.P.ghash + ((size_t)blockIdx.x * wpb + wib) * A.P.ghash_stride, A.L, A.H)
+                            : carve_beam(smem + (size_t)wib * A.search_bytes, A.L, A.H);
+    if constexpr (RING)
+        carve_ring(sm, smem + (size_t)(wib + 1) * A.search_bytes - ring_smem_bytes_dev(A.P.dp, A.P.ring), A.P.dp,
+                   A.P.ring);
+    unsigned ring_t = 0;
+    const MakeAt<MODE, QV, RING> make{A.D};
     long long ev = 0, expansions = 0, un = 0;
     const bool uniq = starts_increasing(A.P);
     for (int t = blockIdx.x * wpb + wib; t < A.m; t += gridDim.x * wpb) {
@@ -71,6 +77,7 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, A.L, A.vlog_i + (size_t)t * A.vcap, A.vlog_d + (size_t)t * A.vcap, A.vcap, A.err);
         wb.qid = p;
+        wb.rt = ring_t;
         wb.begin_counting(A.P.ubm ? A.P.ubm + ((size_t)blockIdx.x * wpb + wib) * A.P.uwords : nullptr, A.P.uwords);
         {
             PK_PT_BEGIN
@@ -84,6 +91,7 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         un += wb.uniq;
         ev += wb.evals;
         expansions += wb.vl;
+        ring_t = wb.rt;
         if (lane == 0) A.vlen[t] = min(wb.vl, A.vcap);
         __syncwarp();
     }
@@ -1300,9 +1308,18 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     const int SR = std::min(capR, env_int("PK_REV_S", 128));
 
     BuildArgs A;
-    A.search_bytes = align16(beam_smem_bytes(L, H));
+    // row ring of the float searches with lazy keys (beam.cuh carve_ring), behind the beam state
+    const bool lazy_screen = MODE == MODE_SEQ64 && D.screen && env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
+    int ring = MODE == MODE_SEQ64 && QV >= 4 && env_int("PK_RING_BUILD", 0) == 1 ? ring_slots(D.dp, QV, lazy_screen) : 0;
+    if (align16(beam_smem_bytes(L, H)) + align16(ring_smem_bytes(D.dp, ring)) > (size_t)max_smem_optin()) ring = 0;
+    // with the ring, the seen table moves to a global slab per warp (carve_beam_gh)
+    const bool ghash = ring && env_int("PK_HASH_GLOBAL", 1) == 1;
+    A.search_bytes = align16(beam_smem_bytes(L, ghash ? 0 : H)) + align16(ring_smem_bytes(D.dp, ring));
     A.prune_bytes = cand_smem_bytes(cap, D.dw, S, u8);
-    auto sk = build_search_kernel<MODE, QV>;
+    auto sk = build_search_kernel<MODE, QV, false>;
+    if constexpr (MODE == MODE_SEQ64 && QV >= 4) {
+        if (ring) sk = build_search_kernel<MODE, QV, true>;
+    }
     auto pkk = build_prune_kernel<MODE, QV>;
     auto rk = reverse_kernel<MODE, QV>;
     int wpb_s, grid_s, wpb_p, grid_p, wpb_r, grid_r, rc;
@@ -1424,11 +1441,14 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.P.screen = D.screen;
     A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     A.P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && D.dp >= 512;  // measured: helps 4 KB rows (C5), not 1.5 KB (C4)
-    A.P.spec_rows = env_int("PK_SPEC_ROWS", 0);
-    unsigned* sbm = nullptr;  // start ids re-met as neighbours are skipped (see pk_beam_knn_seeded)
-    PK_CHECK(start_bitmap(starts, s, n, &sbm, st));
-    A.P.start_bm = sbm;
     A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
+    A.P.ring = ring;
+    unsigned char* gh = nullptr;
+    if (ghash) {
+        A.P.ghash_stride = (size_t)H * 2;
+        PK_CHECK(scratch(&gh, (size_t)grid_s * wpb_s * A.P.ghash_stride, st));
+        A.P.ghash = gh;
+    }
     A.P.seed_select = env_int("PK_SEED_SELECT", 1);
     if (SH.seed_bd && SH.seed_bi && SH.seed_bl && SH.world == 1) {
         A.P.seed_bd = SH.seed_bd;
@@ -1675,7 +1695,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
                     (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)adjd, (void*)new_d,
-                    (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, (void*)sbm, cub_tmp})
+                    (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, (void*)gh, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

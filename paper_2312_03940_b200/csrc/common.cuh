@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #define PK_FULL 0xffffffffu
 #define PK_VIS 0x80000000u   // visited flag, stored in bit 31 of a beam id
 #define PK_APX 0x40000000u   // lazy keys: the stored distance is an approximation (bit 30) ...
@@ -103,13 +105,49 @@ __device__ __forceinline__ bool seen_or_insert(unsigned short* hash, unsigned ma
     return false;
 }
 
-// read-only probe of the seen table (speculative row requests)
-__device__ __forceinline__ bool seen_probe(const unsigned short* hash, unsigned mask, int hbits, unsigned id) {
+// seen_or_insert in two steps, so the set loads of several ids can be issued
+// together (one round trip when the table lives in global memory): the second
+// id's view of a shared set may miss the first id's insert, which can only
+// lose an entry (a re-evaluation), never report an unseen id as seen
+__device__ __forceinline__ uint2 seen_load(const unsigned short* hash, unsigned mask, unsigned id) {
+    return reinterpret_cast<const uint2*>(hash)[id & (mask >> 2)];
+}
+__device__ __forceinline__ bool seen_apply(unsigned short* hash, unsigned mask, int hbits, unsigned id, uint2 v) {
     const unsigned set = id & (mask >> 2);
     const unsigned tag = id >> (hbits - 2);
-    const uint2 v = reinterpret_cast<const uint2*>(hash)[set];
     const unsigned t2 = tag | (tag << 16);
-    return (__vcmpeq2(v.x, t2) | __vcmpeq2(v.y, t2)) != 0u;
+    if (__vcmpeq2(v.x, t2) | __vcmpeq2(v.y, t2)) return true;
+    const unsigned ex = __vcmpeq2(v.x, 0xffffffffu), ey = __vcmpeq2(v.y, 0xffffffffu);
+    const unsigned way = ex ? ((ex & 0xffffu) ? 0u : 1u) : ey ? ((ey & 0xffffu) ? 2u : 3u) : ((tag ^ (id >> 5)) & 3u);
+    hash[4 * set + way] = (unsigned short)tag;
+    return false;
+}
+
+// ---- mbarrier + bulk copy (tensor-core kernels; row ring of the float beam searches) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// global -> shared bulk copy (TMA engine, no tensor map): bytes % 16 == 0, both sides 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
 }
 
 // ---- distance policies ---------------------------------------------------------
@@ -389,6 +427,27 @@ struct Seq64Screened : Seq64Member {
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, o);
         return acc;
     }
+    // screen() of a row staged in shared memory (row ring, beam.cuh): the same
+    // arithmetic in the same order, so the same value as screen()
+    __device__ __forceinline__ float screen_smem(const float4* __restrict__ r) const {
+        const int nv = dp >> 2, lane = lane_id();
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < QV; ++j) {
+            const int f = lane + 32 * j;
+            if (f < nv) {
+                const float4 y = qr[j], x = r[f];
+                const float d0 = y.x - x.x, d1 = y.y - x.y, d2 = y.z - x.z, d3 = y.w - x.w;
+                acc = fmaf(d0, d0, acc);
+                acc = fmaf(d1, d1, acc);
+                acc = fmaf(d2, d2, acc);
+                acc = fmaf(d3, d3, acc);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, o);
+        return acc;
+    }
     // Warp-cooperative float64 value of the squared distance (lazy keys): each
     // lane accumulates its 4*QV coordinates with fma, then an xor butterfly
     // (commutative adds: every lane ends with the same value).  Within
@@ -440,11 +499,28 @@ struct has_screen<Seq64Screened<QV>> {
     static constexpr bool value = true;
 };
 
-template <int MODE, int QV>
-struct DistFor;
+// Seq64Screened whose beam search stages candidate rows through the shared-memory
+// row ring (beam.cuh: ring_screens) instead of loading them into registers
 template <int QV>
-struct DistFor<MODE_SEQ64, QV> {
-    using T = Seq64Screened<QV>;
+struct Seq64Ring : Seq64Screened<QV> {};
+template <int QV>
+struct has_screen<Seq64Ring<QV>> {
+    static constexpr bool value = true;
+};
+template <class D>
+struct uses_ring {
+    static constexpr bool value = false;
+};
+template <int QV>
+struct uses_ring<Seq64Ring<QV>> {
+    static constexpr bool value = true;
+};
+
+template <int MODE, int QV, bool RING = false>
+struct DistFor;
+template <int QV, bool RING>
+struct DistFor<MODE_SEQ64, QV, RING> {
+    using T = typename std::conditional<RING, Seq64Ring<QV>, Seq64Screened<QV>>::type;
     __device__ static T make(const DataRef& D, unsigned id) {
         T t;
         t.q = D.X + (size_t)id * D.dp;
@@ -454,7 +530,7 @@ struct DistFor<MODE_SEQ64, QV> {
     }
 };
 template <int QV>
-struct DistFor<MODE_EXACT32, QV> {
+struct DistFor<MODE_EXACT32, QV, false> {
     using T = Exact32<QV>;
     __device__ static T make(const DataRef& D, unsigned id) {
         T t;
@@ -463,7 +539,7 @@ struct DistFor<MODE_EXACT32, QV> {
     }
 };
 template <int QV>
-struct DistFor<MODE_EXACT_U8, QV> {
+struct DistFor<MODE_EXACT_U8, QV, false> {
     using T = ExactU8<QV>;
     __device__ static T make(const DataRef& D, unsigned id) {
         T t;
@@ -558,10 +634,12 @@ __device__ __forceinline__ int screen_le(double alpha2, float dscr, double k) {
 }
 
 // functor: id -> distance policy object for that query row
-template <int MODE, int QV>
+template <int MODE, int QV, bool RING = false>
 struct MakeAt {
     DataRef D;
-    __device__ typename DistFor<MODE, QV>::T operator()(unsigned id) const { return DistFor<MODE, QV>::make(D, id); }
+    __device__ typename DistFor<MODE, QV, RING>::T operator()(unsigned id) const {
+        return DistFor<MODE, QV, RING>::make(D, id);
+    }
 };
 
 // ---- warp utilities --------------------------------------------------------------

@@ -10,7 +10,9 @@
 namespace pk {
 
 // ---- beam kNN of member queries (_kernels.py:230-262) --------------------------------
-template <int MODE, int QV>
+// RING (float data, QV >= 4): candidate rows staged through the per-warp row
+// ring (bulk copies into shared memory) instead of registers
+template <int MODE, int QV, bool RING>
 __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 5 : 8) : 8) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
                                                        int L, int kk, int H, size_t warp_bytes,
                                                        long long* __restrict__ out_ids, double* __restrict__ out_d,
@@ -23,15 +25,19 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
     const int lane = lane_id();
     unsigned char* mine = smem + (size_t)wib * warp_bytes;
     BeamSmem sm = gbeam ? carve_beam_spill(mine, gbeam + ((size_t)blockIdx.x * wpb + wib) * gstride, L, H)
-                        : carve_beam(mine, L, H);
+                  : P.ghash ? carve_beam_gh(mine, P.ghash + ((size_t)blockIdx.x * wpb + wib) * P.ghash_stride, L, H)
+                            : carve_beam(mine, L, H);
+    if constexpr (RING) carve_ring(sm, mine + warp_bytes - ring_smem_bytes_dev(P.dp, P.ring), P.dp, P.ring);
+    unsigned ring_t = 0;
     long long ev = 0, ex = 0, un = 0;
     const bool uniq = starts_increasing(P);
     for (int t0 = blockIdx.x * wpb + wib; t0 < m; t0 += gridDim.x * wpb) {
         const int t = ord ? __ldg(ord + t0) : t0;  // processing order (locality) != output row order
         const unsigned qi = (unsigned)qids[t];
-        auto dist = DistFor<MODE, QV>::make(P.data(), qi);
+        auto dist = DistFor<MODE, QV, RING>::make(P.data(), qi);
         WarpBeam<decltype(dist)> wb;
         wb.init(sm, L, nullptr, nullptr, 0, nullptr);
+        wb.rt = ring_t;
         wb.begin_counting(P.ubm ? P.ubm + ((size_t)blockIdx.x * wpb + wib) * P.uwords : nullptr, P.uwords);
         {
             PK_PT_BEGIN
@@ -57,6 +63,7 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
         PK_PT_END(5);
         ev += wb.evals;
         ex += wb.vl;
+        ring_t = wb.rt;
         __syncwarp();
     }
     if (evals_out && lane == 0 && ev) {
@@ -330,23 +337,6 @@ __global__ void start_bitmap_kernel(const int* starts, int s, unsigned* bm) {
         atomicOr(bm + (starts[x] >> 5), 1u << (starts[x] & 31));
 }
 
-int grid_for(long long work, int block);
-
-cudaError_t start_bitmap(const int* starts, int s, long long n, unsigned** out, cudaStream_t st) {
-    *out = nullptr;
-    if (env_int("PK_START_SKIP", 0) != 1 || s <= 0) return cudaSuccess;
-    const size_t words = (size_t)((n + 31) / 32);
-    cudaError_t e = scratch(out, words, st);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(*out, 0, words * sizeof(unsigned), st);
-    if (e != cudaSuccess) return e;
-    {
-        ProfScope _ps("start_bitmap_kernel", st);
-        start_bitmap_kernel<<<grid_for(s, 256), 256, 0, st>>>(starts, s, *out);
-    }
-    return cudaGetLastError();
-}
-
 int grid_for(long long work, int block) {
     long long g = (work + block - 1) / block;
     long long cap = (long long)sm_count() * 16;
@@ -419,6 +409,14 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     const bool spill = wb > (size_t)max_smem_optin();
     const size_t gstride = spill ? spill_slab_bytes(L) : 0;
     if (spill) wb = align16(spill_smem_bytes(H));
+    // row ring of the float searches with lazy keys (beam.cuh carve_ring), behind the beam state
+    SearchParams Pr = P;
+    Pr.ring = MODE == MODE_SEQ64 && QV >= 4 ? ring_slots(P.dp, QV, P.screen && P.lazy) : 0;
+    if (spill || wb + align16(ring_smem_bytes(P.dp, Pr.ring)) > (size_t)max_smem_optin()) Pr.ring = 0;
+    // with the ring, the seen table moves to a global slab per warp (carve_beam_gh)
+    const bool ghash = Pr.ring && env_int("PK_HASH_GLOBAL", 1) == 1;
+    if (ghash) wb = align16(beam_smem_bytes(L, 0));
+    wb += align16(ring_smem_bytes(P.dp, Pr.ring));
     // warps per block: the most resident warps per SM (wide beams: a block of 2
     // x 64 KB leaves a third warp's worth of the SM's shared memory unused)
     const size_t sm_bytes = (size_t)max_smem_optin() + 1024;  // per-SM capacity (one block's reserve)
@@ -431,7 +429,10 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
             wpb = w;
         }
     }
-    auto kern = beam_knn_kernel<MODE, QV>;
+    auto kern = beam_knn_kernel<MODE, QV, false>;
+    if constexpr (MODE == MODE_SEQ64 && QV >= 4) {
+        if (Pr.ring) kern = beam_knn_kernel<MODE, QV, true>;
+    }
     PK_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wb * wpb)));
     int per_sm = 0;
     PK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, wb * wpb));
@@ -447,6 +448,12 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     if (grid < 1) grid = 1;
     unsigned char* gbeam = nullptr;
     if (spill) PK_CHECK(scratch(&gbeam, (size_t)grid * wpb * gstride, st));
+    unsigned char* gh = nullptr;
+    if (ghash) {
+        Pr.ghash_stride = (size_t)H * 2;
+        PK_CHECK(scratch(&gh, (size_t)grid * wpb * Pr.ghash_stride, st));
+        Pr.ghash = gh;
+    }
     int* ord = nullptr;
     if (P.seed_load && m >= (1 << 16) && env_int("PK_LOCALITY", 1) == 1) {
         const int rc = query_locality_order(P, qids, m, L, P.n_points, &ord, st);
@@ -454,7 +461,7 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     }
     // counting mode (bench.py's untimed pass): exact number of distinct ids
     // evaluated, added to evals[2] (the caller then passes 3 counters)
-    SearchParams Pc = P;
+    SearchParams Pc = Pr;
     unsigned* ubm = nullptr;
     if (evals && env_int("PK_COUNT_UNIQUE", 0) == 1) {
         Pc.uwords = (int)((P.n_points + 31) / 32);
@@ -469,6 +476,7 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     PK_CHECK_LAUNCH("beam_knn_kernel");
     if (ubm) release(ubm, st);
     if (gbeam) release(gbeam, st);
+    if (gh) release(gh, st);
     if (ord) release(ord, st);
     return 0;
 }
@@ -638,12 +646,14 @@ extern "C" int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const u
         set_error("too many points for the beam kernels (ids are 30-bit)");
         return 2;
     }
+    // Start points re-met as neighbours are simply re-evaluated (and dropped
+    // by the key-equality check when already in the beam): cheaper than a
+    // dependent bitmap load on every neighbour.
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, x8, (int)dw};
     P.screen = env_int("PK_SCREEN", 1) == 1;
     P.n_points = n;
     P.prefetch = env_int("PK_PREFETCH", 1) == 1;
     P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && dp >= 512;  // measured: helps rows of 4 KB (C5), not 1.5 KB (C4)
-    P.spec_rows = env_int("PK_SPEC_ROWS", 0);
     P.lazy = env_int("PK_LAZY", 1) == 1 && n < (int64_t)PK_IDMASK;
     P.seed_only = env_int("PK_SEED_ONLY", 0);
     P.seed_select = env_int("PK_SEED_SELECT", 1);
@@ -664,17 +674,11 @@ extern "C" int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const u
         set_error("u8 mode needs the packed rows");
         return 2;
     }
-    // every start was merged into the seeded beam: one re-met as a neighbour is
-    // either in the beam or above its L-th key, which never increases -- skip it
-    unsigned* sbm = nullptr;
-    PK_CHECK(start_bitmap(starts, (int)s, n, &sbm, st));
-    P.start_bm = sbm;
     int rc = mode == MODE_EXACT_U8
                  ? dispatch_beam_knn<MODE_EXACT_U8>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st)
              : mode == MODE_EXACT32
                  ? dispatch_beam_knn<MODE_EXACT32>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st)
                  : dispatch_beam_knn<MODE_SEQ64>(P, q, (int)m, (int)L, (int)kk, H, oi, out_sqd, oc, ev, st);
-    release(sbm, st);
     if (rc) return rc;
     if (brute_fallback) {
         int* list = nullptr;
