@@ -195,6 +195,9 @@ int pk_parse_pecg(const uint32_t* words, int64_t nwords, int64_t n, int64_t R, i
  * library was compiled with -DPK_PHASE_TIMERS (tools/variant.sh). */
 int pk_phase_timers(unsigned long long* out8, int reset);
 int pk_phase_timers_build(unsigned long long* out8, int reset);
+/* the tensor-core build prune: candidates + sort, norms, Gram, epilogue, greedy,
+ * output; [6] exact pair decisions, [7] items */
+int pk_phase_timers_prune(unsigned long long* out8, int reset);
 
 /* Host helper: index of the first non-finite value of x[0, count) in
  * row-major order (-1 if none) -> *first_bad; all host threads scan.  The

@@ -51,6 +51,7 @@ SIGNATURES = {
     "pk_parse_pecg": [_P, _I, _I, _I, _P, _P, _P],
     "pk_phase_timers": [_P, _i],
     "pk_phase_timers_build": [_P, _i],
+    "pk_phase_timers_prune": [_P, _i],
     "pk_scan_points": [_P, _I, _I, _I, _P, _P],
     "pk_robust_prune": [_P, _I, _I, _I, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P],
     "pk_nearest_to_centroid": [_P, _I, _I, _P, _P],

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <string>
 
+#include <cuda_fp16.h>
 #include <cub/cub.cuh>
 
 #include "../../include/peakann_b200.h"
@@ -1364,6 +1365,19 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         }
         PK_CHECK_LAUNCH("norms64_kernel");
     }
+    // fp16 copy of the rows for the Gram tiles (half the gather bytes, half the K
+    // chunks of the tf32 Gram; PK_PRUNE_F16=0: tf32 from the fp32 rows)
+    __half* xh = nullptr;
+    const int kph = (D.dp + 63) & ~63;
+    if (tcp && env_int("PK_PRUNE_F16", 1) == 1) {
+        PK_CHECK(scratch(&xh, (size_t)n * kph, st));
+        {
+            ProfScope _ps("rows_to_half_kernel", st);
+            rows_to_half_kernel<<<sm_count() * 16, 256, 0, st>>>(D.X, n, D.dp, kph, xh);
+        }
+        PK_CHECK_LAUNCH("rows_to_half_kernel");
+    }
+    const PTAux aux{nrm64, xh, kph};
     const int capB = 8192;
     const size_t big_bytes = (size_t)capB * 13 + 16;
     auto bigk = reverse_big_kernel<MODE, QV>;
@@ -1569,7 +1583,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                 PK_CHECK(cudaMemsetAsync(nover, 0, sizeof(int), st));
                 if (tcb) {
                     ProfScope _ps("prune_tc_build_kernel", st);
-                    tpk<<<std::min(2 * sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, nrm64, over, nover);
+                    tpk<<<std::min(2 * sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, aux, over, nover);
                 } else {
                     ProfScope _ps("build_prune_block_kernel", st);
                     bpk<<<std::min(grid_bp, my_m), BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(A, over, nover);
@@ -1644,12 +1658,12 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             PK_CHECK(cudaMemsetAsync(nmid, 0, sizeof(int), st));
             {
                 ProfScope _ps("prune_tc_reverse_kernel", st);
-                trk<<<std::min(2 * sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, nrm64, nullptr, nullptr, midl, nmid);
+                trk<<<std::min(2 * sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, aux, nullptr, nullptr, midl, nmid);
             }
             PK_CHECK_LAUNCH("prune_tc_reverse_kernel");
             {
                 ProfScope _ps("prune_tc_reverse_kernel", st);
-                trk2<<<sm_count(), PT_THREADS, pt_smem_bytes(PT_CAP_BIG), st>>>(B, nrm64, midl, nmid, nullptr, nullptr);
+                trk2<<<sm_count(), PT_THREADS, pt_smem_bytes(PT_CAP_BIG), st>>>(B, aux, midl, nmid, nullptr, nullptr);
             }
         } else {
             ProfScope _ps("reverse_kernel", st);
@@ -1694,7 +1708,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
-                    (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)adjd, (void*)new_d,
+                    (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)xh, (void*)adjd, (void*)new_d,
                     (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, (void*)gh, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
@@ -1861,6 +1875,22 @@ extern "C" int pk_phase_timers_build(unsigned long long* out8, int reset) {
     if (reset) {
         unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         PK_CHECK(cudaMemcpyToSymbol(pk_phase_cycles, z, sizeof z));
+    }
+#else
+    (void)reset;
+    for (int i = 0; i < 8; ++i) out8[i] = 0;
+#endif
+    return 0;
+}
+
+// Diagnostics: the tensor-core build prune's phase timers (prune_tc.cuh).
+extern "C" int pk_phase_timers_prune(unsigned long long* out8, int reset) {
+#ifdef PK_PHASE_TIMERS
+    PK_CHECK(cudaDeviceSynchronize());
+    PK_CHECK(cudaMemcpyFromSymbol(out8, pk_prune_cycles, sizeof(unsigned long long) * 8));
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        PK_CHECK(cudaMemcpyToSymbol(pk_prune_cycles, z, sizeof z));
     }
 #else
     (void)reset;

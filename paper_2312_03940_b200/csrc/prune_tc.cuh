@@ -32,6 +32,32 @@
 // uses (BuildArgs, RevArgs, BPSmem, bp_sort, bp_unique, prune_by_selection).
 #pragma once
 
+// Phase timers of the tensor-core prune (diagnostics build only, -DPK_PHASE_TIMERS):
+// clock64 cycles of thread 0 per phase summed over blocks into pk_prune_cycles[]
+// -- 0 candidates + sort + unique, 1 norms / row pointers, 2 Gram staging + MMAs,
+// 3 epilogue (bit rows), 4 greedy picks, 5 output; [6] = exact pair decisions,
+// [7] = items.  Read by pk_phase_timers_prune.
+#ifdef PK_PHASE_TIMERS
+static __device__ unsigned long long pk_prune_cycles[8];
+#define PT_T0 pp.t0 = clock64();
+#define PT_TICK(ph)                                                                                        \
+    do {                                                                                                   \
+        if (threadIdx.x == 0 && pp.t0 >= 0) {                                                              \
+            const long long _n = clock64();                                                                \
+            atomicAdd(&pk_prune_cycles[ph], (unsigned long long)(_n - pp.t0));                             \
+            pp.t0 = _n;                                                                                   \
+        }                                                                                                  \
+    } while (0)
+#define PT_COUNT(slot, v)                                                               \
+    do {                                                                                \
+        if (threadIdx.x == 0 && pp.t0 >= 0) atomicAdd(&pk_prune_cycles[slot], (unsigned long long)(v)); \
+    } while (0)
+#else
+#define PT_T0
+#define PT_TICK(ph) do { } while (0)
+#define PT_COUNT(slot, v) do { } while (0)
+#endif
+
 constexpr int PT_CAP = 512;   // candidates per item, two-CTA-per-SM kernels (bit rows in 128-row blocks)
 constexpr int PT_CAP_BIG = 1024;  // reverse groups of 513..1024 candidates: one CTA per SM
 constexpr int PT_THREADS = 128;
@@ -56,6 +82,10 @@ struct PTSmem {
     unsigned* unc;         // [128][words]
     int words;             // bit words per row (cap / 32)
     unsigned long long* rowp;  // [PT_CAP] global address of each sorted candidate row
+    // fp32 operands of the epilogue's first-pass decision (pt_gram_pass), in the
+    // space of S.ki / S.kd, which are dead between pt_unique and the next item:
+    float* su32;               // [cap] |u| rounded up
+    float2* ab32;              // [cap] (A_u rounded down, B_u rounded up); NaN = out of the fp32 range
     unsigned long long* bar;  // [PT_STAGES] MMAs of the stage's chunk done
     unsigned* tmem_slot;
     BPSmem S;              // kd, ki, kd2, ki2, scal (bp_sort / bp_unique)
@@ -84,6 +114,8 @@ __device__ __forceinline__ PTSmem carve_pt(unsigned char* raw) {
     P.S.rows = nullptr;
     P.S.nrm = nullptr;
     P.S.kill = nullptr;
+    P.su32 = reinterpret_cast<float*>(P.S.ki);
+    P.ab32 = reinterpret_cast<float2*>(P.S.kd);
     return P;
 }
 
@@ -112,6 +144,7 @@ __device__ __forceinline__ void tmem_ld16(unsigned taddr, float (&v)[16]) {
 struct PTPipe {
     unsigned tmem;
     unsigned phase;  // bit s: parity of the next completion of bar[s]
+    long long t0;    // phase timers (diagnostics build): start of the current phase
 };
 
 // float64 |x|^2 of every point (warp per row), for the Gram epilogue
@@ -132,6 +165,27 @@ __global__ void norms64_kernel(const float* __restrict__ X, long long n, int dp,
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, o);
         if (lane == 0) out[r] = acc;
+    }
+}
+
+// Per-build inputs of the tensor-core prune: float64 |x|^2 of every point and,
+// for the fp16 Gram (PK_PRUNE_F16, default), an fp16 copy of the rows padded to
+// kp = a multiple of 64 coordinates.  xh == nullptr: tf32 Gram from the fp32 rows.
+struct PTAux {
+    const double* nrm64;
+    const __half* xh;
+    int kp;
+};
+
+// fp16 copy of every row (round to nearest), K padded with zeros to kp
+__global__ void rows_to_half_kernel(const float* __restrict__ X, long long n, int dp, int kp, __half* __restrict__ out) {
+    const long long total = n * (long long)(kp >> 1);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / (kp >> 1);
+        const int t = (int)(i - r * (kp >> 1)) * 2;
+        const float a = t < dp ? __ldg(X + (size_t)r * dp + t) : 0.f;
+        const float b = t + 1 < dp ? __ldg(X + (size_t)r * dp + t + 1) : 0.f;
+        reinterpret_cast<__half2*>(out)[i] = __halves2half2(__float2half_rn(a), __float2half_rn(b));
     }
 }
 
@@ -175,8 +229,10 @@ __device__ __forceinline__ void pt_stage_plan(const unsigned long long* rowp, in
 
 // Copy K chunk kc (floats 32 kc .. 32 kc + 31) of the planned slots into stage
 // buffer `st` (row slot x at x * 128 bytes, 16-byte piece j at (j ^ (x & 7))).
-__device__ __forceinline__ void pt_stage_chunk(int dp, const PTStagePlan& pl, int kc, unsigned char* st) {
-    const bool in = kc * 32 + pl.j * 4 < dp;
+// (rowbytes = the row's length in bytes: dp * 4 for fp32 rows, kp * 2 for the
+// fp16 copy, whose chunk of 128 bytes holds 64 coordinates)
+__device__ __forceinline__ void pt_stage_chunk(int rowbytes, const PTStagePlan& pl, int kc, unsigned char* st) {
+    const bool in = kc * 128 + pl.j * 16 < rowbytes;
     const unsigned sbase = smem_u32(st);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -197,18 +253,20 @@ __device__ __forceinline__ void pt_stage_chunk(int dp, const PTStagePlan& pl, in
 // columns (pairs u > t only).
 template <int QV>
 __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& P, PTPipe& pp, int c, int r0, int b0,
-                             int nb, double alpha2) {
+                             int nb, double alpha2, int rowbytes, bool f16) {
     const int tid = threadIdx.x;
-    const int nk = (dp + 31) >> 5;
+    const int nk = (rowbytes + 127) >> 7;
     const int na = min(128, c - r0);
     const int ncol = (nb + 15) & ~15;
-    const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(ncol >> 3) << 17) | ((128u >> 4) << 24);
+    // fp32 accumulators; operands tf32 (format 2) or f16 (format 0), K-major
+    const unsigned fmt = f16 ? 0u : 2u;
+    const unsigned idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((unsigned)(ncol >> 3) << 17) | ((128u >> 4) << 24);
     PTStagePlan pl;
     pt_stage_plan(P.rowp, r0, na, b0, nb, pl);
     const unsigned boff = (b0 == r0) ? 0u : 128u * 128u;  // B operand offset inside a stage
     // prologue: chunks 0 .. PT_STAGES - 2
     for (int k = 0; k < PT_STAGES - 1; ++k) {
-        if (k < nk) pt_stage_chunk(dp, pl, k, P.stage + (size_t)k * PT_STAGE_BYTES);
+        if (k < nk) pt_stage_chunk(rowbytes, pl, k, P.stage + (size_t)k * PT_STAGE_BYTES);
         else asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     for (int kc = 0; kc < nk; ++kc) {
@@ -219,7 +277,7 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
             mbar_wait(P.bar + sn, (pp.phase >> sn) & 1u);
             pp.phase ^= 1u << sn;
         }
-        if (kn < nk) pt_stage_chunk(dp, pl, kn, P.stage + (size_t)sn * PT_STAGE_BYTES);
+        if (kn < nk) pt_stage_chunk(rowbytes, pl, kn, P.stage + (size_t)sn * PT_STAGE_BYTES);
         else asm volatile("cp.async.commit_group;\n" ::: "memory");
         asm volatile("cp.async.wait_group %0;\n" ::"n"(PT_STAGES - 1) : "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -230,9 +288,15 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
             unsigned char* sb = P.stage + (size_t)s * PT_STAGE_BYTES;
             const unsigned long long da = umma_desc_sw128(sb);
             const unsigned long long db = umma_desc_sw128(sb + boff);
+            if (f16) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // 8 tf32 = 32 bytes per UMMA_K step
-                tc_mma_tf32(pp.tmem, da + 2ull * k, db + 2ull * k, idesc, (kc | k) != 0);
+                for (int k = 0; k < 4; ++k)  // 16 f16 = 32 bytes per UMMA_K step
+                    tc_mma_f16(pp.tmem, da + 2ull * k, db + 2ull * k, idesc, (kc | k) != 0);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // 8 tf32 = 32 bytes per UMMA_K step
+                    tc_mma_tf32(pp.tmem, da + 2ull * k, db + 2ull * k, idesc, (kc | k) != 0);
+            }
             tc_commit(P.bar + s);
         }
     }
@@ -243,18 +307,39 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
         pp.phase ^= 1u << s;
     }
     tc_fence_after();
+    PT_TICK(2);
 
     // epilogue: thread tid = TMEM lane, candidate row t = r0 + tid
     const int warp = tid >> 5;
     // relative bound of the tf32 Gram (inputs keep >= 10 mantissa bits, fp32
     // accumulation) and an absolute term for subnormal inputs / partial sums
     // flushed to zero: <= (dp + 8) 2^-126 (|t| + |u| + 1)
-    const double eg = 0.001953125 + (double)(dp + 8) * 1.1920928955078125e-07;
-    const double eabs = (double)(dp + 8) * 1.1754943508222875e-38;
+    // fp16 operands (round to nearest, 11 significant bits; below 2^-14 the
+    // spacing is 2^-24): |x^ - x| <= 2^-11 |x| + 2^-25 per coordinate, so
+    // |G^ - G| <= 2^-10 (1 + 2^-10) |t||u| + 2^-25 sqrt(dp) (|t| + |u|) (1 + 2^-10),
+    // plus the same fp32 accumulation term; a coordinate past the fp16 range makes
+    // the accumulator non-finite (decided exactly below)
+    const double eg = f16 ? 0.0009775171065493646 + (double)(dp + 8) * 1.1932570e-07
+                          : 0.001953125 + (double)(dp + 8) * 1.1920928955078125e-07;
+    const double eabs = f16 ? 5.9604644775390625e-08 * sqrt((double)dp) : (double)(dp + 8) * 1.1754943508222875e-38;
     const int t = r0 + tid;
     const unsigned tbase = pp.tmem + ((unsigned)(warp * 32) << 16);
     const bool live = t < c;
     const double nt = live ? P.nrm[t] : 0.0, st = live ? P.sq[t] : 0.0;
+    // First-pass decision in fp32 (the float64 form below costs ~17 FP64 operations
+    // per pair, and FP64 issue is what bounded this epilogue).  With E = c1 |u| + c0
+    // + 1e-12 |u|^2, c1 = 2 eg |t| + 2 eabs, c0 = 2 eabs (|t| + 1) + 1e-12 |t|^2:
+    //   alpha^2 (d~ + E) <= K  <=>  (|t|^2 + c0) - 2 G~ + c1 |u| <= A_u = K / alpha^2 - |u|^2 (1 + 1e-12)
+    //   alpha^2 (d~ - E) >  K  <=>  (|t|^2 - c0) - 2 G~ - c1 |u| >  B_u = K / alpha^2 - |u|^2 (1 - 1e-12)
+    // Per-row and per-candidate terms are rounded outwards (pt_prune: su32, ab32),
+    // and `tol` covers the three fp32 roundings of each side, so a pair the fp32
+    // test calls is called the same way by exact arithmetic; every other pair
+    // (and any operand outside the fp32 range: NaN) takes the float64 form.
+    const double c1d = 2.0 * eg * st + 2.0 * eabs;
+    const double c0d = 2.0 * eabs * (st + 1.0) + 1e-12 * nt;
+    float Pt = __double2float_ru(nt + c0d), Mt = __double2float_rd(nt - c0d);
+    const float c1f = __double2float_ru(c1d);
+    if (!(Pt < 1e30f) || !(c1f < 1e30f)) Pt = Mt = __int_as_float(0x7fc00000);
     // in the diagonal block, columns below this warp's first row hold only pairs u <= t
     for (int wd = (b0 == r0) ? warp : 0; wd * 32 < ncol; ++wd) {
         unsigned kb = 0u, ub = 0u;
@@ -272,6 +357,16 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
                     if (!isfinite(g[i])) {  // fp32 accumulator overflow (huge coordinates): decide exactly
                         ub |= bit;
                         continue;
+                    }
+                    {
+                        const float y = c1f * P.su32[u];
+                        const float2 ab = P.ab32[u];
+                        const float tol = fmaf(4e-7f, Pt + 2.f * fabsf(g[i]) + y, 1e-30f);
+                        if (fmaf(-2.f, g[i], Pt) + y + tol <= ab.x) {
+                            kb |= bit;
+                            continue;
+                        }
+                        if (fmaf(-2.f, g[i], Mt) - y - tol > ab.y) continue;
                     }
                     const double dt = nt + P.nrm[u] - 2.0 * (double)g[i];
                     const double su = P.sq[u];
@@ -292,15 +387,17 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
     }
     tc_fence_before();
     __syncthreads();
+    PT_TICK(3);
 }
 
 // Bit rows of candidates r0 .. r0 + 127 against every later candidate: the
 // diagonal block (columns r0 .. r0 + 255) then 128-column blocks up to c.
 template <int QV>
 __device__ void pt_gram_rows(const float* __restrict__ X, int dp, const PTSmem& P, PTPipe& pp, int c, int r0,
-                             double alpha2) {
-    pt_gram_pass<QV>(X, dp, P, pp, c, r0, r0, min(256, c - r0), alpha2);
-    for (int b0 = r0 + 256; b0 < c; b0 += 128) pt_gram_pass<QV>(X, dp, P, pp, c, r0, b0, min(128, c - b0), alpha2);
+                             double alpha2, int rowbytes, bool f16) {
+    pt_gram_pass<QV>(X, dp, P, pp, c, r0, r0, min(256, c - r0), alpha2, rowbytes, f16);
+    for (int b0 = r0 + 256; b0 < c; b0 += 128)
+        pt_gram_pass<QV>(X, dp, P, pp, c, r0, b0, min(128, c - b0), alpha2, rowbytes, f16);
 }
 
 // Greedy picks (warp 0) among the candidates of the current row block
@@ -406,16 +503,29 @@ __device__ __forceinline__ int pt_unique(const BPSmem& S, int c, unsigned self) 
 // Bit rows are computed one 128-candidate block at a time, only as far as the
 // greedy needs them (R picks usually come from the first block).
 template <int QV>
-__device__ int pt_prune(const float* __restrict__ X, int dp, const double* __restrict__ nrm64, const PTSmem& P,
+__device__ int pt_prune(const float* __restrict__ X, int dp, const PTAux& aux, const PTSmem& P,
                         PTPipe& pp, int c, double alpha2, int R, int* out, double* out_d, long long* exact_pairs) {
+    const bool f16 = aux.xh != nullptr;
+    const int rowbytes = f16 ? aux.kp * 2 : dp * 4;
     for (int x = threadIdx.x; x < c; x += PT_THREADS) {
         const unsigned id = P.S.ki2[x];
-        const double v = nrm64[id];
+        const double v = aux.nrm64[id];
         P.nrm[x] = v;
         P.sq[x] = sqrt(v);
-        P.rowp[x] = reinterpret_cast<unsigned long long>(X + (size_t)id * dp);
+        P.rowp[x] = f16 ? reinterpret_cast<unsigned long long>(aux.xh + (size_t)id * aux.kp)
+                        : reinterpret_cast<unsigned long long>(X + (size_t)id * dp);
+        // fp32 operands of the epilogue's first-pass decision (see pt_gram_pass)
+        const double Kq = P.S.kd2[x] / alpha2;
+        const double slack = 1e-14 * (Kq + v);
+        const double Au = Kq - v * (1.0 + 1e-12) - slack, Bu = Kq - v * (1.0 - 1e-12) + slack;
+        float af = __double2float_rd(Au), bf = __double2float_ru(Bu);
+        const float sf = __double2float_ru(P.sq[x]);
+        if (!(fabsf(af) < 1e30f) || !(fabsf(bf) < 1e30f) || !(sf < 1e30f)) af = bf = __int_as_float(0x7fc00000);
+        P.su32[x] = sf;
+        P.ab32[x] = make_float2(af, bf);
     }
     __syncthreads();
+    PT_TICK(1);
     const int lane = lane_id();
     const int nw = (c + 31) >> 5;
     unsigned alive = 0u;  // warp 0: lane l holds alive word l
@@ -423,7 +533,7 @@ __device__ int pt_prune(const float* __restrict__ X, int dp, const double* __res
     int sel = 0;
     long long nex = 0;
     for (int r0 = 0; r0 < c; r0 += 128) {
-        pt_gram_rows<QV>(X, dp, P, pp, c, r0, alpha2);
+        pt_gram_rows<QV>(X, dp, P, pp, c, r0, alpha2, rowbytes, f16);
         if ((threadIdx.x >> 5) == 0) {
             const bool done = pt_greedy_block<QV>(X, dp, P, c, r0, alpha2, R, out, out_d, alive, sel, nex);
             if (lane == 0) {
@@ -432,8 +542,11 @@ __device__ int pt_prune(const float* __restrict__ X, int dp, const double* __res
             }
         }
         __syncthreads();
+        PT_TICK(4);
         if (P.S.scal[9]) break;
     }
+    PT_COUNT(6, nex);
+    PT_COUNT(7, 1);
     if (threadIdx.x == 0 && exact_pairs) *exact_pairs += nex;
     const int r = P.S.scal[8];
     __syncthreads();
@@ -455,6 +568,7 @@ __device__ __forceinline__ void pt_setup(const PTSmem& P, PTPipe& pp) {
     tc_fence_after();
     pp.tmem = *P.tmem_slot;
     pp.phase = 0u;
+    pp.t0 = -1;  // phase timers: only the kernels that start them (PT_T0) are timed
 }
 
 __device__ __forceinline__ void pt_teardown(const PTSmem& P, const PTPipe& pp) {
@@ -469,7 +583,7 @@ __device__ __forceinline__ void pt_teardown(const PTSmem& P, const PTPipe& pp) {
 // build phase 2 for float data: one block per inserted point (items with more
 // than PT_CAP candidates are queued for build_prune_kernel)
 template <int QV>
-__global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs A, const double* __restrict__ nrm64,
+__global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs A, const PTAux aux,
                                                                       int* over, int* nover) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const PTSmem P = carve_pt<PT_CAP>(smem_raw);
@@ -481,6 +595,7 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
     const float* X = A.D.X;
     long long pairs = 0, exact_pairs = 0;
     for (int t = blockIdx.x; t < A.m; t += gridDim.x) {
+        PT_T0
         const unsigned p = (unsigned)A.bids[t];
         const int vl = A.vlen[t];
         const int nd = __ldg(A.P.deg + p);
@@ -512,6 +627,7 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
         __syncthreads();
         bp_sort(P.S.kd, P.S.ki, Pw);
         const int c = pt_unique<PT_CAP>(P.S, c0, p);
+        PT_TICK(0);
         if (c > PT_CAP) {  // more unique candidates than one Gram holds: warp path
             if (tid == 0) over[atomicAdd(nover, 1)] = t;
             __syncthreads();
@@ -527,7 +643,7 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
                 if (out_d) out_d[0] = P.S.kd2[0];
             }
         } else {
-            sel = pt_prune<QV>(X, dp, nrm64, P, pp, c, A.alpha2, R, out, out_d, &exact_pairs);
+            sel = pt_prune<QV>(X, dp, aux, P, pp, c, A.alpha2, R, out, out_d, &exact_pairs);
             if (tid == 0) pairs += (long long)c * (c - 1) / 2;
         }
         for (int x = sel + tid; x < R; x += PT_THREADS) {
@@ -536,6 +652,7 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
         }
         if (tid == 0) A.new_len[t] = sel;
         __syncthreads();
+        PT_TICK(5);
     }
     if (tid == 0 && A.stats && pairs)
         atomicAdd(reinterpret_cast<unsigned long long*>(A.stats + 1), (unsigned long long)(pairs + exact_pairs));
@@ -549,8 +666,7 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
 // launch (one CTA per SM) over items = mid.
 template <int MODE, int QV, int CAP>
 __global__ void __launch_bounds__(PT_THREADS, CAP == PT_CAP ? 2 : 1)
-    prune_tc_reverse_kernel(RevArgs A, const double* __restrict__ nrm64, const int* items, const int* nitems,
-                            int* mid, int* nmid) {
+    prune_tc_reverse_kernel(RevArgs A, const PTAux aux, const int* items, const int* nitems, int* mid, int* nmid) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const PTSmem P = carve_pt<CAP>(smem_raw);
     PTPipe pp;
@@ -623,7 +739,7 @@ __global__ void __launch_bounds__(PT_THREADS, CAP == PT_CAP ? 2 : 1)
                 sel = c;
             } else {
                 long long ex = 0;
-                sel = pt_prune<QV>(X, dp, nrm64, P, pp, c, A.alpha2, A.R, row, rowd, &ex);
+                sel = pt_prune<QV>(X, dp, aux, P, pp, c, A.alpha2, A.R, row, rowd, &ex);
                 if (tid == 0) ev += ex;
             }
             if (rowd)

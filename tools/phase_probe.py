@@ -43,11 +43,19 @@ p = pk.PointSet(data)
 for rep in range(2):
     read()
     read(fn="pk_phase_timers_build")
+    read(fn="pk_phase_timers_prune")
     idx = pk.build_vamana(p, R=w.R, L_build=w.L, alpha=w.alpha, seed=0, query_beam=w.L)
     torch.cuda.synchronize()
     b = read(fn="pk_phase_timers_build")
     idx.knn_batch_device(torch.arange(p.n, dtype=torch.int64, device="cuda"), w.k)
     torch.cuda.synchronize()
     q = read()
+pr = read(fn="pk_phase_timers_prune")
+if pr.sum():
+    names = ["cand+sort", "norms", "gram", "epilogue", "greedy", "output"]
+    tot = pr[:6].sum()
+    print("tc build prune:", "  ".join(f"{n} {100 * x / tot:.1f}%" for n, x in zip(names, pr[:6])),
+          f"(total {tot:.3e} block-cycles, {int(pr[7])} items, {pr[6] / max(1, pr[7]):.2f} exact pair decisions per item,"
+          f" {tot / max(1, pr[7]) / 1.965e3:.1f} us per item)")
 show("build searches:", b)
 show("knn_all:", q)
