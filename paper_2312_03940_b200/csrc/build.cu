@@ -87,8 +87,11 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
             PK_PT_END(6);
         }
         wb.walk(A.P, dist);
-        if constexpr (has_screen<decltype(dist)>::value)
+        if constexpr (has_screen<decltype(dist)>::value) {
+            PK_PT_BEGIN
             if (wb.lazy) wb.finalize_log(A.P, dist);
+            PK_PT_END(5);
+        }
         un += wb.uniq;
         ev += wb.evals;
         expansions += wb.vl;
