@@ -332,9 +332,10 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
     //   alpha^2 (d~ + E) <= K  <=>  (|t|^2 + c0) - 2 G~ + c1 |u| <= A_u = K / alpha^2 - |u|^2 (1 + 1e-12)
     //   alpha^2 (d~ - E) >  K  <=>  (|t|^2 - c0) - 2 G~ - c1 |u| >  B_u = K / alpha^2 - |u|^2 (1 - 1e-12)
     // Per-row and per-candidate terms are rounded outwards (pt_prune: su32, ab32),
-    // and `tol` covers the three fp32 roundings of each side, so a pair the fp32
-    // test calls is called the same way by exact arithmetic; every other pair
-    // (and any operand outside the fp32 range: NaN) takes the float64 form.
+    // and `tol` covers the fp32 roundings of each side, so a pair the fp32 test
+    // calls is called the same way by exact arithmetic; every other pair (and any
+    // operand outside the fp32 range: NaN) is "uncertain" -- the fp32 slack widens
+    // the uncertain band (2 E ~ 2^-9 |t||u|) by ~1e-6 of it.
     const double c1d = 2.0 * eg * st + 2.0 * eabs;
     const double c0d = 2.0 * eabs * (st + 1.0) + 1e-12 * nt;
     float Pt = __double2float_ru(nt + c0d), Mt = __double2float_rd(nt - c0d);
@@ -358,24 +359,11 @@ __device__ void pt_gram_pass(const float* __restrict__ X, int dp, const PTSmem& 
                         ub |= bit;
                         continue;
                     }
-                    {
-                        const float y = c1f * P.su32[u];
-                        const float2 ab = P.ab32[u];
-                        const float tol = fmaf(4e-7f, Pt + 2.f * fabsf(g[i]) + y, 1e-30f);
-                        if (fmaf(-2.f, g[i], Pt) + y + tol <= ab.x) {
-                            kb |= bit;
-                            continue;
-                        }
-                        if (fmaf(-2.f, g[i], Mt) - y - tol > ab.y) continue;
-                    }
-                    const double dt = nt + P.nrm[u] - 2.0 * (double)g[i];
-                    const double su = P.sq[u];
-                    const double E = 2.0 * (eg * st * su + eabs * (st + su + 1.0)) + 1e-12 * (nt + P.nrm[u]);
-                    const double K = P.S.kd2[u];
-                    const double hi = alpha2 * (dt + E) * (1.0 + 1e-12);
-                    const double lo = alpha2 * (dt - E) * (1.0 - 1e-12);
-                    if (hi <= K) kb |= bit;
-                    else if (!(lo > K)) ub |= bit;
+                    const float y = c1f * P.su32[u];
+                    const float2 ab = P.ab32[u];
+                    const float tol = fmaf(4e-7f, Pt + 2.f * fabsf(g[i]) + y, 1e-30f);
+                    if (fmaf(-2.f, g[i], Pt) + y + tol <= ab.x) kb |= bit;
+                    else if (!(fmaf(-2.f, g[i], Mt) - y - tol > ab.y)) ub |= bit;
                 }
             }
         }
@@ -410,13 +398,22 @@ __device__ bool pt_greedy_block(const float* __restrict__ X, int dp, const PTSme
                                 int R, int* out, double* out_d, unsigned& alive, int& sel, long long& nex) {
     const int lane = lane_id();
     const int nw = (c + 31) >> 5;
+    // the alive word the next pick comes from is also held warp-uniform (wl, aw),
+    // updated from a broadcast read of the pick's kill word: the serial chain per
+    // pick is ffs -> one shared-memory read -> and, without a ballot + shuffle
+    int wl = 0;
+    unsigned aw = 0u;
     while (sel < R) {
-        const unsigned nz = __ballot_sync(PK_FULL, alive != 0u);
-        if (!nz) return true;
-        const int wl = __ffs(nz) - 1;
-        const int t = 32 * wl + __ffs(__shfl_sync(PK_FULL, alive, wl)) - 1;
+        if (aw == 0u) {
+            const unsigned nz = __ballot_sync(PK_FULL, alive != 0u);
+            if (!nz) return true;
+            wl = __ffs(nz) - 1;
+            aw = __shfl_sync(PK_FULL, alive, wl);
+        }
+        const int t = 32 * wl + __ffs(aw) - 1;
         if (t >= r0 + 128) return false;
-        if (lane == wl) alive &= ~(1u << (t & 31));
+        aw &= aw - 1u;
+        if (lane == wl) alive = aw;
         const unsigned tid_t = P.S.ki2[t];
         if (lane == 0) {
             out[sel] = (int)tid_t;
@@ -426,6 +423,7 @@ __device__ bool pt_greedy_block(const float* __restrict__ X, int dp, const PTSme
         if (sel >= R) return true;
         const int row = (t - r0) * P.words;
         unsigned kill = lane < nw ? P.kill[row + lane] : 0u;
+        unsigned kill_wl = P.kill[row + wl];
         unsigned unc = lane < nw ? (P.unc[row + lane] & alive) : 0u;
         if (__any_sync(PK_FULL, unc != 0u)) {
             Fp32Pick<QV> pick;
@@ -451,9 +449,11 @@ __device__ bool pt_greedy_block(const float* __restrict__ X, int dp, const PTSme
                     ++nex;
                 }
                 if (lane == w) kill |= kw;
+                if (w == wl) kill_wl |= kw;
             }
         }
         alive &= ~kill;
+        aw &= ~kill_wl;
     }
     return true;
 }
@@ -596,6 +596,16 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
     long long pairs = 0, exact_pairs = 0;
     for (int t = blockIdx.x; t < A.m; t += gridDim.x) {
         PT_T0
+        {   // the next item's visit log (first 256 entries) on its way to L2 while this one is pruned
+            const int tn = t + gridDim.x;
+            if (tn < A.m && tid < 24) {
+                const bool ids = tid < 8;
+                const int off = 128 * (ids ? tid : tid - 8);
+                const char* a = ids ? reinterpret_cast<const char*>(A.vlog_i + (size_t)tn * A.vcap)
+                                    : reinterpret_cast<const char*>(A.vlog_d + (size_t)tn * A.vcap);
+                if (off < A.vcap * (ids ? 4 : 8)) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
+            }
+        }
         const unsigned p = (unsigned)A.bids[t];
         const int vl = A.vlen[t];
         const int nd = __ldg(A.P.deg + p);
