@@ -133,6 +133,7 @@ struct SearchParams {
     int prefetch = 1;          // L1 prefetch of the next expansion's adjacency row
     int prefetch_rows = 1;     // float data: L2 prefetch of every candidate row of an expansion (PK_PREFETCH_ROWS)
     int ring = 0;              // float data, lazy keys: slots of the per-warp row ring (0 = rows through registers)
+    int* ticket = nullptr;     // dynamic work assignment: next unprocessed position of the launch (zeroed before it)
     unsigned char* ghash = nullptr;  // seen tables in global memory (carve_beam_gh): [warps][ghash_stride]
     size_t ghash_stride = 0;
     int lazy = 1;              // float data: lazy keys (fp32 screen values until a decision needs the exact one)
@@ -154,6 +155,16 @@ struct SearchParams {
     const unsigned* seed_tab = nullptr;
     __device__ DataRef data() const { return DataRef{X, dp, X8, dw}; }
 };
+
+// Next position of a launch for this warp: a ticket from the shared counter
+// (searches differ in length, so a static stride leaves most warps idle while
+// the slowest finish their share), or the static stride without one.
+__device__ __forceinline__ int next_position(int* ticket, int prev, int stride) {
+    if (!ticket) return prev + stride;
+    int v = 0;
+    if (lane_id() == 0) v = atomicAdd(ticket, 1);
+    return __shfl_sync(PK_FULL, v, 0);
+}
 
 // strictly increasing start list (every warp checks once per launch)
 __device__ __forceinline__ bool starts_increasing(const SearchParams& P) {

@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
     const MakeAt<MODE, QV, RING> make{A.D};
     long long ev = 0, expansions = 0, un = 0;
     const bool uniq = starts_increasing(A.P);
-    for (int t = blockIdx.x * wpb + wib; t < A.m; t += gridDim.x * wpb) {
+    for (int t = next_position(A.P.ticket, blockIdx.x * wpb + wib - gridDim.x * wpb, gridDim.x * wpb); t < A.m;
+         t = next_position(A.P.ticket, t, gridDim.x * wpb)) {
         const unsigned p = (unsigned)A.bids[t];
         auto dist = make(p);
         WarpBeam<decltype(dist)> wb;
@@ -1460,6 +1461,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     A.P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && D.dp >= 512;  // measured: helps 4 KB rows (C5), not 1.5 KB (C4)
     A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
     A.P.ring = ring;
+    int* ticket = nullptr;
+    if (env_int("PK_TICKETS", 1) == 1) PK_CHECK(scratch(&ticket, 1, st));
     unsigned char* gh = nullptr;
     if (ghash) {
         A.P.ghash_stride = (size_t)H * 2;
@@ -1577,6 +1580,12 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         A.new_ids = new_ids + (size_t)my_lo * R;
         A.new_len = new_len + my_lo;
         if (my_m > 0) {
+            // tickets for the large batches (searches differ in length)
+            A.P.ticket = nullptr;
+            if (ticket && (long long)my_m > 2ll * grid_s * wpb_s) {
+                PK_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+                A.P.ticket = ticket;
+            }
             {
                 ProfScope _ps("build_search_kernel", st);
                 sk<<<std::min(grid_s, (my_m + wpb_s - 1) / wpb_s), 32 * wpb_s, A.search_bytes * wpb_s, st>>>(A);
@@ -1712,7 +1721,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
                     (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)xh, (void*)adjd, (void*)new_d,
-                    (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, (void*)gh, cub_tmp})
+                    (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, (void*)gh, (void*)ticket, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));
     if (herr) {

@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >=
     unsigned ring_t = 0;
     long long ev = 0, ex = 0, un = 0;
     const bool uniq = starts_increasing(P);
-    for (int t0 = blockIdx.x * wpb + wib; t0 < m; t0 += gridDim.x * wpb) {
+    for (int t0 = next_position(P.ticket, blockIdx.x * wpb + wib - gridDim.x * wpb, gridDim.x * wpb); t0 < m;
+         t0 = next_position(P.ticket, t0, gridDim.x * wpb)) {
         const int t = ord ? __ldg(ord + t0) : t0;  // processing order (locality) != output row order
         const unsigned qi = (unsigned)qids[t];
         auto dist = DistFor<MODE, QV, RING>::make(P.data(), qi);
@@ -454,6 +455,12 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
         PK_CHECK(scratch(&gh, (size_t)grid * wpb * Pr.ghash_stride, st));
         Pr.ghash = gh;
     }
+    int* ticket = nullptr;
+    if ((long long)m > 2ll * grid * wpb && env_int("PK_TICKETS", 1) == 1) {
+        PK_CHECK(scratch(&ticket, 1, st));
+        PK_CHECK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+        Pr.ticket = ticket;
+    }
     int* ord = nullptr;
     if (P.seed_load && m >= (1 << 16) && env_int("PK_LOCALITY", 1) == 1) {
         const int rc = query_locality_order(P, qids, m, L, P.n_points, &ord, st);
@@ -477,6 +484,7 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     if (ubm) release(ubm, st);
     if (gbeam) release(gbeam, st);
     if (gh) release(gh, st);
+    if (ticket) release(ticket, st);
     if (ord) release(ord, st);
     return 0;
 }
