@@ -54,9 +54,9 @@ inline size_t spill_smem_bytes(int H) { return (((size_t)H * 2 + 15) & ~(size_t)
 inline size_t spill_slab_bytes(int L) { return ((size_t)L * 12 + 15) & ~(size_t)15; }
 // row ring behind the beam state (carve_ring): slots x dp floats + one mbarrier per slot
 inline size_t ring_smem_bytes(int dp, int slots) { return slots ? (size_t)slots * dp * 4 + (size_t)slots * 8 : 0; }
-// slots of the row ring for a float search with lazy keys (PK_RING, default 2,
-// a power of two; 0 = rows through registers): rows of >= 1 KB that the fp32
-// screen covers
+// slots of the row ring for a float search with lazy keys (PK_RING = 2 or 4; default
+// 0 = rows through registers, which is faster since the searches are handed out by
+// tickets -- profiles/r2_ring_ab.md): rows of >= 1 KB that the fp32 screen covers
 inline int ring_slots(int dp, int qv, bool lazy_screen);
 inline size_t sort_smem_bytes(int cap) {
     return (size_t)cap * 13 + 128;
@@ -82,7 +82,7 @@ inline int env_int(const char* name, int dflt) {
 
 inline int ring_slots(int dp, int qv, bool lazy_screen) {
     if (!lazy_screen || dp < 256 || dp > 128 * qv) return 0;
-    int s = env_int("PK_RING", 2);
+    int s = env_int("PK_RING", 0);
     if (s <= 0) return 0;
     if (s > 8) s = 8;
     while (s & (s - 1)) s &= s - 1;  // power of two

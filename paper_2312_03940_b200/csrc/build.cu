@@ -1381,7 +1381,9 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         }
         PK_CHECK_LAUNCH("rows_to_half_kernel");
     }
-    const PTAux aux{nrm64, xh, kph};
+    int* ptick = nullptr;  // item counters of the tensor-core prune launches: [0] build, [1] reverse, [2] reverse (big groups)
+    if (tcp) PK_CHECK(scratch(&ptick, 4, st));
+    PTAux aux{nrm64, xh, kph, nullptr};
     const int capB = 8192;
     const size_t big_bytes = (size_t)capB * 13 + 16;
     auto bigk = reverse_big_kernel<MODE, QV>;
@@ -1457,8 +1459,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
 
     A.P = SearchParams{D.X, D.dp, adj, R, deg, starts, s};
     A.P.screen = D.screen;
-    A.P.prefetch = env_int("PK_PREFETCH", 1) == 1;
-    A.P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && D.dp >= 512;  // measured: helps 4 KB rows (C5), not 1.5 KB (C4)
+    A.P.prefetch = env_int("PK_PREFETCH", 0) == 1;  // adjacency-row L1 prefetch: measured slower on every configuration
+    A.P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 0) == 1 && D.dp >= 512;  // L2 prefetch of candidate rows: a gain before the ticket scheduling, a 2 % loss since
     A.P.lazy = env_int("PK_LAZY", 1) == 1 && n < (long long)PK_IDMASK;
     A.P.ring = ring;
     int* ticket = nullptr;
@@ -1594,6 +1596,8 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             if (blockp || tcb) {
                 PK_CHECK(cudaMemsetAsync(nover, 0, sizeof(int), st));
                 if (tcb) {
+                    PK_CHECK(cudaMemsetAsync(ptick, 0, 4 * sizeof(int), st));
+                    aux.ticket = ptick;
                     ProfScope _ps("prune_tc_build_kernel", st);
                     tpk<<<std::min(2 * sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, aux, over, nover);
                 } else {
@@ -1668,12 +1672,15 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             }
         } else if (tcr) {
             PK_CHECK(cudaMemsetAsync(nmid, 0, sizeof(int), st));
+            if (!tcb) PK_CHECK(cudaMemsetAsync(ptick, 0, 4 * sizeof(int), st));
             {
+                aux.ticket = ptick + 1;
                 ProfScope _ps("prune_tc_reverse_kernel", st);
                 trk<<<std::min(2 * sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, aux, nullptr, nullptr, midl, nmid);
             }
             PK_CHECK_LAUNCH("prune_tc_reverse_kernel");
             {
+                aux.ticket = ptick + 2;
                 ProfScope _ps("prune_tc_reverse_kernel", st);
                 trk2<<<sm_count(), PT_THREADS, pt_smem_bytes(PT_CAP_BIG), st>>>(B, aux, midl, nmid, nullptr, nullptr);
             }
@@ -1720,7 +1727,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
                     (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
-                    (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)xh, (void*)adjd, (void*)new_d,
+                    (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)xh, (void*)ptick, (void*)adjd, (void*)new_d,
                     (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, (void*)gh, (void*)ticket, cub_tmp})
         release(p, st);
     PK_CHECK(cudaStreamSynchronize(st));

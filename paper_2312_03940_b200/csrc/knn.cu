@@ -660,8 +660,8 @@ extern "C" int pk_beam_knn_seeded(const float* x, int64_t n, int64_t dp, const u
     SearchParams P{x, (int)dp, adj, (int)R, deg, starts, (int)s, x8, (int)dw};
     P.screen = env_int("PK_SCREEN", 1) == 1;
     P.n_points = n;
-    P.prefetch = env_int("PK_PREFETCH", 1) == 1;
-    P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 1) == 1 && dp >= 512;  // measured: helps rows of 4 KB (C5), not 1.5 KB (C4)
+    P.prefetch = env_int("PK_PREFETCH", 0) == 1;  // adjacency-row L1 prefetch: measured slower on every configuration
+    P.prefetch_rows = env_int("PK_PREFETCH_ROWS", 0) == 1 && dp >= 512;  // L2 prefetch of candidate rows: a gain before the ticket scheduling, a 2 % loss since
     P.lazy = env_int("PK_LAZY", 1) == 1 && n < (int64_t)PK_IDMASK;
     P.seed_only = env_int("PK_SEED_ONLY", 0);
     P.seed_select = env_int("PK_SEED_SELECT", 1);

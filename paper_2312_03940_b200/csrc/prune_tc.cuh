@@ -175,6 +175,28 @@ struct PTAux {
     const double* nrm64;
     const __half* xh;
     int kp;
+    int* ticket;  // this launch's item counter (zeroed before it): items are handed out one at a time
+};
+
+// Next item of the launch for this block (thread 0 takes a ticket, the block
+// reads it after the next __syncthreads): items differ in cost (reverse groups
+// of 65 .. 512 candidates), so a static stride leaves blocks idle at the end.
+struct PTTickets {
+    int* slot;  // two shared ints, alternating
+    int par;
+    __device__ int first(int* ticket) {
+        par = 0;
+        if (threadIdx.x == 0) slot[0] = atomicAdd(ticket, 1);
+        __syncthreads();
+        return slot[0];
+    }
+    // call at the top of an item (takes the following item's ticket) ...
+    __device__ void take_next(int* ticket) {
+        par ^= 1;
+        if (threadIdx.x == 0) slot[par] = atomicAdd(ticket, 1);
+    }
+    // ... and at its end, after a __syncthreads
+    __device__ int next() const { return slot[par]; }
 };
 
 // fp16 copy of every row (round to nearest), K padded with zeros to kp
@@ -594,18 +616,11 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
     const int dp = A.D.dp;
     const float* X = A.D.X;
     long long pairs = 0, exact_pairs = 0;
-    for (int t = blockIdx.x; t < A.m; t += gridDim.x) {
+    __shared__ int s_tick[2];
+    PTTickets tk{s_tick, 0};
+    for (int t = tk.first(aux.ticket); t < A.m; __syncthreads(), t = tk.next()) {
         PT_T0
-        {   // the next item's visit log (first 256 entries) on its way to L2 while this one is pruned
-            const int tn = t + gridDim.x;
-            if (tn < A.m && tid < 24) {
-                const bool ids = tid < 8;
-                const int off = 128 * (ids ? tid : tid - 8);
-                const char* a = ids ? reinterpret_cast<const char*>(A.vlog_i + (size_t)tn * A.vcap)
-                                    : reinterpret_cast<const char*>(A.vlog_d + (size_t)tn * A.vcap);
-                if (off < A.vcap * (ids ? 4 : 8)) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
-            }
-        }
+        tk.take_next(aux.ticket);
         const unsigned p = (unsigned)A.bids[t];
         const int vl = A.vlen[t];
         const int nd = __ldg(A.P.deg + p);
@@ -687,7 +702,10 @@ __global__ void __launch_bounds__(PT_THREADS, CAP == PT_CAP ? 2 : 1)
     const float* X = A.X;
     const int nt = items ? *nitems : *A.ntargets;
     long long ev = 0;
-    for (int it = blockIdx.x; it < nt; it += gridDim.x) {
+    __shared__ int s_tick[2];
+    PTTickets tk{s_tick, 0};
+    for (int it = tk.first(aux.ticket); it < nt; __syncthreads(), it = tk.next()) {
+        tk.take_next(aux.ticket);
         const int s = items ? items[it] : it;
         const unsigned u = (unsigned)A.targets[s];
         if (A.world > 1 && (int)(u % (unsigned)A.world) != A.rank) {
