@@ -166,6 +166,35 @@ __device__ __forceinline__ int next_position(int* ticket, int prev, int stride) 
     return __shfl_sync(PK_FULL, v, 0);
 }
 
+// The same for kernels that give one item to a block: thread 0 takes a ticket,
+// the block reads it after the next __syncthreads.  Items differ in cost
+// (reverse groups of 65 .. 8,192 candidates), so a static stride leaves blocks
+// idle at the end of a launch.  `ticket` null: static stride.
+struct BlockTickets {
+    int* slot;  // two shared ints, alternating
+    int par;
+    int stat;   // static position (no ticket counter)
+    __device__ int first(int* ticket) {
+        par = 0;
+        stat = blockIdx.x;
+        if (!ticket) return stat;
+        if (threadIdx.x == 0) slot[0] = atomicAdd(ticket, 1);
+        __syncthreads();
+        return slot[0];
+    }
+    // call at the top of an item (takes the following item's ticket) ...
+    __device__ void take_next(int* ticket) {
+        if (!ticket) {
+            stat += gridDim.x;
+            return;
+        }
+        par ^= 1;
+        if (threadIdx.x == 0) slot[par] = atomicAdd(ticket, 1);
+    }
+    // ... and at its end, after a __syncthreads
+    __device__ int next(int* ticket) const { return ticket ? slot[par] : stat; }
+};
+
 // strictly increasing start list (every warp checks once per launch)
 __device__ __forceinline__ bool starts_increasing(const SearchParams& P) {
     bool ok = true;

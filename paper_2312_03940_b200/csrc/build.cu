@@ -29,6 +29,7 @@ namespace pk {
 int grid_for(long long work, int block);
 
 struct BuildArgs {
+    int* ticket = nullptr;  // this launch's item counter (BlockTickets; block-per-item prune kernels)
     SearchParams P;
     DataRef D;
     const int* bids;
@@ -302,6 +303,7 @@ __global__ void scatter_kernel(const int* bids, int m, int R, const int* new_ids
 }
 
 struct RevArgs {
+    int* ticket = nullptr;  // this launch's item counter (BlockTickets), zeroed before it
     const float* X;
     int dp;
     DataRef D;
@@ -857,7 +859,10 @@ __global__ void __launch_bounds__(BP_THREADS) build_prune_block_kernel(BuildArgs
     const int tid = threadIdx.x;
     const int R = A.P.R;
     long long pairs = 0;
-    for (int t = blockIdx.x; t < A.m; t += gridDim.x) {
+    __shared__ int s_tick[2];
+    BlockTickets tk{s_tick, 0, 0};
+    for (int t = tk.first(A.ticket); t < A.m; __syncthreads(), t = tk.next(A.ticket)) {
+        tk.take_next(A.ticket);
         const unsigned p = (unsigned)A.bids[t];
         const int vl = A.vlen[t];
         const int nd = __ldg(A.P.deg + p);
@@ -931,7 +936,10 @@ __global__ void __launch_bounds__(BP_THREADS) reverse_block_kernel(RevArgs A, in
     const MakeAt<MODE, QV> make{A.D};
     const int nt = items ? *nitems : *A.ntargets;
     long long ev = 0;
-    for (int it = blockIdx.x; it < nt; it += gridDim.x) {
+    __shared__ int s_tick[2];
+    BlockTickets tk{s_tick, 0, 0};
+    for (int it = tk.first(A.ticket); it < nt; __syncthreads(), it = tk.next(A.ticket)) {
+        tk.take_next(A.ticket);
         const int s = items ? items[it] : it;
         const unsigned u = (unsigned)A.targets[s];
         if (A.world > 1 && (int)(u % (unsigned)A.world) != A.rank) {
@@ -1038,7 +1046,10 @@ __global__ void __launch_bounds__(kBigThreads) reverse_big_kernel(RevArgs A) {
     const int tid = threadIdx.x;
     const int nb = *A.nbig;
     long long ev = 0;
-    for (int g = blockIdx.x; g < nb; g += gridDim.x) {
+    __shared__ int s_tick[2];
+    BlockTickets tk{s_tick, 0, 0};
+    for (int g = tk.first(A.ticket); g < nb; __syncthreads(), g = tk.next(A.ticket)) {
+        tk.take_next(A.ticket);
         const int s = A.biglist[g];
         const unsigned u = (unsigned)A.targets[s];
         const int nd = A.deg[u];
@@ -1381,8 +1392,10 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         }
         PK_CHECK_LAUNCH("rows_to_half_kernel");
     }
-    int* ptick = nullptr;  // item counters of the tensor-core prune launches: [0] build, [1] reverse, [2] reverse (big groups)
-    if (tcp) PK_CHECK(scratch(&ptick, 4, st));
+    // item counters of the block-per-item launches of a batch (BlockTickets), zeroed once per batch:
+    // [0] build prune, [1..3] reverse launches, [4] reverse_big_kernel
+    int* ptick = nullptr;
+    if (env_int("PK_TICKETS", 1) == 1) PK_CHECK(scratch(&ptick, 8, st));
     PTAux aux{nrm64, xh, kph, nullptr};
     const int capB = 8192;
     const size_t big_bytes = (size_t)capB * 13 + 16;
@@ -1581,6 +1594,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         A.m = my_m;
         A.new_ids = new_ids + (size_t)my_lo * R;
         A.new_len = new_len + my_lo;
+        if (ptick) PK_CHECK(cudaMemsetAsync(ptick, 0, 8 * sizeof(int), st));
         if (my_m > 0) {
             // tickets for the large batches (searches differ in length)
             A.P.ticket = nullptr;
@@ -1595,9 +1609,9 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             PK_CHECK_LAUNCH("build_search_kernel");
             if (blockp || tcb) {
                 PK_CHECK(cudaMemsetAsync(nover, 0, sizeof(int), st));
+                aux.ticket = ptick;
+                A.ticket = ptick;
                 if (tcb) {
-                    PK_CHECK(cudaMemsetAsync(ptick, 0, 4 * sizeof(int), st));
-                    aux.ticket = ptick;
                     ProfScope _ps("prune_tc_build_kernel", st);
                     tpk<<<std::min(2 * sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, aux, over, nover);
                 } else {
@@ -1654,6 +1668,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         if (blockp) {
             PK_CHECK(cudaMemsetAsync(nmid, 0, sizeof(int), st));
             {
+                B.ticket = ptick ? ptick + 1 : nullptr;
                 ProfScope _ps("reverse_block_kernel", st);
                 rbk<<<std::min(grid_rb, ubb), BP_THREADS, bp_smem_bytes(kRevCap), st>>>(B, kRevCap, nullptr, nullptr,
                                                                                        midl, nmid);
@@ -1661,26 +1676,27 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             PK_CHECK_LAUNCH("reverse_block_kernel");
             PK_CHECK(cudaMemsetAsync(nmid2, 0, sizeof(int), st));
             {
+                B.ticket = ptick ? ptick + 2 : nullptr;
                 ProfScope _ps("reverse_block_kernel", st);
                 rbk<<<grid_bp, BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(B, BP_CAP, midl, nmid, midl2, nmid2);
             }
             PK_CHECK_LAUNCH("reverse_block_kernel");
             {
+                B.ticket = ptick ? ptick + 3 : nullptr;
                 ProfScope _ps("reverse_block_kernel", st);
                 rbk<<<2 * sm_count(), BP_THREADS, bp_smem_bytes(BP_CAP_MAX), st>>>(B, BP_CAP_MAX, midl2, nmid2,
                                                                                    nullptr, nullptr);
             }
         } else if (tcr) {
             PK_CHECK(cudaMemsetAsync(nmid, 0, sizeof(int), st));
-            if (!tcb) PK_CHECK(cudaMemsetAsync(ptick, 0, 4 * sizeof(int), st));
             {
-                aux.ticket = ptick + 1;
+                aux.ticket = ptick ? ptick + 1 : nullptr;
                 ProfScope _ps("prune_tc_reverse_kernel", st);
                 trk<<<std::min(2 * sm_count(), ubb), PT_THREADS, PT_SMEM, st>>>(B, aux, nullptr, nullptr, midl, nmid);
             }
             PK_CHECK_LAUNCH("prune_tc_reverse_kernel");
             {
-                aux.ticket = ptick + 2;
+                aux.ticket = ptick ? ptick + 2 : nullptr;
                 ProfScope _ps("prune_tc_reverse_kernel", st);
                 trk2<<<sm_count(), PT_THREADS, pt_smem_bytes(PT_CAP_BIG), st>>>(B, aux, midl, nmid, nullptr, nullptr);
             }
@@ -1690,6 +1706,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         }
         PK_CHECK_LAUNCH("reverse_kernel");
         {
+            B.ticket = ptick ? ptick + 4 : nullptr;
             ProfScope _ps("reverse_big_kernel", st);
             bigk<<<grid_big, kBigThreads, big_bytes, st>>>(B);
         }

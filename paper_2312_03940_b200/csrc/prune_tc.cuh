@@ -178,26 +178,7 @@ struct PTAux {
     int* ticket;  // this launch's item counter (zeroed before it): items are handed out one at a time
 };
 
-// Next item of the launch for this block (thread 0 takes a ticket, the block
-// reads it after the next __syncthreads): items differ in cost (reverse groups
-// of 65 .. 512 candidates), so a static stride leaves blocks idle at the end.
-struct PTTickets {
-    int* slot;  // two shared ints, alternating
-    int par;
-    __device__ int first(int* ticket) {
-        par = 0;
-        if (threadIdx.x == 0) slot[0] = atomicAdd(ticket, 1);
-        __syncthreads();
-        return slot[0];
-    }
-    // call at the top of an item (takes the following item's ticket) ...
-    __device__ void take_next(int* ticket) {
-        par ^= 1;
-        if (threadIdx.x == 0) slot[par] = atomicAdd(ticket, 1);
-    }
-    // ... and at its end, after a __syncthreads
-    __device__ int next() const { return slot[par]; }
-};
+using PTTickets = BlockTickets;
 
 // fp16 copy of every row (round to nearest), K padded with zeros to kp
 __global__ void rows_to_half_kernel(const float* __restrict__ X, long long n, int dp, int kp, __half* __restrict__ out) {
@@ -617,8 +598,8 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
     const float* X = A.D.X;
     long long pairs = 0, exact_pairs = 0;
     __shared__ int s_tick[2];
-    PTTickets tk{s_tick, 0};
-    for (int t = tk.first(aux.ticket); t < A.m; __syncthreads(), t = tk.next()) {
+    PTTickets tk{s_tick, 0, 0};
+    for (int t = tk.first(aux.ticket); t < A.m; __syncthreads(), t = tk.next(aux.ticket)) {
         PT_T0
         tk.take_next(aux.ticket);
         const unsigned p = (unsigned)A.bids[t];
@@ -703,8 +684,8 @@ __global__ void __launch_bounds__(PT_THREADS, CAP == PT_CAP ? 2 : 1)
     const int nt = items ? *nitems : *A.ntargets;
     long long ev = 0;
     __shared__ int s_tick[2];
-    PTTickets tk{s_tick, 0};
-    for (int it = tk.first(aux.ticket); it < nt; __syncthreads(), it = tk.next()) {
+    PTTickets tk{s_tick, 0, 0};
+    for (int it = tk.first(aux.ticket); it < nt; __syncthreads(), it = tk.next(aux.ticket)) {
         tk.take_next(aux.ticket);
         const int s = items ? items[it] : it;
         const unsigned u = (unsigned)A.targets[s];
