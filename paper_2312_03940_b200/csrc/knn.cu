@@ -13,7 +13,9 @@ namespace pk {
 // RING (float data, QV >= 4): candidate rows staged through the per-warp row
 // ring (bulk copies into shared memory) instead of registers
 template <int MODE, int QV, bool RING>
-__global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 4 : QV >= 4 ? 5 : 8) : 8) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
+// (float data: 5 blocks of 96 registers at QV = 8 and 6 blocks of 80 at QV = 4 measured best
+// for the member queries -- C5 1.22 -> 1.20 s, C4 0.85 -> 0.73 s; the build searches keep 4 / 5)
+__global__ void __launch_bounds__(128, MODE == MODE_SEQ64 ? (QV >= 8 ? 5 : QV >= 4 ? 6 : 8) : 8) beam_knn_kernel(SearchParams P, const long long* __restrict__ qids, int m,
                                                        int L, int kk, int H, size_t warp_bytes,
                                                        long long* __restrict__ out_ids, double* __restrict__ out_d,
                                                        long long* __restrict__ counts, long long* evals_out,
