@@ -358,24 +358,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1) tc_sc
 // fp16 rows (K padded to a multiple of 64 with zeros) and fp32 squared norms
 __global__ void tc_prep_kernel(const float* __restrict__ X, int dp, const long long* rows, int m, int kp,
                                __half* out, float* nrm) {
-    const int r = blockIdx.x;
-    if (r >= m) return;
-    const long long src = rows ? rows[r] : r;
-    const float* x = X + (size_t)src * dp;
-    double acc = 0.0;
-    for (int t = threadIdx.x; t < kp; t += blockDim.x) {
-        const float v = t < dp ? x[t] : 0.f;
-        out[(size_t)r * kp + t] = __float2half_rn(v);
-        acc += (double)v * (double)v;
-    }
-    __shared__ double red[8];
-    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, s);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double tot = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
-        nrm[r] = (float)tot;
+    // one warp per row (a block per row spent its time launching: 31 ms for the
+    // 1.28 M rows of C5 where the copy needs ~1.5 ms of HBM time)
+    const int lane = threadIdx.x & 31;
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = w; r < m; r += nw) {
+        const long long src = rows ? rows[r] : r;
+        const float* x = X + (size_t)src * dp;
+        __half2* o = reinterpret_cast<__half2*>(out + (size_t)r * kp);
+        double acc = 0.0;
+        // dp is a multiple of 4 (16-byte rows), kp a multiple of 64
+        for (int t = lane * 4; t < kp; t += 128) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t < dp) v = *reinterpret_cast<const float4*>(x + t);
+            o[t >> 1] = __halves2half2(__float2half_rn(v.x), __float2half_rn(v.y));
+            o[(t >> 1) + 1] = __halves2half2(__float2half_rn(v.z), __float2half_rn(v.w));
+            acc += (double)v.x * (double)v.x + (double)v.y * (double)v.y + (double)v.z * (double)v.z +
+                   (double)v.w * (double)v.w;
+        }
+        for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(PK_FULL, acc, s);
+        if (lane == 0) nrm[r] = (float)acc;
     }
 }
 
@@ -547,9 +550,9 @@ static int tc_knn_core(const float* x, int64_t n, int64_t dp, const int64_t* qid
     PK_CHECK(scratch(&pmax, 1, st));
     {
         ProfScope _ps("tc_prep_kernel", st);
-        tc_prep_kernel<<<(unsigned)m, 256, 0, st>>>(x, (int)dp, reinterpret_cast<const long long*>(qids), (int)m, kp,
+        tc_prep_kernel<<<(unsigned)std::min<long long>(((long long)(m) + 7) / 8, 148ll * 32), 256, 0, st>>>(x, (int)dp, reinterpret_cast<const long long*>(qids), (int)m, kp,
                                                     qh, qn);
-        tc_prep_kernel<<<(unsigned)n, 256, 0, st>>>(x, (int)dp, nullptr, (int)n, kp, ph, pn);
+        tc_prep_kernel<<<(unsigned)std::min<long long>(((long long)(n) + 7) / 8, 148ll * 32), 256, 0, st>>>(x, (int)dp, nullptr, (int)n, kp, ph, pn);
     }
     PK_CHECK(cudaMemsetAsync(pmax, 0, sizeof(float), st));
     {
@@ -711,7 +714,7 @@ int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int ta
     widen_ids_kernel<<<(s + 255) / 256, 256, 0, st>>>(starts, s, sid);
     {
         ProfScope _ps("tc_prep_kernel", st);
-        tc_prep_kernel<<<(unsigned)s, 256, 0, st>>>(x, dp, sid, s, kp, ph, pn);
+        tc_prep_kernel<<<(unsigned)std::min<long long>(((long long)(s) + 7) / 8, 148ll * 32), 256, 0, st>>>(x, dp, sid, s, kp, ph, pn);
     }
     PK_CHECK(cudaMemsetAsync(smax2, 0, sizeof(float), st));
     {
@@ -737,7 +740,7 @@ int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int ta
         const int rows = std::min(chunk, n - r0);
         {
             ProfScope _ps("tc_prep_kernel", st);
-            tc_prep_kernel<<<(unsigned)rows, 256, 0, st>>>(x + (size_t)r0 * dp, dp, nullptr, rows, kp, qh, qn);
+            tc_prep_kernel<<<(unsigned)std::min<long long>(((long long)(rows) + 7) / 8, 148ll * 32), 256, 0, st>>>(x + (size_t)r0 * dp, dp, nullptr, rows, kp, qh, qn);
         }
         if ((rc = make_map(&mq, qh, rows, kp, TC_BM))) return rc;
         TcArgs A;
@@ -840,8 +843,8 @@ int tc_count_decide(const float* x, int n, int dp, const long long* qids, int m,
     PK_CHECK(scratch(&hi, (size_t)m, st));
     {
         ProfScope _ps("tc_prep_kernel", st);
-        tc_prep_kernel<<<(unsigned)m, 256, 0, st>>>(x, dp, qids, m, kp, qh, qn);
-        tc_prep_kernel<<<(unsigned)n, 256, 0, st>>>(x, dp, nullptr, n, kp, ph, pn);
+        tc_prep_kernel<<<(unsigned)std::min<long long>(((long long)(m) + 7) / 8, 148ll * 32), 256, 0, st>>>(x, dp, qids, m, kp, qh, qn);
+        tc_prep_kernel<<<(unsigned)std::min<long long>(((long long)(n) + 7) / 8, 148ll * 32), 256, 0, st>>>(x, dp, nullptr, n, kp, ph, pn);
     }
     PK_CHECK(cudaMemsetAsync(pmax2, 0, sizeof(float), st));
     PK_CHECK(cudaMemsetAsync(lo, 0, sizeof(unsigned) * (size_t)m, st));
