@@ -1364,12 +1364,15 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     const int tcmode = env_int("PK_TC_PRUNE", 1);  // 1: build + reverse, 2: build only, 3: reverse only
     const bool tcp = MODE == MODE_SEQ64 && D.dp <= 128 * QV && QV <= 8 && D.screen && tcmode >= 1 && tcmode <= 3;
     const bool tcb = tcp && tcmode != 3, tcr = tcp && tcmode != 2;
-    auto tpk = prune_tc_build_kernel<QV>;
+    auto tpk = prune_tc_build_kernel<QV, PT_CAP>;
+    auto tpk2 = prune_tc_build_kernel<QV, PT_CAP_BIG>;
     auto trk = prune_tc_reverse_kernel<MODE, QV, PT_CAP>;
     auto trk2 = prune_tc_reverse_kernel<MODE, QV, PT_CAP_BIG>;
     double* nrm64 = nullptr;
     if (tcp) {
         PK_CHECK(cudaFuncSetAttribute(tpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_SMEM));
+        PK_CHECK(cudaFuncSetAttribute(tpk2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)pt_smem_bytes(PT_CAP_BIG)));
         PK_CHECK(cudaFuncSetAttribute(trk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_SMEM));
         PK_CHECK(cudaFuncSetAttribute(trk2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)pt_smem_bytes(PT_CAP_BIG)));
@@ -1439,9 +1442,10 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     }
     int* npack = nullptr;
     PK_CHECK(scratch(&npack, 1, st));
-    int *over = nullptr, *nover = nullptr;
+    int *over = nullptr, *nover = nullptr, *over1 = nullptr;  // over1 / nover[1]: first tensor-core launch's queue
     PK_CHECK(scratch(&over, (size_t)mb, st));
-    PK_CHECK(scratch(&nover, 1, st));
+    PK_CHECK(scratch(&over1, (size_t)mb, st));
+    PK_CHECK(scratch(&nover, 2, st));
     int *midl = nullptr, *nmid = nullptr, *midl2 = nullptr, *nmid2 = nullptr;
     PK_CHECK(scratch(&midl, (size_t)ub, st));
     PK_CHECK(scratch(&nmid, 1, st));
@@ -1608,12 +1612,19 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             }
             PK_CHECK_LAUNCH("build_search_kernel");
             if (blockp || tcb) {
-                PK_CHECK(cudaMemsetAsync(nover, 0, sizeof(int), st));
+                PK_CHECK(cudaMemsetAsync(nover, 0, 2 * sizeof(int), st));
                 aux.ticket = ptick;
                 A.ticket = ptick;
                 if (tcb) {
+                    {
+                        ProfScope _ps("prune_tc_build_kernel", st);
+                        tpk<<<std::min(2 * sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, aux, nullptr, nullptr, over1,
+                                                                                         nover + 1);
+                    }
+                    aux.ticket = ptick ? ptick + 5 : nullptr;
                     ProfScope _ps("prune_tc_build_kernel", st);
-                    tpk<<<std::min(2 * sm_count(), my_m), PT_THREADS, PT_SMEM, st>>>(A, aux, over, nover);
+                    tpk2<<<std::min(sm_count(), my_m), PT_THREADS, pt_smem_bytes(PT_CAP_BIG), st>>>(A, aux, over1, nover + 1,
+                                                                                                  over, nover);
                 } else {
                     ProfScope _ps("build_prune_block_kernel", st);
                     bpk<<<std::min(grid_bp, my_m), BP_THREADS, bp_smem_bytes(BP_CAP), st>>>(A, over, nover);
@@ -1743,7 +1754,7 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     }
     for (void* p : {(void*)vlog_i, (void*)vlog_d, (void*)vlen, (void*)cnt, (void*)tslot, (void*)targets, (void*)sizes,
                     (void*)offs, (void*)fill, (void*)adds, (void*)adist, (void*)aalive, (void*)ntargets, (void*)err,
-                    (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)nover, (void*)midl,
+                    (void*)biglist, (void*)nbig, (void*)npack, (void*)over, (void*)over1, (void*)nover, (void*)midl,
                     (void*)nmid, (void*)midl2, (void*)nmid2, (void*)ubm, (void*)nrm64, (void*)xh, (void*)ptick, (void*)adjd, (void*)new_d,
                     (void*)addd, (void*)seed_mask, (void*)seed_tab, (void*)near, (void*)lorder, (void*)gh, (void*)ticket, cub_tmp})
         release(p, st);

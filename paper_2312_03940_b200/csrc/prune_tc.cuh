@@ -585,11 +585,15 @@ __device__ __forceinline__ void pt_teardown(const PTSmem& P, const PTPipe& pp) {
 
 // build phase 2 for float data: one block per inserted point (items with more
 // than PT_CAP candidates are queued for build_prune_kernel)
-template <int QV>
-__global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs A, const PTAux aux,
-                                                                      int* over, int* nover) {
+// CAP = PT_CAP (two CTAs per SM) over the whole batch, then CAP = PT_CAP_BIG (one
+// CTA per SM) over the items the first launch queued on (over, nover); what
+// that one queues goes to build_prune_kernel (a warp per item: 20 ms for a
+// 600-candidate item, which a launch then waits for)
+template <int QV, int CAP>
+__global__ void __launch_bounds__(PT_THREADS, CAP == PT_CAP ? 2 : 1)
+    prune_tc_build_kernel(BuildArgs A, const PTAux aux, const int* items, const int* nitems, int* over, int* nover) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const PTSmem P = carve_pt<PT_CAP>(smem_raw);
+    const PTSmem P = carve_pt<CAP>(smem_raw);
     PTPipe pp;
     pt_setup(P, pp);
     const int tid = threadIdx.x;
@@ -599,14 +603,16 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
     long long pairs = 0, exact_pairs = 0;
     __shared__ int s_tick[2];
     PTTickets tk{s_tick, 0, 0};
-    for (int t = tk.first(aux.ticket); t < A.m; __syncthreads(), t = tk.next(aux.ticket)) {
+    const int total = items ? *nitems : A.m;
+    for (int it = tk.first(aux.ticket); it < total; __syncthreads(), it = tk.next(aux.ticket)) {
         PT_T0
         tk.take_next(aux.ticket);
+        const int t = items ? items[it] : it;
         const unsigned p = (unsigned)A.bids[t];
         const int vl = A.vlen[t];
         const int nd = __ldg(A.P.deg + p);
         const int c0 = vl + nd;
-        if (c0 > PT_CAP) {
+        if (c0 > CAP) {
             if (tid == 0) over[atomicAdd(nover, 1)] = t;
             continue;
         }
@@ -632,9 +638,9 @@ __global__ void __launch_bounds__(PT_THREADS, 2) prune_tc_build_kernel(BuildArgs
         }
         __syncthreads();
         bp_sort(P.S.kd, P.S.ki, Pw);
-        const int c = pt_unique<PT_CAP>(P.S, c0, p);
+        const int c = pt_unique<CAP>(P.S, c0, p);
         PT_TICK(0);
-        if (c > PT_CAP) {  // more unique candidates than one Gram holds: warp path
+        if (c > CAP) {  // more unique candidates than one Gram holds: warp path
             if (tid == 0) over[atomicAdd(nover, 1)] = t;
             __syncthreads();
             continue;
