@@ -680,3 +680,30 @@ def test_seeded_beam_cache_equals_fresh_seeding(monkeypatch, case):
         out[flag] = [st.neighbors.ids, st.neighbors.dists, st.rho, st.lam, st.delta, res.clustering.labels]
     for a, b in zip(out["0"], out["1"]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("switch,values", [("PK_TICKETS", ("0", "1")), ("PK_RING", ("0", "2")),
+                                           ("PK_PRUNE_F16", ("0", "1")), ("PK_PREFETCH", ("0", "1")),
+                                           ("PK_PREFETCH_ROWS", ("0", "1"))])
+def test_round2_switches_are_output_neutral(monkeypatch, switch, values):
+    """Round-2 scheduling / staging switches change how the work is
+    done, never its result: ticket assignment vs the static stride, the row ring of the
+    float kNN searches, the fp16 vs tf32 Gram of the tensor-core prune, the two prefetches.
+    A C5-shaped instance wide enough for the ring (d = 1024) with s >= 256 starts; the
+    graph, kNN rows, densities, dependent points and labels must be identical (the default
+    settings are compared with the oracle in test_parity_scale_gpu.py)."""
+    data, _ = workloads.generate("C5", n=70_000, components=55)
+    out = {}
+    for v in values:
+        monkeypatch.setenv(switch, v)
+        ps = pk.PointSet(data)
+        idx = pk.build_vamana(ps, R=32, L_build=128, alpha=1.1, seed=5, query_beam=128)
+        res = pk.run_pipeline(ps, pk.VamanaConfig(R=32, L_build=128, L=128, alpha=1.1, seed=5), k=16,
+                              density_kind="kth", center_policy=pk.ProductCenter(55),
+                              noise_policy=pk.NoisePolicy(0.0),
+                              doubling_params=pk.DoublingParams(initial_k=32, threshold=100))
+        st = res.state
+        out[v] = [idx.adjacency, idx.degrees, st.neighbors.ids, st.neighbors.dists, st.rho, st.lam, st.delta,
+                  res.clustering.labels]
+    for a, b in zip(out[values[0]], out[values[1]]):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
