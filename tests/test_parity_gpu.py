@@ -703,7 +703,7 @@ def test_round2_switches_are_output_neutral(monkeypatch, switch, values):
                               noise_policy=pk.NoisePolicy(0.0),
                               doubling_params=pk.DoublingParams(initial_k=32, threshold=100))
         st = res.state
-        out[v] = [idx.adjacency, idx.degrees, st.neighbors.ids, st.neighbors.dists, st.rho, st.lam, st.delta,
+        out[v] = [idx.graph.adjacency, idx.graph.degrees, st.neighbors.ids, st.neighbors.dists, st.rho, st.lam, st.delta,
                   res.clustering.labels]
     for a, b in zip(out[values[0]], out[values[1]]):
         assert np.array_equal(np.asarray(a), np.asarray(b))
