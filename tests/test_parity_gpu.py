@@ -300,11 +300,36 @@ def test_lazy_keys_equal_eager(monkeypatch, case):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("case", ["c5", "c4", "dup128", "wide"])
+@pytest.mark.parametrize("case", ["c5", "c4", "dup128", "wide", "huge", "tiny", "mixed"])
 def test_tensor_core_prune_equals_warp_prune(monkeypatch, case):
-    """Float data: RobustPrune decided from tcgen05 tf32 Gram tiles with a
-    rigorous error bound (uncertain pairs decided exactly) builds the same graph
-    as the warp-per-item screened prune (PK_TC_PRUNE=0)."""
+    """Float data: RobustPrune decided from tcgen05 Gram tiles (fp16 copy of the
+    rows; PK_PRUNE_F16=0: tf32) with a rigorous error bound (uncertain pairs
+    decided exactly) builds the same graph as the warp-per-item screened prune
+    (PK_TC_PRUNE=0) -- also where the fp16 bound does not hold or is loose:
+    coordinates past the fp16 range (non-finite accumulators), subnormal fp16
+    coordinates, rows of very different norms."""
+    if case in ("huge", "tiny", "mixed"):
+        rng = np.random.default_rng(21)
+        hubs = rng.normal(size=(12, 96))
+        lab = rng.integers(0, 12, 5_000)
+        data = hubs[lab] + 0.15 * rng.normal(size=(5_000, 96))
+        data[:40] = hubs[lab[:40]]
+        if case == "huge":
+            data[::7] *= 2.0e5   # fp16 overflow on every 7th row
+        elif case == "tiny":
+            data *= 1.0e-6       # fp16 subnormals
+        else:
+            data[::5] *= 300.0   # norms 300x apart: the bound |t||u| dwarfs the small rows' distances
+            data[1::5] *= 1.0e-3
+        data = data.astype(np.float32)
+        out = {}
+        for flag in ("0", "1"):
+            monkeypatch.setenv("PK_TC_PRUNE", flag)
+            g = pk.build_vamana(pk.PointSet(data), R=32, L_build=96, alpha=1.2, seed=2, query_beam=96)
+            out[flag] = (g.graph.adjacency.copy(), g.graph.degrees.copy())
+        assert np.array_equal(out["0"][1], out["1"][1])
+        assert np.array_equal(out["0"][0], out["1"][0])
+        return
     if case == "c5":
         data, _ = workloads.generate("C5", n=6_000, components=8)
     elif case == "c4":
