@@ -166,6 +166,10 @@ int pk_build_vamana_seeds(const float* x, int64_t n, int64_t dp, const uint32_t*
 typedef int64_t (*pk_exchange_fn)(void* ctx, int kind, int64_t a, int64_t b);
 #define PK_XCHG_OUTLISTS 0
 #define PK_XCHG_ROWS 1
+/* exchange(ctx, PK_XCHG_ORDER, n, 0): broadcast xids[0, n) from rank 0 (the
+ * search order inside the batches, float builds with the start pre-screen:
+ * every rank derives it from the same data, rank 0's copy is authoritative) */
+#define PK_XCHG_ORDER 2
 int pk_build_vamana_sharded(const float* x, int64_t n, int64_t dp, const uint32_t* x8, int64_t dw, int mode,
                             int64_t R, int64_t L, double alpha,
                             const int32_t* starts, int64_t s, const int32_t* order, int32_t* adj_out,

@@ -1513,9 +1513,10 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
         s >= env_int("PK_SEED_TC_MIN", 256) && s <= 8192 && env_int("PK_SEED_TC", 1) == 1 && tc_supported()) {
         const int mw = (s + 31) / 32;
         PK_CHECK(scratch(&seed_mask, (size_t)n * mw, st));
-        // (one GPU only: ranks must agree on the chunk of every batch, and the order
-        // below is derived from floating-point screens)
-        if (env_int("PK_LOCALITY", 1) == 1 && !multi) PK_CHECK(scratch(&near, (size_t)n, st));
+        // (sharded builds: the ranks must agree on the chunks of every batch, and the
+        // order below is derived from floating-point screens, so rank 0's order is
+        // broadcast -- PK_XCHG_ORDER, below)
+        if (env_int("PK_LOCALITY", 1) == 1 && (!multi || R >= 4)) PK_CHECK(scratch(&near, (size_t)n, st));
         if ((rc = tc_seed_mask(D.X, n, D.dp, starts, s, std::min(L, s), seed_mask, mw, near, st))) return rc;
         A.P.seed_mask = seed_mask;
         A.P.seed_mw = mw;
@@ -1529,6 +1530,17 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     int* lorder = nullptr;
     if (near && n >= (1 << 16) && s <= (1 << 20)) {
         if ((rc = locality_order(order, n, near, s, &lorder, st))) return rc;
+        if (multi) {
+            // every rank computed the same keys from the same data with the same kernels;
+            // rank 0's order is made authoritative anyway (xids holds >= n ints, R >= 4)
+            PK_CHECK(cudaMemcpyAsync(SH.xids, lorder, sizeof(int) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+            PK_CHECK(cudaStreamSynchronize(st));
+            if (SH.fn(SH.ctx, PK_XCHG_ORDER, n, 0) < 0) {
+                set_error("search-order broadcast failed");
+                return 4;
+            }
+            PK_CHECK(cudaMemcpyAsync(lorder, SH.xids, sizeof(int) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+        }
         order = lorder;
     }
     // u8 rows of d = 128: the exact start distances of every point from one

@@ -157,6 +157,16 @@ class Comm:
         else:
             dist.all_reduce(t, op=rop, group=self.group)
 
+    def broadcast(self, t: torch.Tensor, src: int = 0) -> None:
+        if self.world == 1:
+            return
+        if self._host_staged(t):
+            h = t.cpu()
+            dist.broadcast(h, src=src, group=self.group)
+            t.copy_(h)
+        else:
+            dist.broadcast(t, src=src, group=self.group)
+
     def max_time(self, ms: float, device) -> float:
         t = torch.tensor([ms], dtype=torch.float64, device=device)
         self.all_reduce(t, "max")
@@ -177,12 +187,14 @@ class BuildExchange:
     kind PK_XCHG_OUTLISTS (a = chunk): all-gather xids[0, world*a*R) and
     xlen[0, world*a) in place.  kind PK_XCHG_ROWS (a = own record count):
     gather the counts into xcnt and the records xsend[0, maxc*(R+2)) into
-    xrecv; returns maxc.  Errors are kept in `.error` and reported to the C
+    xrecv; returns maxc.  kind PK_XCHG_ORDER (a = n): broadcast xids[0, n) from
+    rank 0.  Errors are kept in `.error` and reported to the C
     side as -1 (the build then fails with a status instead of raising through
     the C frame)."""
 
     OUTLISTS = 0
     ROWS = 1
+    ORDER = 2  # a = n: broadcast xids[0, n) from rank 0 (search order inside the batches)
 
     def __init__(self, comm: Comm, n: int, R: int, device):
         self.comm = comm
@@ -196,7 +208,7 @@ class BuildExchange:
         self.xrecv = torch.empty(w * U * (R + 2), dtype=torch.int32, device=device)
         self.xcnt = torch.zeros(w, dtype=torch.int32, device=device)
         self.error = None
-        self.calls = {self.OUTLISTS: 0, self.ROWS: 0}
+        self.calls = {self.OUTLISTS: 0, self.ROWS: 0, self.ORDER: 0}
         self.callback = _lib.EXCHANGE_FN(self._exchange)
 
     def _exchange(self, ctx, kind, a, b):
@@ -210,6 +222,9 @@ class BuildExchange:
         if kind not in self.calls:
             raise ValueError(f"unknown exchange kind {kind}")
         self.calls[kind] += 1
+        if kind == self.ORDER:
+            self.comm.broadcast(self.xids[:a], src=0)
+            return 0
         if kind == self.OUTLISTS:
             self.comm.all_gather_chunks(self.xids, a * self.R)
             self.comm.all_gather_chunks(self.xlen, a)

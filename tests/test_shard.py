@@ -231,18 +231,31 @@ def test_sharded_build_single_rank_matches_plain_build():
     assert torch.equal(adj, a0) and torch.equal(deg, d0)
 
 
-def _pipeline_digest(comm):
-    """Sharded pipeline on this rank; returns digests of every output array."""
+def _pipeline_digest(comm, case="c1"):
+    """Sharded pipeline on this rank; returns digests of every output array.
+    case "c5": a C5-shaped instance large enough for the tensor-core start
+    pre-screen and the locality order of the build batches (rank 0's order is
+    broadcast: PK_XCHG_ORDER), sharded batches of >= 2,048 points."""
     import hashlib
 
     import paper_2312_03940_b200 as pk
-    from paper_2312_03940_b200 import workloads
+    from paper_2312_03940_b200 import _lib, workloads
     from paper_2312_03940_b200.cluster import run_pipeline_device
 
     torch.cuda.set_device(0)
-    data, _ = workloads.generate("C1", n=6000, components=10)
-    kw = workloads.pipeline_args("C1", pk, n_centers=10)
+    if case == "c5":
+        data, _ = workloads.generate("C5", n=70_000, components=55)
+        kw = workloads.pipeline_args("C5", pk, n_centers=55)
+    else:
+        data, _ = workloads.generate("C1", n=6000, components=10)
+        kw = workloads.pipeline_args("C1", pk, n_centers=10)
+    _lib.prof_collect(reset=True)
+    _lib.prof_only([])
+    _lib.prof_enable(True)
     out = run_pipeline_device(pk.PointSet(data), **kw, comm=comm)
+    torch.cuda.synchronize()
+    _lib.prof_enable(False)
+    ran_locality = "locality_keys_kernel" in _lib.prof_collect(reset=True)
     adj, deg = out["index"].graph.device_arrays()[:2]
     ids, dists = out["ids"], out["dists"]
     if comm is not None:  # each rank holds only its own rows
@@ -252,13 +265,14 @@ def _pipeline_digest(comm):
     for name, t in (("adj", adj), ("deg", deg), ("ids", ids), ("dists", dists), ("rho", out["rho"]),
                     ("lam", out["lam"]), ("delta", out["delta"]), ("labels", out["labels"])):
         h[name] = hashlib.sha256(t.detach().cpu().numpy().tobytes()).hexdigest()
+    h["locality_order_ran"] = ran_locality
     return h
 
 
-def _pipeline_worker(rank, world, port, q):
+def _pipeline_worker(rank, world, port, q, case="c1"):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
-        q.put((rank, _pipeline_digest(shard.Comm())))
+        q.put((rank, _pipeline_digest(shard.Comm(), case)))
     except Exception:  # noqa: BLE001
         import traceback
 
@@ -268,15 +282,17 @@ def _pipeline_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_sharded_pipeline_matches_single_gpu():
+@pytest.mark.parametrize("case", ["c1", "c5"])
+def test_sharded_pipeline_matches_single_gpu(case):
     """Functional check of the split (not a measurement): two ranks sharing
     one device, host (gloo) collectives, must reproduce the single-process
     graph, kNN rows, densities, dependents and labels bit for bit."""
-    ref = _pipeline_digest(None)
+    ref = _pipeline_digest(None, case)
+    assert ref["locality_order_ran"] == (case == "c5")
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_pipeline_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, 2, port, q, case)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
