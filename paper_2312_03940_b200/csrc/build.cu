@@ -1259,7 +1259,7 @@ int config_kernel(K kern, size_t warp_bytes, int want_wpb, int* wpb_out, int* gr
 // tc_knn.cu: tensor-core screens of all points against the start set
 bool tc_supported();
 int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int take, unsigned* mask, int mw,
-                 int* near, cudaStream_t st);
+                 int* near, cudaStream_t st, const long long* rows_ids = nullptr);
 // scan.cu: exact u8 distances of every point to every start on the integer tensor cores
 int u8_seed_table(const unsigned* x8, int n, const int* starts, int s, unsigned* tab, cudaStream_t st);
 

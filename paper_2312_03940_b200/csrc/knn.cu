@@ -404,6 +404,56 @@ int query_locality_order(const SearchParams& P, const long long* qids, int m, in
     return 0;
 }
 
+// tc_knn.cu
+bool tc_supported();
+int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int take, unsigned* mask, int mw,
+                 int* near, cudaStream_t st, const long long* rows_ids);
+
+__global__ void near_keys_kernel(const int* near, int m, unsigned* keys, int* vals) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
+        keys[t] = (unsigned)near[t];
+        vals[t] = t;
+    }
+}
+
+// The same order for member queries that have no seeded beams (a graph loaded from
+// disk, L != L_build, the ranks of a sharded run): the nearest start of every query
+// from one tensor-core screen of the queries against the start rows (the build's
+// tc_seed_mask; only its `near` output is used here).  Float data with >= 256 starts.
+int near_locality_order(const SearchParams& P, const long long* qids, int m, int** ord, cudaStream_t st) {
+    const int mw = (P.s + 31) / 32;
+    int* near = nullptr;
+    unsigned* mask = nullptr;
+    PK_CHECK(scratch(&near, (size_t)m, st));
+    PK_CHECK(scratch(&mask, (size_t)m * mw, st));
+    int rc = tc_seed_mask(P.X, m, P.dp, P.starts, P.s, 1, mask, mw, near, st, qids);
+    release(mask, st);
+    if (rc) return rc;
+    int bits = 1;
+    while ((1 << bits) < P.s) ++bits;
+    unsigned *k0 = nullptr, *k1 = nullptr;
+    int* v0 = nullptr;
+    PK_CHECK(scratch(&k0, (size_t)m, st));
+    PK_CHECK(scratch(&k1, (size_t)m, st));
+    PK_CHECK(scratch(&v0, (size_t)m, st));
+    PK_CHECK(scratch(ord, (size_t)m, st));
+    {
+        ProfScope _ps("near_keys_kernel", st);
+        near_keys_kernel<<<grid_for(m, 256), 256, 0, st>>>(near, m, k0, v0);
+    }
+    PK_CHECK_LAUNCH("near_keys_kernel");
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0, k1, v0, *ord, m, 0, bits, st);
+    void* tmp = nullptr;
+    PK_CHECK(cudaMallocAsync(&tmp, bytes + 16, st));
+    {
+        ProfScope _ps("cub_DeviceRadixSort_SortPairs", st);
+        PK_CHECK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0, k1, v0, *ord, m, 0, bits, st));
+    }
+    for (void* p : {(void*)near, (void*)k0, (void*)k1, (void*)v0, tmp}) release(p, st);
+    return 0;
+}
+
 template <int MODE, int QV>
 int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, int kk, int H,
                     long long* out_ids, double* out_d, long long* counts, long long* evals, cudaStream_t st) {
@@ -466,6 +516,10 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     int* ord = nullptr;
     if (P.seed_load && m >= (1 << 16) && env_int("PK_LOCALITY", 1) == 1) {
         const int rc = query_locality_order(P, qids, m, L, P.n_points, &ord, st);
+        if (rc) return rc;
+    } else if (MODE == MODE_SEQ64 && QV <= 8 && P.dp <= 128 * QV && P.screen && m >= (1 << 16) && P.s >= 256 &&
+               P.s <= 8192 && tc_supported() && env_int("PK_LOCALITY", 1) == 1) {
+        const int rc = near_locality_order(P, qids, m, &ord, st);
         if (rc) return rc;
     }
     // counting mode (bench.py's untimed pass): exact number of distinct ids

@@ -688,8 +688,10 @@ __global__ void seed_mask_kernel(const float* __restrict__ dump, long long ld, i
 // rows on the tcgen05 kernel (fp16 operands, fp32 TMEM accumulation, every
 // distance dumped), each chunk reduced to its bits by seed_mask_kernel.  Used by
 // beam.cuh seed_select_lazy to skip the fp32 screens of far starts.
+// `rows` (optional): the screened points are x[rows[0 .. n)] instead of x[0 .. n)
+// (mask and near are indexed by position either way).
 int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int take, unsigned* mask, int mw,
-                 int* near, cudaStream_t st) {
+                 int* near, cudaStream_t st, const long long* rows_ids) {
     if (!tc_supported()) {
         set_error("tensor-core screens need an sm_100 device");
         return 2;
@@ -740,7 +742,7 @@ int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int ta
         const int rows = std::min(chunk, n - r0);
         {
             ProfScope _ps("tc_prep_kernel", st);
-            tc_prep_kernel<<<(unsigned)std::min<long long>(((long long)(rows) + 7) / 8, 148ll * 32), 256, 0, st>>>(x + (size_t)r0 * dp, dp, nullptr, rows, kp, qh, qn);
+            tc_prep_kernel<<<(unsigned)std::min<long long>(((long long)(rows) + 7) / 8, 148ll * 32), 256, 0, st>>>(rows_ids ? x : x + (size_t)r0 * dp, dp, rows_ids ? rows_ids + r0 : nullptr, rows, kp, qh, qn);
         }
         if ((rc = make_map(&mq, qh, rows, kp, TC_BM))) return rc;
         TcArgs A;
