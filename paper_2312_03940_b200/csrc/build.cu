@@ -1263,6 +1263,27 @@ int tc_seed_mask(const float* x, int n, int dp, const int* starts, int s, int ta
 // scan.cu: exact u8 distances of every point to every start on the integer tensor cores
 int u8_seed_table(const unsigned* x8, int n, const int* starts, int s, unsigned* tab, cudaStream_t st);
 
+// nearest start of every point from the u8 start-distance table (ties: lowest index)
+__global__ void argmin_rows_kernel(const unsigned* __restrict__ tab, int n, int s, int* __restrict__ near) {
+    const int lane = lane_id();
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = w; r < n; r += nw) {
+        const unsigned* row = tab + (size_t)r * s;
+        unsigned long long best = ~0ull;
+        for (int j = lane; j < s; j += 32) {
+            const unsigned long long k = ((unsigned long long)__ldg(row + j) << 32) | (unsigned)j;
+            best = k < best ? k : best;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long ob = __shfl_xor_sync(PK_FULL, best, o);
+            best = ob < best ? ob : best;
+        }
+        if (lane == 0) near[r] = (int)(best & 0xffffffffull);
+    }
+}
+
 // ---- locality order of the batches' points ------------------------------------
 // key of position i of the insertion order: (batch of i, nearest start of the
 // point); batches are [2^b - 1, 2^(b+1) - 1), so the batch is floor(log2(i + 1))
@@ -1527,6 +1548,23 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
     // any order without changing the graph.  Grouped by their nearest start,
     // the warps running at the same time walk the same region of the data and
     // share its rows in L2 instead of each pulling its own from HBM.
+    // u8 rows of d = 128: the exact start distances of every point from one
+    // integer tensor-core pass (beam.cuh seed_select reads them); the nearest start
+    // of every point falls out of the table (the locality key of the u8 builds)
+    unsigned* seed_tab = nullptr;
+    if (MODE == MODE_EXACT_U8 && D.dw == 32 && D.X8 && A.P.seed_select && !ubm && L >= 128 &&
+        (L & (L - 1)) == 0 && s > 32 && (long long)n * s <= (1ll << 31) && env_int("PK_SEED_TAB", 1) == 1) {
+        PK_CHECK(scratch(&seed_tab, (size_t)n * s, st));
+        if ((rc = u8_seed_table(D.X8, n, starts, s, seed_tab, st))) return rc;
+        A.P.seed_tab = seed_tab;
+        if (!near && env_int("PK_LOCALITY", 1) == 1 && env_int("PK_LOCALITY_U8", 1) == 1 && n >= (1 << 16) &&
+            (!multi || R >= 4)) {
+            PK_CHECK(scratch(&near, (size_t)n, st));
+            ProfScope _ps("argmin_rows_kernel", st);
+            argmin_rows_kernel<<<sm_count() * 8, 256, 0, st>>>(seed_tab, n, s, near);
+        }
+        PK_CHECK_LAUNCH("argmin_rows_kernel");
+    }
     int* lorder = nullptr;
     if (near && n >= (1 << 16) && s <= (1 << 20)) {
         if ((rc = locality_order(order, n, near, s, &lorder, st))) return rc;
@@ -1542,15 +1580,6 @@ int run_build(const DataRef& D, int n, int R, int L, double alpha, const int* st
             PK_CHECK(cudaMemcpyAsync(lorder, SH.xids, sizeof(int) * (size_t)n, cudaMemcpyDeviceToDevice, st));
         }
         order = lorder;
-    }
-    // u8 rows of d = 128: the exact start distances of every point from one
-    // integer tensor-core pass (beam.cuh seed_select reads them)
-    unsigned* seed_tab = nullptr;
-    if (MODE == MODE_EXACT_U8 && D.dw == 32 && D.X8 && A.P.seed_select && !ubm && L >= 128 &&
-        (L & (L - 1)) == 0 && s > 32 && (long long)n * s <= (1ll << 31) && env_int("PK_SEED_TAB", 1) == 1) {
-        PK_CHECK(scratch(&seed_tab, (size_t)n * s, st));
-        if ((rc = u8_seed_table(D.X8, n, starts, s, seed_tab, st))) return rc;
-        A.P.seed_tab = seed_tab;
     }
     A.D = D;
     A.L = L;

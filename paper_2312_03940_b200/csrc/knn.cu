@@ -419,7 +419,8 @@ __global__ void near_keys_kernel(const int* near, int m, unsigned* keys, int* va
 // The same order for member queries that have no seeded beams (a graph loaded from
 // disk, L != L_build, the ranks of a sharded run): the nearest start of every query
 // from one tensor-core screen of the queries against the start rows (the build's
-// tc_seed_mask; only its `near` output is used here).  Float data with >= 256 starts.
+// tc_seed_mask; only its `near` output is used here, an order key, so integer
+// data takes the same fp16 screen).  Rows of <= 1,024 coordinates, >= 256 starts.
 int near_locality_order(const SearchParams& P, const long long* qids, int m, int** ord, cudaStream_t st) {
     const int mw = (P.s + 31) / 32;
     int* near = nullptr;
@@ -517,8 +518,8 @@ int launch_beam_knn(const SearchParams& P, const long long* qids, int m, int L, 
     if (P.seed_load && m >= (1 << 16) && env_int("PK_LOCALITY", 1) == 1) {
         const int rc = query_locality_order(P, qids, m, L, P.n_points, &ord, st);
         if (rc) return rc;
-    } else if (MODE == MODE_SEQ64 && QV <= 8 && P.dp <= 128 * QV && P.screen && m >= (1 << 16) && P.s >= 256 &&
-               P.s <= 8192 && tc_supported() && env_int("PK_LOCALITY", 1) == 1) {
+    } else if (P.X && P.dp <= 1024 && m >= (1 << 16) && P.s >= 256 && P.s <= 8192 && tc_supported() &&
+               env_int("PK_LOCALITY", 1) == 1) {
         const int rc = near_locality_order(P, qids, m, &ord, st);
         if (rc) return rc;
     }
