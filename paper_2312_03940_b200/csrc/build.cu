@@ -618,25 +618,34 @@ __device__ __forceinline__ unsigned bp_dist_global(const uint4 (&q)[8], unsigned
     return nq + (n0 + n1) - 2u * (d0 + d1);
 }
 
-// block bitonic sort of (kd, ki)[0, P) by (dist, id); P a power of two
+// block bitonic sort of (kd, ki)[0, P) by (dist, id); P a power of two.  One
+// compare-exchange per thread and stage (thread -> pair, nobody idles), and a
+// block barrier only around the stages that cross a warp's own 64 elements: pair
+// p = tid + 128 it lies in elements [64 (p >> 5), 64 (p >> 5) + 64) whenever
+// j <= 32, and a warp owns the same pair blocks in every stage, so consecutive
+// stages with j <= 32 only need the warp in step (3 block barriers at P = 256
+// instead of 36).  Callers enter and leave through a block barrier.
 __device__ __forceinline__ void bp_sort(double* kd, unsigned* ki, int P) {
+    const int half = P >> 1;
     for (int k = 2; k <= P; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P; i += BP_THREADS) {
-                const int x = i ^ j;
-                if (x > i) {
-                    const double a = kd[i], b = kd[x];
-                    const unsigned ia = ki[i], ib = ki[x];
-                    if (key_lt(b, ib, a, ia) == ((i & k) == 0)) {
-                        kd[i] = b;
-                        kd[x] = a;
-                        ki[i] = ib;
-                        ki[x] = ia;
-                    }
+            for (int p = threadIdx.x; p < half; p += BP_THREADS) {
+                const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+                const int x = i | j;
+                const double a = kd[i], b = kd[x];
+                const unsigned ia = ki[i], ib = ki[x];
+                if (key_lt(b, ib, a, ia) == ((i & k) == 0)) {
+                    kd[i] = b;
+                    kd[x] = a;
+                    ki[i] = ib;
+                    ki[x] = ia;
                 }
             }
-            __syncthreads();
+            const int jn = j > 1 ? (j >> 1) : k;  // the next stage's j (k: first stage of the next k)
+            if (j >= 64 || jn >= 64) __syncthreads();
+            else __syncwarp();
         }
+    __syncthreads();
 }
 
 // Reverse groups: kd/ki[0, nd) is the target's current row -- every adjacency
